@@ -1,0 +1,192 @@
+/*
+ * sgns.c -- oracle (TEST INFRASTRUCTURE ONLY): embedding initialisation (O9),
+ * the SGNS update of Alg. 1 (O10) and the 2D-partitioned epoch (O7, O11).
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include "ne_oracle.h"
+
+/* O9: vertex rows U(-0.5/d, 0.5/d), context rows 0 (reading D11; the paper
+ * keeps GraphVite's "embedding initialization method").
+ * V[i][c] = ((float)(x[c&3] >> 8) * 2^-24 - 0.5f) / (float)d with
+ * x = Philox(ctr = (i_lo, i_hi, c>>2, INIT<<24)).  Every step is exact except
+ * the final correctly-rounded division.  V points at row row_begin. */
+void or_init_vertex(float *V, uint64_t row_begin, uint64_t row_end, uint32_t d, uint64_t seed)
+{
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint64_t i;
+    for (i = row_begin; i < row_end; ++i) {
+        uint32_t c, ctr[4], x[4];
+        for (c = 0; c < d; ++c) {
+            float u;
+            if ((c & 3) == 0) {
+                ctr[0] = (uint32_t)i; ctr[1] = (uint32_t)(i >> 32);
+                ctr[2] = c >> 2; ctr[3] = (uint32_t)OR_TAG_INIT << 24;
+                or_philox4x32_10(ctr, key, x);
+            }
+            u = (float)(x[c & 3] >> 8) * 0x1p-24f;
+            V[(i - row_begin) * d + c] = (u - 0.5f) / (float)d;
+        }
+    }
+}
+
+/* The logistic function, input clamped to [-30, 30]. */
+double or_sigmoid(double x)
+{
+    if (x > 30.0) x = 30.0;
+    if (x < -30.0) x = -30.0;
+    return 1.0 / (1.0 + exp(-x));
+}
+
+/* Gradient of the per-pair logistic loss
+ *   L(v, c) = -y log s(v.c) - (1-y) log(1 - s(v.c))
+ * with respect to v and c: dL/dv = (s - y) c, dL/dc = (s - y) v.
+ * The dot product is accumulated in index order in fp64 ("computing the
+ * dot product of vertex[u] and context[v]"). */
+void or_sgns_grad(const double *v, const double *c, uint32_t d, int label,
+                  double *gv, double *gc, double *loss)
+{
+    double x = 0.0, s, g;
+    uint32_t i;
+    for (i = 0; i < d; ++i) x += v[i] * c[i];
+    s = or_sigmoid(x);
+    g = s - (double)label;
+    for (i = 0; i < d; ++i) { gv[i] = g * c[i]; gc[i] = g * v[i]; }
+    if (loss) *loss = label ? -log(s) : -log(1.0 - s);
+}
+
+/* O10: one Train(Emb_vertex(v), Emb_context(u), label) of Alg. 1
+ * with "a standard SGD": (v, c) <- (v - lr*dL/dv, c - lr*dL/dc), both
+ * gradients taken at the pre-update values.  Rows are stored in
+ * fp32 and rounded once per update.  Returns the loss term. */
+double or_sgns_step(float *v, float *c, uint32_t d, int label, float lr)
+{
+    double vd[d], cd[d], gv[d], gc[d]; /* C99 VLAs; d <= 4096 is checked by callers */
+    double loss = 0.0, eta = (double)lr;
+    uint32_t i;
+    for (i = 0; i < d; ++i) { vd[i] = (double)v[i]; cd[i] = (double)c[i]; }
+    or_sgns_grad(vd, cd, d, label, gv, gc, &loss);
+    for (i = 0; i < d; ++i) {
+        v[i] = (float)(vd[i] - eta * gv[i]);
+        c[i] = (float)(cd[i] - eta * gc[i]);
+    }
+    return loss;
+}
+
+/* Alg. 1 lines 8-12 for one positive sample (src, dst): the positive update
+ * (P:75), then one update per negative in draw order (reading D2).
+ * The vertex row carries over between the 1+K updates; a repeated context id
+ * sees its earlier update because rows are updated in place. */
+double or_train_sample(float *V, float *C, uint32_t d, uint32_t src, uint32_t dst,
+                       const uint32_t *negs, uint32_t K, float lr)
+{
+    float *v = V + (size_t)src * d;
+    double loss = or_sgns_step(v, C + (size_t)dst * d, d, 1, lr);
+    uint32_t j;
+    for (j = 0; j < K; ++j) loss += or_sgns_step(v, C + (size_t)negs[j] * d, d, 0, lr);
+    return loss;
+}
+
+/* Alias tables of every context part (O3), part-local ids, stored at the
+ * global row index of each part's first row. */
+int or_build_alias_tables(const or_config *cfg, uint64_t n, const uint64_t *offsets,
+                          uint32_t *thr, uint32_t *alias)
+{
+    uint64_t bounds[257], i;
+    uint64_t *deg = (uint64_t *)malloc((n ? n : 1) * sizeof(uint64_t));
+    uint32_t j;
+    if (!deg || cfg->parts == 0 || cfg->parts > 256) { free(deg); return -1; }
+    for (i = 0; i < n; ++i) deg[i] = offsets[i + 1] - offsets[i]; /* O2 */
+    or_partition_bounds(0, n, cfg->parts, bounds);
+    for (j = 0; j < cfg->parts; ++j) {
+        uint64_t b = bounds[j], e = bounds[j + 1];
+        if (e > b && or_alias_build(deg + b, e - b, thr + b, alias + b) != 0) { free(deg); return -1; }
+    }
+    free(deg);
+    return 0;
+}
+
+/* O7: the vertex sub-part context part g trains at round r, slot t.  Ring of
+ * after each block a GPU sends its sub-part to g+1 and
+ * receives from g-1, so at round r it holds vertex part (g - r) mod P, and
+ * sub-part slot t of it ("split vertex embeddings on one GPU into k
+ * sub-parts").  Returns vsub = part*k + t. */
+uint32_t or_plan_vsub(uint32_t P, uint32_t k, uint32_t r, uint32_t t, uint32_t g)
+{
+    return ((g + P - (r % P)) % P) * k + t;
+}
+
+/* O7 + O11: episodes [episode_begin, episode_end) of one epoch.  Per episode:
+ * build the pool (O4-O6), then replay the hierarchical plan:
+ *   for round r in 0..P-1, slot t in 0..k-1, context part g in 0..P-1:
+ *       train block (vertex sub-part ((g - r) mod P)*k + t, context part g)
+ * Blocks of one (r, t) step touch disjoint rows ("orthogonal vertex
+ * usage"), so the order over g is immaterial; reverse_within_step = 1 replays
+ * it backwards to let a test check exactly that.  thr/alias come from
+ * or_build_alias_tables.  Returns 0, or -1 on a bad configuration. */
+int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offsets,
+                          const uint32_t *targets, const uint32_t *thr, const uint32_t *alias,
+                          uint32_t epoch, float lr, uint32_t episode_begin, uint32_t episode_end,
+                          int reverse_within_step, float *V, float *C, or_stats *stats)
+{
+    uint32_t P = cfg->parts, k = cfg->subparts, d = cfg->dim, K = cfg->negatives;
+    uint64_t nblocks = (uint64_t)P * k * P, bounds[257], nnz = offsets[n];
+    uint64_t *boff = NULL;
+    uint32_t *pairs = NULL, negs[256], e;
+    if (P == 0 || P > 256 || k == 0 || nblocks > 4096 || K > 256 || d == 0 || d > 4096 ||
+        cfg->episodes == 0 || cfg->episodes > 4096 || epoch >= (1u << 24))
+        return -1;
+    if (cfg->walk_len > 0 && (cfg->window == 0 || cfg->walks_per_node == 0)) return -1;
+    or_partition_bounds(0, n, P, bounds);
+    boff = (uint64_t *)malloc((nblocks + 1) * sizeof(uint64_t));
+    if (!boff) return -1;
+    for (e = episode_begin; e < episode_end; ++e) {
+        uint64_t u0, units = or_episode_units(cfg, n, nnz, e, &u0);
+        uint64_t Pw = cfg->walk_len == 0 ? 1 : or_pairs_per_walk(cfg->walk_len, cfg->window);
+        uint64_t cap = units * Pw;
+        int64_t cnt;
+        uint32_t r, t, gi;
+        pairs = (uint32_t *)malloc(2 * (cap ? cap : 1) * sizeof(uint32_t));
+        if (!pairs) { free(boff); return -1; }
+        cnt = or_build_episode(cfg, n, offsets, targets, epoch, e, pairs, cap, boff);
+        if (cnt < 0) { free(pairs); free(boff); return -1; }
+        for (r = 0; r < P; ++r)
+            for (t = 0; t < k; ++t)
+                for (gi = 0; gi < P; ++gi) {
+                    uint32_t g = reverse_within_step ? (P - 1 - gi) : gi;
+                    uint32_t s = or_plan_vsub(P, k, r, t, g);
+                    uint32_t B = s * P + g;
+                    uint64_t p, cb = bounds[g], cn = bounds[g + 1] - bounds[g];
+                    for (p = 0; p < boff[B + 1] - boff[B]; ++p) {
+                        const uint32_t *pr = pairs + 2 * (boff[B] + p);
+                        double loss;
+                        if (K > 0) or_negatives(cfg, thr + cb, alias + cb, cb, cn, epoch, e, B, p, negs);
+                        loss = or_train_sample(V, C, d, pr[0], pr[1], negs, K, lr);
+                        if (stats) { stats->samples += 1; stats->loss_sum += loss; }
+                    }
+                }
+        free(pairs);
+        pairs = NULL;
+    }
+    free(boff);
+    return 0;
+}
+
+/* Convenience wrapper: build the alias tables, then run the episodes. */
+int or_train_epoch(const or_config *cfg, uint64_t n, const uint64_t *offsets,
+                   const uint32_t *targets, uint32_t epoch, float lr,
+                   uint32_t episode_begin, uint32_t episode_end,
+                   int reverse_within_step, float *V, float *C, or_stats *stats)
+{
+    uint32_t *thr = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+    uint32_t *alias = (uint32_t *)malloc((n ? n : 1) * sizeof(uint32_t));
+    int rc;
+    if (!thr || !alias) { free(thr); free(alias); return -1; }
+    rc = or_build_alias_tables(cfg, n, offsets, thr, alias);
+    if (rc == 0)
+        rc = or_train_epoch_tables(cfg, n, offsets, targets, thr, alias, epoch, lr,
+                                   episode_begin, episode_end, reverse_within_step, V, C, stats);
+    free(thr); free(alias);
+    return rc;
+}
