@@ -1,0 +1,308 @@
+"""Benchmark: positive edge samples/s of the SGNS training path (BASELINE.json
+metric) on B200, one process per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3] [--impl reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+A step is one epoch of the whole hot path through the C ABI (ne_train_epoch):
+walk engine -> window augmentation -> Feistel order + 2D bucketing -> SGNS
+with K alias negatives, and at N > 1 the NCCL ring of vertex sub-parts.
+`value` = positive samples trained by all ranks / max-over-ranks device time
+(CUDA events on the library's compute stream), inputs resident in HBM.
+`e2e` = the same metric with the CSR copied from pinned host memory every step
+(ne_load_graph) and the step's loss read back (D2H).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "positive edge samples/sec at d=128, K=5 (1/2/4/8 B200); HBM GB/s vs peak"
+UNIT = "positive samples/s"
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+
+
+def alg_bytes_per_sample(d: int, K: int) -> int:
+    """pair (8 B) + K alias entries (8 B) + read and write of the
+    vertex row, the positive context row and K negative rows (8 d (2 + K))."""
+    return 8 + 8 * K + 8 * d * (2 + K)
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def workload_desc(name):
+    import synth
+    w = synth.CONFIGS[name]
+    return w, (f"{w.name} R-MAT (Graph500 a,b,c=.57,.19,.19) {w.n:,} nodes / {w.m:,} undirected edges "
+               f"(nnz {2 * w.m:,}), DeepWalk k={w.walk_len} l={w.window} w=1, d={w.dim}, K={w.negatives}")
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    w, desc = workload_desc(args.workload)
+    off, tgt = synth.workload_graph(args.workload)
+    n = len(off) - 1
+    E = args.ref_episodes
+    cfg = oracle.Config(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
+                        walks_per_node=1, episodes=E, subparts=4, parts=1, seed=42)
+    V = oracle.init_vertex(n, w.dim, 42)
+    Cm = np.zeros_like(V)
+    tables = oracle.build_alias_tables(cfg, off)
+    for s in range(args.warmup):
+        oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025, s, s + 1, tables=tables)
+    samples = 0
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        e = args.warmup + s
+        ns, _ = oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025, e, e + 1, tables=tables)
+        samples += ns
+    dt = time.perf_counter() - t0
+    value = samples / dt
+    sample = (f"episodes {args.warmup}..{args.warmup + args.steps - 1} of {E} of epoch 0 "
+              f"(~{n // E:,} walkers each, {samples:,} positive samples timed), full-size matrices")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64 arithmetic, f32 storage", "data": "synthetic",
+            "config": {"workload": desc, "impl": "oracle/ (plain C, single thread)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, off, tgt, w):
+    """The oracle timed on this host on a bounded sample of the same workload."""
+    import oracle
+    n = len(off) - 1
+    E = args.cpu_episodes
+    cfg = oracle.Config(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
+                        walks_per_node=1, episodes=E, subparts=4, parts=1, seed=42)
+    V = oracle.init_vertex(n, w.dim, 42)
+    Cm = np.zeros_like(V)
+    tables = oracle.build_alias_tables(cfg, off)
+    t0 = time.perf_counter()
+    ns, _ = oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025, 0, 1, tables=tables)
+    dt = time.perf_counter() - t0
+    return {"value": ns / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"episode 0 of {E} (~{n // E:,} walkers, {ns:,} positive samples: walk + pool + "
+                      f"SGNS) of epoch 0 on the full-size graph and matrices, {dt:.1f} s, single thread"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-episodes", type=int, default=384)
+    ap.add_argument("--ref-episodes", type=int, default=1536)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2005_13789_b200 import ne
+    from paper_2005_13789_b200.engine import Engine
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w, desc = workload_desc(args.workload)
+    off, tgt = synth.workload_graph(args.workload)
+    n = len(off) - 1
+    nccl_id = None
+    if world > 1:
+        obj = [ne.ne_get_nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.current_stream()
+    eng = Engine(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
+                 walks_per_node=1, episodes=1, subparts=4, deterministic=False, seed=42,
+                 device=local, rank=rank, world=world, nccl_id=nccl_id, torch_allocator=True,
+                 stream=stream.cuda_stream)
+    eng.load_graph(off, tgt)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for s in range(args.warmup):
+        eng.train_epoch(s, 0.025)
+    barrier()
+    stats = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for s in range(args.steps):
+            stats.append(eng.train_epoch(args.warmup + s, 0.025))
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    samples = sum(st["samples"] for st in stats)
+    ms_train = sum(st["ms_train"] for st in stats)
+    launches = sum(st["kernel_launches"] for st in stats)
+    train_launches = sum(st["train_launches"] for st in stats)
+    t = torch.tensor([ms, samples, ms_train, launches, sum(st["ms_walk"] for st in stats),
+                      sum(st["ms_build"] for st in stats), sum(st["ms_comm_wait"] for st in stats),
+                      train_launches], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    else:
+        tmax = tsum = t
+    ms_max = float(tmax[0])
+    samples_all = float(tsum[1])
+    value = samples_all / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (SGNS), this rank's launches
+    B = alg_bytes_per_sample(w.dim, w.negatives)
+    achieved = samples * B / (ms_train / 1e3) / 1e9 if ms_train > 0 else 0.0
+    peak, peak_src = hbm_peak()
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "sgns_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            tr = json.load(f).get(args.workload)
+        if tr:
+            traffic = tr.get("dram_bytes_per_launch")
+
+    # end-to-end through the public API with host buffers (pinned)
+    off_h = torch.from_numpy(off.view(np.int64)).pin_memory()
+    tgt_h = torch.from_numpy(tgt.view(np.int32)).pin_memory()
+    h2d = off.nbytes + tgt.nbytes
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_samples = 0
+    e0.record(stream)
+    for s in range(args.e2e_steps):
+        ne.ne_load_graph(eng.ctx, off_h, tgt_h)
+        st = eng.train_epoch(s, 0.025)  # loss_sum / samples read back (D2H) by the call
+        e_samples += st["samples"]
+    e1.record(stream)
+    barrier()
+    e_ms = torch.tensor([e0.elapsed_time(e1), e_samples], dtype=torch.float64, device="cuda")
+    if world > 1:
+        em = e_ms.clone()
+        dist.all_reduce(em, op=dist.ReduceOp.MAX)
+        es = e_ms.clone()
+        dist.all_reduce(es, op=dist.ReduceOp.SUM)
+        e_value = float(es[1]) / (float(em[0]) / 1e3)
+    else:
+        e_value = e_samples / (float(e_ms[0]) / 1e3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, off, tgt, w)
+    eng.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": desc, "step": "one epoch: walk + augment + order/bucket + SGNS (+ ring)",
+                       "samples_per_step": samples_all / args.steps, "episodes": 1, "subparts": 4,
+                       "mode": "hogwild", "parallelism": f"2D ring x{world}",
+                       "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * 4 / 1e9)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "ne::sgns_kernel<1>",
+                         "bytes_per_sample": B, "launches": train_launches,
+                         "avg_launch_ms": ms_train / max(train_launches, 1), "peak_source": peak_src},
+            "phases_ms_per_step": {"walk": float(tsum[4]) / world / args.steps,
+                                   "build": float(tsum[5]) / world / args.steps,
+                                   "train": float(tsum[2]) / world / args.steps,
+                                   "comm_wait": float(tsum[6]) / world / args.steps},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    # CSR validation flags + offsets ends (32 B), block offsets (5 x 8 B), loss (8 B)
+                    "d2h_bytes_per_step": 32 + 8 * (4 * world + 1) + 8},
+            "clocks": clk.summary(),
+            "gpu_launches": int(tsum[3]),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

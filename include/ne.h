@@ -1,0 +1,218 @@
+/*
+ * ne.h -- C ABI of the B200-native SGNS node-embedding training engine.
+ *
+ * Implements the hot path of Wei et al., "A Distributed Multi-GPU System for
+ * Large-Scale Node Embedding at Tencent" (arXiv 2005.13789): network
+ * augmentation by random walks (Alg. 1), SGNS SGD with K
+ * negatives per positive sample (Alg. 1 lines 8-12), applied block by
+ * block to 2D-partitioned vertex / context embedding matrices
+ * with vertex sub-parts rotating around a ring of GPUs.
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n; R#/O#/D# = the
+ * contract and readings listed in DESIGN.md.
+ *
+ * Conventions (every entry point):
+ *   - returns an NE_* status; no C++ exception crosses the ABI;
+ *   - ne_last_error(ctx) then holds one machine-parsable line
+ *     ("NE_EINVAL: offsets[17]=5 < offsets[16]=9"), cf. S:564;
+ *   - input arrays are BORROWED for the duration of the call (copied);
+ *     they may be host (pageable or pinned) or device pointers (UVA);
+ *   - output arrays are caller-owned; capacities are checked (NE_ERANGE);
+ *   - all device memory is owned by the ctx (allocated through the optional
+ *     allocator callbacks, else cudaMalloc) and released by ne_destroy;
+ *   - a ctx is bound to one CUDA device and one rank; it is NOT thread-safe;
+ *   - calls are host-synchronous with respect to their results: when a call
+ *     returns, every output it produced is complete.
+ * There is no CPU fallback: without a CUDA device ne_create fails (NE_ECUDA).
+ */
+#ifndef NE_H
+#define NE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NE_ABI_VERSION 1
+
+typedef struct ne_ctx ne_ctx;
+
+/* Status codes. */
+enum {
+    NE_OK = 0,
+    NE_EINVAL = -1,  /* bad argument or malformed graph (S:24 CSR invariants)      */
+    NE_ERANGE = -2,  /* size/capacity/id out of range, rows not owned by the rank   */
+    NE_ENOMEM = -3,  /* device allocation failed                                    */
+    NE_ESTATE = -4,  /* call out of order (train before load, export before build)  */
+    NE_ECUDA = -5,   /* CUDA runtime error (no device, launch failure, ...)         */
+    NE_ENCCL = -6,   /* NCCL error in the ring exchange                             */
+    NE_ESCHED = -7   /* schedule violation: a sample outside its 2D block   */
+};
+
+/* ne_train_epoch flags. */
+enum {
+    NE_REUSE_SAMPLES = 1u  /* train again on the pool built earlier instead of
+                              walking anew (walk reuse); needs episodes == 1 */
+};
+
+/* ne_get_embeddings / ne_set_embeddings: which matrix. */
+enum { NE_VERTEX = 0, NE_CONTEXT = 1 };
+
+/* Optional device allocator (e.g. PyTorch's caching allocator).  alloc returns
+ * a device pointer of at least `bytes` bytes on `device`, usable on `stream`,
+ * or NULL on failure.  free releases a pointer alloc returned. */
+typedef void *(*ne_alloc_fn)(size_t bytes, int device, void *stream, void *user);
+typedef void (*ne_free_fn)(void *ptr, size_t bytes, int device, void *stream, void *user);
+
+/* Training configuration (SPEC RunConfig).  Limits are checked by
+ * ne_create (NE_EINVAL): dim % 4 == 0 and 4 <= dim <= 512; negatives <= 8;
+ * walk_len <= 255 (0 selects LINE mode: the pool is the CSR edge list);
+ * 1 <= window <= walk_len when walk_len > 0; walks_per_node >= 1;
+ * 1 <= episodes <= 4095; 1 <= subparts and world*subparts*world <= 4096. */
+typedef struct {
+    uint32_t dim;            /* d, embedding dimension (tab:perf d = 96..128)     */
+    uint32_t negatives;      /* K negatives per positive sample (tab:perf K = 5)  */
+    uint32_t walk_len;       /* k walk steps ("walk distance"); 0 = LINE mode      */
+    uint32_t window;         /* l context length ("walk context length")          */
+    uint32_t walks_per_node; /* w walks started from every node (reading D5)            */
+    uint32_t episodes;       /* episodes per epoch ("fixed-size sample pool")     */
+    uint32_t subparts;       /* vertex sub-parts per GPU, the paper's k = 4    */
+    uint32_t deterministic;  /* 1: one warp per block in canonical order (parity mode);
+                                0: Hogwild production mode (lock-free warps)            */
+    uint32_t rows_per_warp;  /* Hogwild concurrency cap: at most min(vertex rows, context
+                                rows) / rows_per_warp warps train a block at once, so
+                                small blocks are not swamped by lost updates (0 = 64);
+                                blocks of large graphs fill the GPU regardless          */
+    uint32_t reserved;       /* must be 0                                               */
+    uint64_t seed;           /* Philox key (contract R1)                                */
+} ne_config;
+
+/* Per-call statistics (this rank).  Times are device time from CUDA events. */
+typedef struct {
+    uint64_t samples;        /* positive samples trained                               */
+    double   loss_sum;       /* sum over all 1+K updates of -log s / -log(1-s)         */
+    float    ms_walk;        /* walk kernel time                                       */
+    float    ms_build;       /* pair scatter + bucketing time                          */
+    float    ms_train;       /* sum of SGNS kernel durations                           */
+    float    ms_comm_wait;   /* time the compute stream waited for ring receives       */
+    uint32_t train_launches; /* SGNS kernel launches                                   */
+    uint32_t kernel_launches;/* every kernel this library launched during the call     */
+} ne_stats;
+
+/* Library ABI version (NE_ABI_VERSION). */
+int ne_version(void);
+
+/* Create a context on CUDA `device` (the caller has selected nothing; the
+ * library calls cudaSetDevice itself).  alloc/free may be NULL (cudaMalloc).
+ * Errors: NE_EINVAL (cfg limits above), NE_ECUDA (no device / not sm_100). */
+int ne_create(ne_ctx **out, const ne_config *cfg, int device,
+              ne_alloc_fn alloc, ne_free_fn free_fn, void *user);
+
+/* Use `stream` (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream)
+ * as the compute stream; NULL restores the context's own stream. */
+int ne_set_stream(ne_ctx *ctx, void *stream);
+
+/* NCCL bootstrap for the multi-GPU ring: rank 0 calls
+ * ne_get_nccl_id, the harness broadcasts the 128 bytes (torch.distributed),
+ * then every rank calls ne_init_dist before ne_load_graph.  world == 1 needs
+ * no id (id may be NULL); world > 1 with id == NULL makes a layout-only
+ * context (partitions, pool and negatives of `rank`, no training: NE_ESTATE).  Rank g owns context part g and vertex part g
+ * (contiguous ranges, reading D12; "fix the context embeddings for each
+ * GPU").  Errors: NE_EINVAL, NE_ESTATE (graph already loaded), NE_ENCCL. */
+int ne_get_nccl_id(uint8_t id[128]);
+int ne_init_dist(ne_ctx *ctx, int rank, int world, const uint8_t id[128]);
+
+/* Load the graph G = (V, E) as CSR: offsets[n+1] (u64),
+ * targets[nnz] (u32), validated on the device against S:24 (offsets
+ * monotone, offsets[0] == 0, offsets[n] == nnz, every target < n); the copy is
+ * resident in HBM on every rank.  Also builds this rank's alias table
+ * (deg^0.75 over its context part, O3/D9) and initialises the embeddings
+ * (O9: vertex U(-0.5/d, 0.5/d), context 0).  May be called again to replace
+ * the graph (re-initialises).  Errors: NE_EINVAL (+ first offending index),
+ * NE_ERANGE (n >= 2^32 - 1 or n < world), NE_ENOMEM, NE_ECUDA. */
+int ne_load_graph(ne_ctx *ctx, uint32_t n, uint64_t nnz,
+                  const uint64_t *offsets, const uint32_t *targets);
+
+/* Walk engine, one episode (Alg. 1 "parallel random walk"; O4):
+ * walkers omega of the episode's contiguous range, start = omega mod n, k
+ * steps, Philox(ctr = (omega, t, WALK|epoch)) per step, stop at a node
+ * without out-edges.  Kept on the device; if host_walks != NULL also copied
+ * out as [walkers][walk_len+1] u32, 0xFFFFFFFF after the walk's end
+ * (cap_u32 = capacity in u32).  walkers_out (nullable) receives the count.
+ * Errors: NE_ESTATE (no graph; LINE mode), NE_ERANGE (episode, epoch >= 2^24,
+ * capacity). */
+int ne_random_walk(ne_ctx *ctx, uint32_t epoch, uint32_t episode,
+                   uint32_t *host_walks, size_t cap_u32, uint64_t *walkers_out);
+
+/* Network augmentation + sample pool of the episode (
+ * O5/O6): window pairs (path[i], path[i+delta]), 1 <= delta <= l, of the walks
+ * ne_random_walk produced (LINE mode: the CSR edges of the episode), keeping
+ * those whose context node lies in this rank's context part, ordered by the
+ * Feistel permutation pi of their generation index and grouped by vertex
+ * sub-part (2D block).  n_samples_out (nullable) = pool size.
+ * Errors: NE_ESTATE (walks missing / of another episode), NE_ERANGE. */
+int ne_build_samples(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint64_t *n_samples_out);
+
+/* Train the pool built by ne_build_samples for (epoch, episode) with learning
+ * rate lr, following the ring plan (O7): for round r, slot t, this rank trains
+ * block (vertex sub-part ((rank - r) mod world)*subparts + t, context part
+ * rank), then sends that sub-part to rank+1 and receives the next from
+ * rank-1.  Each positive sample (u, v) gets K alias negatives (O8) and
+ * 1+K sequential SGNS updates (O10).  stats may be NULL.
+ * Errors: NE_ESTATE, NE_ENCCL, NE_ECUDA, NE_ESCHED (debug builds). */
+int ne_train_samples(ne_ctx *ctx, uint32_t epoch, uint32_t episode, float lr, ne_stats *stats);
+
+/* One epoch ("one epoch goes over all the sampled edges"): for every
+ * episode, walk + build + train.  flags: NE_REUSE_SAMPLES.  lr is constant
+ * within the epoch (the caller may decay it between epochs).
+ * stats (nullable) accumulates the whole epoch. */
+int ne_train_epoch(ne_ctx *ctx, uint32_t epoch, float lr, uint32_t flags, ne_stats *stats);
+
+/* Copy rows [row_begin, row_end) of the vertex (which = NE_VERTEX) or context
+ * (NE_CONTEXT) matrix to host_out (row-major fp32, d floats per row;
+ * cap_floats = capacity).  The rows must lie in this rank's part (the vertex
+ * sub-parts are back home after every ne_train_samples).
+ * Errors: NE_ERANGE (rows not owned, capacity), NE_ESTATE. */
+int ne_get_embeddings(ne_ctx *ctx, int which, uint32_t row_begin, uint32_t row_end,
+                      float *host_out, size_t cap_floats);
+
+/* Overwrite rows [row_begin, row_end) of this rank's part (checkpoint resume,
+ * S:399; tests).  Same ownership rules as ne_get_embeddings. */
+int ne_set_embeddings(ne_ctx *ctx, int which, uint32_t row_begin, uint32_t row_end,
+                      const float *in);
+
+/* Last error message of ctx (never NULL; "" after success). */
+const char *ne_last_error(const ne_ctx *ctx);
+
+/* Release the context and all its device memory. */
+void ne_destroy(ne_ctx *ctx);
+
+/* ---- test hooks (bit-exact parity against the oracle) -------------------- */
+
+/* Copy the current pool's samples of local block `vsub` (vertex sub-part id,
+ * 0 <= vsub < world*subparts; the block is (vsub, this rank's context part))
+ * as (src, dst) u32 pairs in canonical order.  count receives the block size
+ * even when pairs_out is NULL.  Errors: NE_ESTATE, NE_ERANGE. */
+int ne_export_samples(ne_ctx *ctx, uint32_t vsub, uint32_t *pairs_out, size_t cap_pairs,
+                      uint64_t *count);
+
+/* Negatives of positions [pos_begin, pos_begin+count) of block (vsub, this
+ * rank's part) in (epoch, episode), computed by the same device function the
+ * SGNS kernel uses (O8); out = count*K u32 (global node ids). */
+int ne_export_negatives(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint32_t vsub,
+                        uint64_t pos_begin, uint64_t count, uint32_t *out);
+
+/* The host-side ring schedule (O7), no device needed: the vertex sub-part
+ * rank g trains at round r, slot t, with `world` ranks and `subparts` slots.
+ * Returns -1 on bad arguments. */
+int ne_plan_vsub(uint32_t world, uint32_t subparts, uint32_t r, uint32_t t, uint32_t g);
+
+/* Contiguous part bounds used by the library (reading D12): bounds[0..parts]
+ * of [0, n).  No device needed.  Returns NE_EINVAL if parts == 0. */
+int ne_partition_bounds(uint64_t n, uint32_t parts, uint64_t *bounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NE_H */

@@ -1,0 +1,104 @@
+// kernels_graph.cu -- CSR validation, embedding initialisation and the walk
+// engine (sm_100a).
+#include <algorithm>
+
+#include "ne_device.cuh"
+#include "ne_internal.h"
+
+namespace ne {
+
+static unsigned grid_for(uint64_t work, int threads, const Device& dev, int per_sm = 8) {
+    uint64_t blocks = (work + threads - 1) / threads;
+    uint64_t cap = (uint64_t)dev.sm_count * per_sm;
+    return (unsigned)std::max<uint64_t>(1, std::min(blocks, cap));
+}
+
+// offsets monotone and targets < n.  The first violation wins (atomicMin).
+__global__ void validate_csr_kernel(const uint64_t* __restrict__ off,
+                                    const uint32_t* __restrict__ tgt, uint64_t n, uint64_t nnz,
+                                    unsigned long long* bad) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        if (off[i + 1] < off[i]) atomicMin(&bad[0], (unsigned long long)i);
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += stride)
+        if (tgt[e] >= n) atomicMin(&bad[1], (unsigned long long)e);
+}
+
+cudaError_t launch_validate_csr(const uint64_t* off, const uint32_t* tgt, uint64_t n,
+                                uint64_t nnz, unsigned long long* bad, const Device& dev,
+                                cudaStream_t s) {
+    validate_csr_kernel<<<grid_for(std::max(n, nnz), 256, dev), 256, 0, s>>>(off, tgt, n, nnz, bad);
+    return cudaGetLastError();
+}
+
+// O9 (P:313 GraphVite's init, reading D11): V[i][c] = ((x[c&3] >> 8) * 2^-24 - 0.5) / d,
+// x = Philox((i_lo, i_hi, c/4, INIT<<24)).  IEEE division (no fast-math), so the
+// result is bit-identical to any correctly rounded implementation.
+__global__ void init_vertex_kernel(float* __restrict__ V, uint64_t row_begin, uint64_t rows,
+                                   uint32_t d, uint64_t seed) {
+    const uint32_t q = d / 4;
+    const uint64_t total = rows * q;
+    const uint2 key = key_of(seed);
+    const float fd = (float)d;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += stride) {
+        const uint64_t r = w / q;
+        const uint32_t c4 = (uint32_t)(w - r * q);
+        const uint64_t i = row_begin + r;
+        const uint4 x = philox(make_uint4((uint32_t)i, (uint32_t)(i >> 32), c4, kTagInit << 24), key);
+        float4 o;
+        o.x = __fdiv_rn(__fsub_rn(__fmul_rn((float)(x.x >> 8), 0x1p-24f), 0.5f), fd);
+        o.y = __fdiv_rn(__fsub_rn(__fmul_rn((float)(x.y >> 8), 0x1p-24f), 0.5f), fd);
+        o.z = __fdiv_rn(__fsub_rn(__fmul_rn((float)(x.z >> 8), 0x1p-24f), 0.5f), fd);
+        o.w = __fdiv_rn(__fsub_rn(__fmul_rn((float)(x.w >> 8), 0x1p-24f), 0.5f), fd);
+        reinterpret_cast<float4*>(V)[w] = o;
+    }
+}
+
+cudaError_t launch_init_vertex(float* V, uint64_t row_begin, uint64_t rows, uint32_t d,
+                               uint64_t seed, const Device& dev, cudaStream_t s) {
+    if (rows == 0) return cudaSuccess;
+    init_vertex_kernel<<<grid_for(rows * (d / 4), 256, dev), 256, 0, s>>>(V, row_begin, rows, d, seed);
+    return cudaGetLastError();
+}
+
+// O4 walk engine (Alg. 1 "parallel random walk"), one
+// lane per walker: the walk is a dependent chain (offsets -> target) so lanes
+// of a warp advance 32 independent walkers to keep loads in flight.  Step t
+// draws Philox(ctr = (omega_lo, omega_hi, t, WALK<<24 | epoch)) and picks
+// neighbour R2(x0|x1<<32, deg).  Rows are padded with kSentinel after a sink.
+__global__ void __launch_bounds__(256) walk_kernel(const uint64_t* __restrict__ off,
+                                                   const uint32_t* __restrict__ tgt, uint64_t n,
+                                                   uint64_t omega0, uint64_t count, uint32_t k,
+                                                   uint64_t seed, uint32_t epoch,
+                                                   uint32_t* __restrict__ walks) {
+    const uint2 key = key_of(seed);
+    const uint32_t tw = tag_word(kTagWalk, epoch);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < count; w += stride) {
+        const uint64_t omega = omega0 + w;
+        uint64_t cur = omega % n;
+        uint32_t* out = walks + w * (uint64_t)(k + 1);
+        out[0] = (uint32_t)cur;
+        uint32_t t = 1;
+        for (; t <= k; ++t) {
+            const uint64_t b = __ldg(off + cur), e = __ldg(off + cur + 1);
+            if (e == b) break;
+            const uint4 x = philox(make_uint4((uint32_t)omega, (uint32_t)(omega >> 32), t, tw), key);
+            cur = __ldg(tgt + b + uniform_index(x.x, x.y, e - b));
+            out[t] = (uint32_t)cur;
+        }
+        for (; t <= k; ++t) out[t] = kSentinel;
+    }
+}
+
+cudaError_t launch_walk(const uint64_t* off, const uint32_t* tgt, uint64_t n, uint64_t omega0,
+                        uint64_t count, uint32_t k, uint64_t seed, uint32_t epoch,
+                        uint32_t* walks, const Device& dev, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    walk_kernel<<<grid_for(count, 256, dev), 256, 0, s>>>(off, tgt, n, omega0, count, k, seed,
+                                                           epoch, walks);
+    return cudaGetLastError();
+}
+
+}  // namespace ne

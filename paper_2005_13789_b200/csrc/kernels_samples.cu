@@ -1,0 +1,299 @@
+// kernels_samples.cu -- network augmentation into the episode's sample pool
+// (sm_100a): window pairs, canonical Feistel order (O6) and
+// the stable bucketing into 2D blocks.
+//
+// Layout: the pi-indexed slot array (u64 per generation slot, ~0 = hole) is a
+// counting sort by construction -- pi is a bijection, so writing each kept
+// pair to slots[pi(x)] orders the whole episode with one scattered 8-byte
+// store per pair.  A stable multi-way partition then groups the non-hole slots
+// by vertex sub-part while keeping pi order inside each block.
+#include <algorithm>
+
+#include "ne_device.cuh"
+#include "ne_internal.h"
+
+namespace ne {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kTile = 4096;                 // slots per CTA tile
+constexpr uint32_t kPerWarp = kTile / kWarps;    // 512 slots, 16 chunks of 32
+constexpr uint32_t kChunks = kPerWarp / 32;
+constexpr uint32_t kScanChunk = 4096;            // elements per scan block
+constexpr uint32_t kMaxBuckets = 256;
+
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+Feistel make_feistel(const PoolParams& p) {
+    uint32_t b = 0;
+    while (b < 64 && (1ull << b) < p.N) ++b;
+    if (b < 2) b = 2;
+    if (b & 1) ++b;
+    Feistel f;
+    f.N = p.N;
+    f.h = b / 2;
+    f.mask = (f.h >= 64) ? ~0ull : ((1ull << f.h) - 1);
+    f.episode = p.episode;
+    f.tagw = (kTagShuf << 24) | p.epoch;
+    f.key = make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+    return f;
+}
+
+unsigned grid_cap(uint64_t blocks, const Device& dev, int per_sm) {
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)dev.sm_count * per_sm));
+}
+
+}  // namespace
+
+// Warp per walker: the walk (k+1 ids) is staged in shared memory, the Pw
+// window slots are spread over the lanes, and every kept pair is written to
+// slots[pi(x)] with x = (omega - omega0) * Pw + s its local generation index.
+__global__ void __launch_bounds__(kThreads) pairs_walk_kernel(const uint32_t* __restrict__ walks,
+                                                              const uint32_t* __restrict__ slot_tab,
+                                                              PoolParams p, Feistel f,
+                                                              uint64_t* __restrict__ slots) {
+    extern __shared__ uint32_t smem_path[];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    uint32_t* path = smem_path + warp * (p.k + 1);
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < p.units; w += nwarps) {
+        const uint32_t* src = walks + w * (uint64_t)(p.k + 1);
+        for (uint32_t i = lane; i <= p.k; i += 32) path[i] = src[i];
+        __syncwarp();
+        for (uint32_t s = lane; s < p.Pw; s += 32) {
+            const uint32_t t = __ldg(slot_tab + s);
+            const uint32_t i = t >> 16, d = t & 0xFFFFu;
+            const uint32_t b = path[i + d];
+            if (b == kSentinel || b < p.c_begin || b >= p.c_end) continue;  // hole / other part
+            const uint64_t y = f(w * (uint64_t)p.Pw + s);
+            slots[y] = (uint64_t)path[i] | ((uint64_t)b << 32);
+        }
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
+                              uint64_t* slots, const Device& dev, cudaStream_t s) {
+    if (p.units == 0) return cudaSuccess;
+    const Feistel f = make_feistel(p);
+    const size_t smem = (size_t)kWarps * (p.k + 1) * sizeof(uint32_t);
+    pairs_walk_kernel<<<grid_cap(ceil_div(p.units, kWarps), dev, 8), kThreads, smem, s>>>(
+        walks, slot_tab, p, f, slots);
+    return cudaGetLastError();
+}
+
+// LINE mode: the pool is the CSR edge list; unit = edge id.
+__global__ void __launch_bounds__(kThreads) pairs_line_kernel(const uint64_t* __restrict__ off,
+                                                              const uint32_t* __restrict__ tgt,
+                                                              uint64_t n, PoolParams p, Feistel f,
+                                                              uint64_t* __restrict__ slots) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < p.units; x += stride) {
+        const uint64_t e = p.u0 + x;
+        const uint32_t dst = __ldg(tgt + e);
+        if (dst < p.c_begin || dst >= p.c_end) continue;
+        const uint32_t src = range_of(off, (uint32_t)n, e);
+        slots[f(x)] = (uint64_t)src | ((uint64_t)dst << 32);
+    }
+}
+
+cudaError_t launch_pairs_line(const uint64_t* off, const uint32_t* tgt, uint64_t n,
+                              const PoolParams& p, uint64_t* slots, const Device& dev,
+                              cudaStream_t s) {
+    if (p.units == 0) return cudaSuccess;
+    const Feistel f = make_feistel(p);
+    pairs_line_kernel<<<grid_cap(ceil_div(p.units, kThreads), dev, 8), kThreads, 0, s>>>(
+        off, tgt, n, p, f, slots);
+    return cudaGetLastError();
+}
+
+// ---- stable partition by vertex sub-part ------------------------------------
+
+__device__ __forceinline__ uint32_t bucket_of(uint64_t v, const uint64_t* sb, uint32_t nb) {
+    return v == kHole ? 0xFFFFFFFFu : range_of(sb, nb, (uint32_t)v);
+}
+
+// counts[b * ntiles + tile] = number of slots of bucket b in the tile.
+__global__ void __launch_bounds__(kThreads) bucket_count_kernel(const uint64_t* __restrict__ slots,
+                                                                uint64_t N,
+                                                                const uint64_t* __restrict__ bounds,
+                                                                uint32_t nb, uint64_t ntiles,
+                                                                uint32_t* __restrict__ counts) {
+    __shared__ uint64_t sb[kMaxBuckets + 1];
+    __shared__ uint32_t hist[kMaxBuckets];
+    for (uint32_t i = threadIdx.x; i <= nb; i += kThreads) sb[i] = bounds[i];
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (uint32_t i = threadIdx.x; i < nb; i += kThreads) hist[i] = 0;
+        __syncthreads();
+        const uint64_t end = min(N, (tile + 1) * kTile);
+        for (uint64_t i = tile * kTile + threadIdx.x; i < end; i += kThreads) {
+            const uint32_t b = bucket_of(slots[i], sb, nb);
+            if (b != 0xFFFFFFFFu) atomicAdd(&hist[b], 1u);
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < nb; b += kThreads) counts[(uint64_t)b * ntiles + tile] = hist[b];
+        __syncthreads();
+    }
+}
+
+// Exclusive scan of u32 counts into u64 offsets: per-chunk sums, a single-CTA
+// scan of the chunk sums, then per-chunk scans with their base.
+__global__ void __launch_bounds__(kThreads) scan_sums_kernel(const uint32_t* __restrict__ in,
+                                                             uint64_t M, uint64_t* __restrict__ sums) {
+    __shared__ uint64_t red[kWarps];
+    const uint64_t base = (uint64_t)blockIdx.x * kScanChunk;
+    uint64_t acc = 0;
+    for (uint64_t i = base + threadIdx.x; i < min(M, base + kScanChunk); i += kThreads) acc += in[i];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if (lane_id() == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (int w = 0; w < kWarps; ++w) t += red[w];
+        sums[blockIdx.x] = t;
+    }
+}
+
+__global__ void scan_partials_kernel(uint64_t* __restrict__ sums, uint64_t nchunks,
+                                     uint64_t* __restrict__ total) {
+    // one warp, sequential over chunks in groups of 32 (nchunks is small)
+    const uint32_t lane = lane_id();
+    uint64_t run = 0;
+    for (uint64_t b = 0; b < nchunks; b += 32) {
+        const uint64_t i = b + lane;
+        const uint64_t v = i < nchunks ? sums[i] : 0;
+        uint64_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += t;
+        }
+        if (i < nchunks) sums[i] = run + incl - v;
+        run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+    if (lane == 0) *total = run;
+}
+
+__global__ void __launch_bounds__(kThreads) scan_chunks_kernel(const uint32_t* __restrict__ in,
+                                                               uint64_t M,
+                                                               const uint64_t* __restrict__ sums,
+                                                               uint64_t* __restrict__ out) {
+    // each thread owns 16 consecutive elements of the 4096-element chunk
+    __shared__ uint64_t warp_tot[kWarps];
+    const uint64_t base = (uint64_t)blockIdx.x * kScanChunk + threadIdx.x * 16ull;
+    uint32_t v[16];
+    uint64_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        v[j] = base + j < M ? in[base + j] : 0u;
+        acc += v[j];
+    }
+    uint64_t incl = acc;
+    const uint32_t lane = lane_id();
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+    }
+    if (lane == 31) warp_tot[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    uint64_t run = sums[blockIdx.x];
+    for (uint32_t w = 0; w < (threadIdx.x >> 5); ++w) run += warp_tot[w];
+    run += incl - acc;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (base + j < M) out[base + j] = run;
+        run += v[j];
+    }
+}
+
+__global__ void block_offsets_kernel(const uint64_t* __restrict__ tile_off, uint64_t ntiles,
+                                     uint32_t nb, const uint64_t* __restrict__ total,
+                                     uint64_t* __restrict__ block_offsets) {
+    for (uint32_t b = threadIdx.x; b <= nb; b += blockDim.x)
+        block_offsets[b] = b < nb ? tile_off[(uint64_t)b * ntiles] : *total;
+}
+
+// Stable scatter: within a tile every warp owns 512 consecutive slots; ranks
+// inside a 32-slot chunk come from __match_any_sync, per-warp bases from a
+// per-tile prefix over warps, so the pool keeps slot (= pi) order per block.
+__global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const uint64_t* __restrict__ slots,
+                                                                  uint64_t N,
+                                                                  const uint64_t* __restrict__ bounds,
+                                                                  uint32_t nb, uint64_t ntiles,
+                                                                  const uint64_t* __restrict__ tile_off,
+                                                                  uint64_t* __restrict__ pool) {
+    __shared__ uint64_t sb[kMaxBuckets + 1];
+    __shared__ uint32_t wcnt[kWarps][kMaxBuckets];
+    __shared__ uint64_t wbase[kWarps][kMaxBuckets];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (uint32_t i = threadIdx.x; i <= nb; i += kThreads) sb[i] = bounds[i];
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (uint32_t i = threadIdx.x; i < kWarps * nb; i += kThreads) wcnt[i / nb][i % nb] = 0;
+        __syncthreads();
+        const uint64_t wb = tile * kTile + (uint64_t)warp * kPerWarp;
+        uint64_t vals[kChunks];
+        uint32_t bks[kChunks];
+#pragma unroll
+        for (uint32_t c = 0; c < kChunks; ++c) {
+            const uint64_t i = wb + c * 32 + lane;
+            vals[c] = i < N ? slots[i] : kHole;
+            bks[c] = bucket_of(vals[c], sb, nb);
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, bks[c]);
+            if (bks[c] != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1))
+                wcnt[warp][bks[c]] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < nb; b += kThreads) {
+            uint64_t run = tile_off[(uint64_t)b * ntiles + tile];
+            for (int w = 0; w < kWarps; ++w) { wbase[w][b] = run; run += wcnt[w][b]; }
+        }
+        __syncthreads();
+#pragma unroll
+        for (uint32_t c = 0; c < kChunks; ++c) {
+            const uint32_t b = bks[c];
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
+            if (b != 0xFFFFFFFFu) {
+                pool[wbase[warp][b] + __popc(peers & lt_mask)] = vals[c];
+            }
+            __syncwarp();
+            if (b != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) wbase[warp][b] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+}
+
+size_t bucket_scratch_bytes(uint64_t N, uint32_t nb) {
+    const uint64_t ntiles = std::max<uint64_t>(1, ceil_div(N, kTile));
+    const uint64_t M = ntiles * nb;
+    const uint64_t nchunks = std::max<uint64_t>(1, ceil_div(M, kScanChunk));
+    return M * sizeof(uint32_t) + M * sizeof(uint64_t) + (nchunks + 2) * sizeof(uint64_t) + 256;
+}
+
+cudaError_t launch_bucket(const uint64_t* slots, uint64_t N, const uint64_t* sub_bounds,
+                          uint32_t nb, void* scratch, uint64_t* pool, uint64_t* block_offsets,
+                          const Device& dev, cudaStream_t s, uint32_t* launches) {
+    if (nb == 0 || nb > kMaxBuckets) return cudaErrorInvalidValue;
+    const uint64_t ntiles = std::max<uint64_t>(1, ceil_div(N, kTile));
+    const uint64_t M = ntiles * nb;
+    const uint64_t nchunks = std::max<uint64_t>(1, ceil_div(M, kScanChunk));
+    uint32_t* counts = reinterpret_cast<uint32_t*>(scratch);
+    uint64_t* tile_off = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(counts + M) + 15) & ~(uintptr_t)15);
+    uint64_t* sums = tile_off + M;
+    uint64_t* total = sums + nchunks;
+    const unsigned g = grid_cap(ntiles, dev, 8);
+    bucket_count_kernel<<<g, kThreads, 0, s>>>(slots, N, sub_bounds, nb, ntiles, counts);
+    scan_sums_kernel<<<(unsigned)nchunks, kThreads, 0, s>>>(counts, M, sums);
+    scan_partials_kernel<<<1, 32, 0, s>>>(sums, nchunks, total);
+    scan_chunks_kernel<<<(unsigned)nchunks, kThreads, 0, s>>>(counts, M, sums, tile_off);
+    block_offsets_kernel<<<1, 256, 0, s>>>(tile_off, ntiles, nb, total, block_offsets);
+    bucket_scatter_kernel<<<g, kThreads, 0, s>>>(slots, N, sub_bounds, nb, ntiles, tile_off, pool);
+    if (launches) *launches += 6;
+    return cudaGetLastError();
+}
+
+}  // namespace ne

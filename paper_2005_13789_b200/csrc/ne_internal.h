@@ -1,0 +1,75 @@
+// ne_internal.h -- kernel launchers shared by the runtime (host C++) and the
+// CUDA translation units.  Not part of the ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ne {
+
+// Device grid sizing: a multiple of the SM count (persistent / grid-stride kernels).
+struct Device {
+    int sm_count = 148;
+    int max_threads_per_sm = 2048;
+};
+
+// ---- graph / init / walks (kernels_graph.cu) -------------------------------
+// S:24 invariants; bad[0] = first i with offsets[i+1] < offsets[i] (or ~0),
+// bad[1] = first e with targets[e] >= n (or ~0).
+cudaError_t launch_validate_csr(const uint64_t* off, const uint32_t* tgt, uint64_t n,
+                                uint64_t nnz, unsigned long long* bad, const Device& dev,
+                                cudaStream_t s);
+// O9: rows [row_begin, row_begin + rows) of the vertex matrix into V (row-major).
+cudaError_t launch_init_vertex(float* V, uint64_t row_begin, uint64_t rows, uint32_t d,
+                               uint64_t seed, const Device& dev, cudaStream_t s);
+// O4: walkers [omega0, omega0 + count) -> walks[count][k+1].
+cudaError_t launch_walk(const uint64_t* off, const uint32_t* tgt, uint64_t n, uint64_t omega0,
+                        uint64_t count, uint32_t k, uint64_t seed, uint32_t epoch,
+                        uint32_t* walks, const Device& dev, cudaStream_t s);
+
+// ---- sample pool (kernels_samples.cu) ---------------------------------------
+struct PoolParams {
+    uint64_t N;           // slots of the episode (units * Pw)
+    uint64_t units;       // walkers (DeepWalk) or edges (LINE) of the episode
+    uint64_t u0;          // first unit (edge id in LINE mode)
+    uint32_t k, l, Pw;    // walk steps, window, pairs per full walk (1 in LINE mode)
+    uint32_t episode, epoch;
+    uint64_t seed;
+    uint64_t c_begin, c_end;   // this rank's context part
+};
+// O5 + O6: kept pairs (dst in the context part) -> slots[pi(x)], holes = ~0.
+// slot_tab[s] = (i << 16) | delta for s < Pw.
+cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
+                              uint64_t* slots, const Device& dev, cudaStream_t s);
+cudaError_t launch_pairs_line(const uint64_t* off, const uint32_t* tgt, uint64_t n,
+                              const PoolParams& p, uint64_t* slots, const Device& dev,
+                              cudaStream_t s);
+// Stable partition of the non-hole slots by vertex sub-part (bounds over
+// nb+1 entries, device pointer): pool[block_offsets[b] ...] in slot order.
+size_t bucket_scratch_bytes(uint64_t N, uint32_t nb);
+cudaError_t launch_bucket(const uint64_t* slots, uint64_t N, const uint64_t* sub_bounds,
+                          uint32_t nb, void* scratch, uint64_t* pool, uint64_t* block_offsets,
+                          const Device& dev, cudaStream_t s, uint32_t* launches);
+
+// ---- SGNS (kernels_sgns.cu) ---------------------------------------------------
+struct SgnsParams {
+    const uint2* pool;          // (src, dst) pairs of the block, canonical order
+    uint64_t count;             // samples in the block
+    float* V;                   // vertex sub-part slot; row (src - v_begin)
+    uint64_t v_begin;
+    float* C;                   // context part; row (dst - c_begin)
+    uint64_t c_begin, c_count;
+    const uint2* alias;         // (thr, alias) per context-part column
+    uint32_t d, K;
+    float lr;
+    uint64_t seed;
+    uint32_t epoch, episode, block;   // block = vsub * world + rank (O8 counter)
+    double* loss;               // += sum of loss terms (device)
+    int deterministic;          // 1: one warp, canonical order
+    uint64_t max_warps;         // Hogwild concurrency cap (>= 1)
+};
+cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s);
+cudaError_t launch_export_negatives(const SgnsParams& p, uint64_t pos_begin, uint64_t count,
+                                    uint32_t* out, const Device& dev, cudaStream_t s);
+
+}  // namespace ne

@@ -1,0 +1,797 @@
+// runtime.cpp -- the C ABI (include/ne.h): context, device memory, the
+// episode pipeline and the NCCL ring of vertex sub-parts.
+//
+// Per-rank HBM layout (rank g of P, k sub-parts; contiguous ranges, D12):
+//   CSR           offsets u64[n+1], targets u32[nnz]           (replicated)
+//   alias         uint2[c_count] (thr, alias) of context part g (O3)
+//   context       fp32[c_count][d], part g, resident for the whole run
+//   vertex slots  2k buffers of fp32[max sub-part rows][d]: the k sub-parts
+//                 being trained this round and the k arriving (ping-pong)
+//   walks         u32[walkers][k+1]        (one episode)
+//   slots         u64[N]   pi-indexed pairs (one episode, ~0 = hole)
+//   pool          u64[N]   (src, dst) grouped by vertex sub-part, pi order
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "ne.h"
+#include "ne_internal.h"
+
+struct ne_ctx {
+    ne_config cfg{};
+    int device = 0;
+    ne::Device dev;
+    cudaStream_t own_stream = nullptr, stream = nullptr, comm_stream = nullptr;
+    ne_alloc_fn alloc = nullptr;
+    ne_free_fn free_fn = nullptr;
+    void* user = nullptr;
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    std::string err;
+
+    struct Alloc { void* p; size_t bytes; };
+    std::vector<Alloc> allocs;
+
+    bool loaded = false;
+    uint64_t n = 0, nnz = 0;
+    uint64_t* d_off = nullptr;
+    uint32_t* d_tgt = nullptr;
+    std::vector<uint64_t> part_bounds, sub_bounds;
+    uint64_t* d_sub_bounds = nullptr;
+    uint2* d_alias = nullptr;
+    float* d_C = nullptr;
+    uint64_t c_begin = 0, c_count = 0;
+    std::vector<float*> vslot;  // 2k buffers
+    int cur = 0;                // half [cur*k, cur*k+k) holds the current sub-parts
+    uint64_t max_sub_rows = 0;
+
+    uint32_t Pw = 1;
+    uint64_t units_total = 0, units_max = 0, N_max = 0;
+    uint32_t* d_walks = nullptr;
+    uint32_t* d_slot_tab = nullptr;
+    uint64_t* d_slots = nullptr;
+    uint64_t* d_pool = nullptr;
+    void* d_scratch = nullptr;
+    uint64_t* d_boff = nullptr;
+    std::vector<uint64_t> boff;
+    double* d_loss = nullptr;
+    unsigned long long* d_bad = nullptr;
+    uint32_t* d_tmp_u32 = nullptr;
+    size_t tmp_u32_cap = 0;
+
+    int64_t walked_epoch = -1, walked_episode = -1;
+    int64_t built_epoch = -1, built_episode = -1;
+    uint64_t walked_units = 0;
+
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    uint32_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_create_error;  // ne_last_error(NULL) after a failed ne_create
+
+int fail(ne_ctx* c, int code, const char* fmt, ...) {
+    static const char* names[] = {"NE_OK", "NE_EINVAL", "NE_ERANGE", "NE_ENOMEM", "NE_ESTATE",
+                                  "NE_ECUDA", "NE_ENCCL", "NE_ESCHED"};
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = std::string(names[-code]) + ": " + buf;
+    return code;
+}
+
+#define NE_CUDA(ctx, call)                                                                  \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(ctx, NE_ECUDA, "%s (%s:%d %s)", cudaGetErrorString(e_), __FILE__,   \
+                        __LINE__, #call);                                                   \
+    } while (0)
+
+#define NE_NCCL(ctx, call)                                                                  \
+    do {                                                                                    \
+        ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            return fail(ctx, NE_ENCCL, "%s (%s:%d)", ncclGetErrorString(r_), __FILE__, __LINE__); \
+    } while (0)
+
+#define NE_TRY(expr)            \
+    do {                        \
+        int rc_ = (expr);       \
+        if (rc_ != NE_OK) return rc_; \
+    } while (0)
+
+void partition(uint64_t begin, uint64_t end, uint32_t parts, uint64_t* out) {
+    const uint64_t len = end - begin, q = len / parts, r = len % parts;
+    for (uint64_t i = 0; i <= parts; ++i) out[i] = begin + i * q + std::min<uint64_t>(i, r);
+}
+
+int plan_vsub(uint32_t P, uint32_t k, uint32_t r, uint32_t t, uint32_t g) {
+    return (int)(((g + P - (r % P)) % P) * k + t);
+}
+
+int dalloc(ne_ctx* c, void** out, size_t bytes) {
+    bytes = std::max<size_t>(bytes, 16);
+    void* p = nullptr;
+    if (c->alloc) {
+        p = c->alloc(bytes, c->device, (void*)c->stream, c->user);
+        if (!p) return fail(c, NE_ENOMEM, "allocator callback returned NULL for %zu bytes", bytes);
+    } else {
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, NE_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+        }
+    }
+    c->allocs.push_back({p, bytes});
+    *out = p;
+    return NE_OK;
+}
+
+template <typename T>
+int dalloc_t(ne_ctx* c, T** out, size_t count) {
+    void* p = nullptr;
+    NE_TRY(dalloc(c, &p, count * sizeof(T)));
+    *out = static_cast<T*>(p);
+    return NE_OK;
+}
+
+void free_all(ne_ctx* c) {
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    for (auto& a : c->allocs) {
+        if (c->free_fn) c->free_fn(a.p, a.bytes, c->device, (void*)c->stream, c->user);
+        else cudaFree(a.p);
+    }
+    c->allocs.clear();
+    c->d_tmp_u32 = nullptr;
+    c->tmp_u32_cap = 0;
+    c->loaded = false;
+    c->walked_epoch = c->walked_episode = c->built_epoch = c->built_episode = -1;
+}
+
+cudaEvent_t next_event(ne_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+
+// O3 on the host, integer Vose (an implementation independent of oracle/):
+// weights q_i = round(deg_i^0.75 * 2^20), columns of capacity W = sum q over
+// n_j = part size, FIFO small/large queues in index order.
+void build_alias(const std::vector<uint64_t>& deg, std::vector<uint2>& out) {
+    const size_t n = deg.size();
+    out.assign(n, make_uint2(0xFFFFFFFFu, 0));
+    if (n == 0) return;
+    std::vector<uint64_t> q(n);
+    unsigned __int128 W = 0;
+    for (size_t i = 0; i < n; ++i) {
+        if (deg[i] == 0) { q[i] = 0; continue; }
+        const double d = (double)deg[i];
+        double d3 = d * d;
+        d3 = d3 * d;
+        q[i] = (uint64_t)std::floor(std::sqrt(std::sqrt(d3)) * 1048576.0 + 0.5);
+        W += q[i];
+    }
+    if (W == 0) {
+        std::fill(q.begin(), q.end(), 1);
+        W = n;
+    }
+    std::vector<unsigned __int128> mass(n);
+    std::vector<uint64_t> num(n);
+    std::vector<uint32_t> alias(n);
+    std::vector<size_t> small, large;
+    small.reserve(2 * n);
+    large.reserve(2 * n);
+    for (size_t i = 0; i < n; ++i) {
+        mass[i] = (unsigned __int128)q[i] * n;
+        (mass[i] < W ? small : large).push_back(i);
+    }
+    size_t sh = 0, lh = 0;
+    while (sh < small.size() && lh < large.size()) {
+        const size_t s = small[sh++], g = large[lh++];
+        num[s] = (uint64_t)mass[s];
+        alias[s] = (uint32_t)g;
+        mass[g] -= W - mass[s];
+        (mass[g] < W ? small : large).push_back(g);
+    }
+    for (; sh < small.size(); ++sh) { num[small[sh]] = (uint64_t)W; alias[small[sh]] = (uint32_t)small[sh]; }
+    for (; lh < large.size(); ++lh) { num[large[lh]] = (uint64_t)W; alias[large[lh]] = (uint32_t)large[lh]; }
+    for (size_t i = 0; i < n; ++i) {
+        const unsigned __int128 t = ((unsigned __int128)num[i] << 32) / W;
+        out[i] = make_uint2(t > 0xFFFFFFFFu ? 0xFFFFFFFFu : (uint32_t)t, alias[i]);
+    }
+}
+
+uint64_t pairs_per_walk(uint32_t k, uint32_t l) {
+    uint64_t c = 0;
+    for (uint32_t i = 0; i < k; ++i) c += std::min<uint32_t>(l, k - i);
+    return c;
+}
+
+void episode_range(const ne_ctx* c, uint32_t episode, uint64_t* u0, uint64_t* units) {
+    const unsigned __int128 U = c->units_total, E = c->cfg.episodes;
+    const uint64_t b = (uint64_t)((episode * U) / E), e = (uint64_t)(((episode + 1) * U) / E);
+    *u0 = b;
+    *units = e - b;
+}
+
+int enter(ne_ctx* c) {
+    if (!c) return NE_EINVAL;
+    c->err.clear();
+    NE_CUDA(c, cudaSetDevice(c->device));
+    return NE_OK;
+}
+
+int check_loaded(ne_ctx* c) {
+    if (!c->loaded) return fail(c, NE_ESTATE, "no graph loaded (call ne_load_graph first)");
+    return NE_OK;
+}
+
+uint32_t nb_local(const ne_ctx* c) { return (uint32_t)c->world * c->cfg.subparts; }
+
+int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
+    uint64_t u0, units;
+    episode_range(c, episode, &u0, &units);
+    NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0, units, c->cfg.walk_len,
+                               c->cfg.seed, epoch, c->d_walks, c->dev, c->stream));
+    if (units) c->launches += 1;
+    c->walked_epoch = epoch;
+    c->walked_episode = episode;
+    c->walked_units = units;
+    c->built_epoch = c->built_episode = -1;
+    return NE_OK;
+}
+
+int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
+    uint64_t u0, units;
+    episode_range(c, episode, &u0, &units);
+    ne::PoolParams p{};
+    p.units = units;
+    p.u0 = u0;
+    p.k = c->cfg.walk_len;
+    p.l = c->cfg.window;
+    p.Pw = c->Pw;
+    p.N = units * c->Pw;
+    p.episode = episode;
+    p.epoch = epoch;
+    p.seed = c->cfg.seed;
+    p.c_begin = c->c_begin;
+    p.c_end = c->c_begin + c->c_count;
+    if (p.N) {
+        NE_CUDA(c, cudaMemsetAsync(c->d_slots, 0xFF, p.N * sizeof(uint64_t), c->stream));
+        if (c->cfg.walk_len > 0)
+            NE_CUDA(c, ne::launch_pairs_walk(c->d_walks, c->d_slot_tab, p, c->d_slots, c->dev, c->stream));
+        else
+            NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_slots, c->dev, c->stream));
+        c->launches += 1;
+    }
+    NE_CUDA(c, ne::launch_bucket(c->d_slots, p.N, c->d_sub_bounds, nb_local(c), c->d_scratch,
+                                 c->d_pool, c->d_boff, c->dev, c->stream, &c->launches));
+    c->boff.assign(nb_local(c) + 1, 0);
+    NE_CUDA(c, cudaMemcpyAsync(c->boff.data(), c->d_boff, c->boff.size() * sizeof(uint64_t),
+                               cudaMemcpyDeviceToHost, c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->built_epoch = epoch;
+    c->built_episode = episode;
+    return NE_OK;
+}
+
+ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t epoch,
+                           uint32_t episode, float lr) {
+    ne::SgnsParams p{};
+    p.pool = reinterpret_cast<const uint2*>(c->d_pool + c->boff[vsub]);
+    p.count = c->boff[vsub + 1] - c->boff[vsub];
+    p.V = V;
+    p.v_begin = c->sub_bounds[vsub];
+    p.C = c->d_C;
+    p.c_begin = c->c_begin;
+    p.c_count = c->c_count;
+    p.alias = c->d_alias;
+    p.d = c->cfg.dim;
+    p.K = c->cfg.negatives;
+    p.lr = lr;
+    p.seed = c->cfg.seed;
+    p.epoch = epoch;
+    p.episode = episode;
+    p.block = vsub * (uint32_t)c->world + (uint32_t)c->rank;
+    p.loss = c->d_loss;
+    p.deterministic = (int)c->cfg.deterministic;
+    const uint64_t rpw = c->cfg.rows_per_warp ? c->cfg.rows_per_warp : 64;
+    const uint64_t rows = std::min<uint64_t>(c->sub_bounds[vsub + 1] - c->sub_bounds[vsub], c->c_count);
+    p.max_warps = std::max<uint64_t>(1, rows / rpw);
+    return p;
+}
+
+// O7 ring: round r, slot t trains block
+// (vsub = ((rank - r) mod P)*k + t, context part rank); the trained sub-part is
+// sent to rank+1 while slot t+1 trains, and the sub-part for round r+1 arrives
+// from rank-1 into the other half of the ping-pong buffers.
+int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st) {
+    const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank;
+    const uint64_t d = c->cfg.dim;
+    if (P > 1 && !c->comm)
+        return fail(c, NE_ESTATE, "world=%u context has no NCCL communicator (layout-only)", P);
+    NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
+    std::vector<cudaEvent_t> recv(k, nullptr);
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, waits;
+    uint64_t samples = 0;
+    for (uint32_t r = 0; r < P; ++r) {
+        for (uint32_t t = 0; t < k; ++t) {
+            const uint32_t vs = (uint32_t)plan_vsub(P, k, r, t, g);
+            float* V = c->vslot[c->cur * k + t];
+            if (recv[t]) {
+                cudaEvent_t w0 = next_event(c), w1 = next_event(c);
+                NE_CUDA(c, cudaEventRecord(w0, c->stream));
+                NE_CUDA(c, cudaStreamWaitEvent(c->stream, recv[t], 0));
+                NE_CUDA(c, cudaEventRecord(w1, c->stream));
+                waits.push_back({w0, w1});
+            }
+            const ne::SgnsParams sp = sgns_params(c, vs, V, epoch, episode, lr);
+            cudaEvent_t e0 = next_event(c), e1 = next_event(c);
+            NE_CUDA(c, cudaEventRecord(e0, c->stream));
+            NE_CUDA(c, ne::launch_sgns(sp, c->dev, c->stream));
+            NE_CUDA(c, cudaEventRecord(e1, c->stream));
+            if (sp.count) { c->launches += 1; if (st) st->train_launches += 1; }
+            timed.push_back({e0, e1});
+            samples += sp.count;
+            if (P > 1) {
+                const uint32_t vs_next = (uint32_t)plan_vsub(P, k, r + 1, t, g);
+                const uint64_t send_rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
+                const uint64_t recv_rows = c->sub_bounds[vs_next + 1] - c->sub_bounds[vs_next];
+                float* Vn = c->vslot[(1 - c->cur) * k + t];
+                NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, e1, 0));
+                NE_NCCL(c, ncclGroupStart());
+                NE_NCCL(c, ncclSend(V, send_rows * d, ncclFloat, (int)((g + 1) % P), c->comm, c->comm_stream));
+                NE_NCCL(c, ncclRecv(Vn, recv_rows * d, ncclFloat, (int)((g + P - 1) % P), c->comm, c->comm_stream));
+                NE_NCCL(c, ncclGroupEnd());
+                cudaEvent_t rv = next_event(c);
+                NE_CUDA(c, cudaEventRecord(rv, c->comm_stream));
+                recv[t] = rv;
+            }
+        }
+        if (P > 1) c->cur = 1 - c->cur;
+    }
+    if (P > 1) {  // the sub-parts are home again; the compute stream waits for them
+        for (uint32_t t = 0; t < k; ++t) {
+            cudaEvent_t w0 = next_event(c), w1 = next_event(c);
+            NE_CUDA(c, cudaEventRecord(w0, c->stream));
+            NE_CUDA(c, cudaStreamWaitEvent(c->stream, recv[t], 0));
+            NE_CUDA(c, cudaEventRecord(w1, c->stream));
+            waits.push_back({w0, w1});
+        }
+    }
+    double loss = 0.0;
+    NE_CUDA(c, cudaMemcpyAsync(&loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (st) {
+        st->samples += samples;
+        st->loss_sum += loss;
+        for (auto& pr : timed) {
+            float ms = 0.f;
+            NE_CUDA(c, cudaEventElapsedTime(&ms, pr.first, pr.second));
+            st->ms_train += ms;
+        }
+        for (auto& pr : waits) {
+            float ms = 0.f;
+            NE_CUDA(c, cudaEventElapsedTime(&ms, pr.first, pr.second));
+            st->ms_comm_wait += ms;
+        }
+    }
+    c->ev_used = 0;
+    return NE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ne_version(void) { return NE_ABI_VERSION; }
+
+int ne_plan_vsub(uint32_t world, uint32_t subparts, uint32_t r, uint32_t t, uint32_t g) {
+    if (world == 0 || subparts == 0 || t >= subparts || g >= world) return -1;
+    return plan_vsub(world, subparts, r, t, g);
+}
+
+int ne_partition_bounds(uint64_t n, uint32_t parts, uint64_t* bounds) {
+    if (parts == 0 || !bounds) return NE_EINVAL;
+    partition(0, n, parts, bounds);
+    return NE_OK;
+}
+
+int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
+              ne_free_fn free_fn, void* user) {
+    g_create_error.clear();
+    if (!out || !cfg) return fail(nullptr, NE_EINVAL, "null argument");
+    *out = nullptr;
+    ne_ctx* c = new ne_ctx();
+    c->cfg = *cfg;
+    c->device = device;
+    c->alloc = alloc;
+    c->free_fn = free_fn;
+    c->user = user;
+    auto bad = [&](int code) {  // the message stays readable through ne_last_error(NULL)
+        g_create_error = c->err;
+        ne_destroy(c);
+        return code;
+    };
+    const ne_config& g = *cfg;
+    if (g.dim == 0 || g.dim % 4 || g.dim > 512)
+        return bad(fail(c, NE_EINVAL, "dim=%u must be a multiple of 4 in [4, 512]", g.dim));
+    if (g.negatives > 8) return bad(fail(c, NE_EINVAL, "negatives=%u > 8", g.negatives));
+    if (g.walk_len > 255) return bad(fail(c, NE_EINVAL, "walk_len=%u > 255", g.walk_len));
+    if (g.walk_len > 0 && (g.window == 0 || g.window > g.walk_len))
+        return bad(fail(c, NE_EINVAL, "window=%u not in [1, walk_len=%u]", g.window, g.walk_len));
+    if (g.walk_len > 0 && g.walks_per_node == 0)
+        return bad(fail(c, NE_EINVAL, "walks_per_node must be >= 1"));
+    if (g.episodes == 0 || g.episodes > 4095)
+        return bad(fail(c, NE_EINVAL, "episodes=%u not in [1, 4095]", g.episodes));
+    if (g.reserved != 0) return bad(fail(c, NE_EINVAL, "reserved field must be 0"));
+    if (g.subparts == 0 || g.subparts > 256)
+        return bad(fail(c, NE_EINVAL, "subparts=%u not in [1, 256]", g.subparts));
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return bad(fail(c, NE_ECUDA, "no CUDA device %d (%s)", device,
+                        e != cudaSuccess ? cudaGetErrorString(e) : "out of range"));
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
+        return bad(fail(c, NE_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device,
+                        prop.major, prop.minor));
+    c->dev.sm_count = prop.multiProcessorCount;
+    c->dev.max_threads_per_sm = prop.maxThreadsPerMultiProcessor;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&c->d_loss, sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&c->d_bad, 2 * sizeof(unsigned long long)) != cudaSuccess)
+        return bad(fail(c, NE_ECUDA, "stream/scratch setup failed on device %d", device));
+    c->stream = c->own_stream;
+    *out = c;
+    return NE_OK;
+}
+
+int ne_set_stream(ne_ctx* c, void* stream) {
+    NE_TRY(enter(c));
+    c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+    return NE_OK;
+}
+
+int ne_get_nccl_id(uint8_t id[128]) {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) return NE_ENCCL;
+    std::memcpy(id, &u, 128);
+    return NE_OK;
+}
+
+int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
+    NE_TRY(enter(c));
+    if (c->loaded) return fail(c, NE_ESTATE, "ne_init_dist must precede ne_load_graph");
+    if (world < 1 || rank < 0 || rank >= world) return fail(c, NE_EINVAL, "rank=%d world=%d", rank, world);
+    if ((uint64_t)world * c->cfg.subparts > 256 || (uint64_t)world * world * c->cfg.subparts > 4096)
+        return fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
+    if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
+    c->rank = rank;
+    c->world = world;
+    if (world > 1 && id) {  // id == NULL: layout-only context (pool/negatives of rank `rank`)
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        NE_NCCL(c, ncclCommInitRank(&c->comm, world, u, rank));
+    }
+    return NE_OK;
+}
+
+int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
+                  const uint32_t* targets) {
+    NE_TRY(enter(c));
+    if (!offsets || (nnz && !targets)) return fail(c, NE_EINVAL, "null offsets/targets");
+    if (n == 0xFFFFFFFFu) return fail(c, NE_ERANGE, "n=%u reserves the sentinel id", n);
+    if (n < (uint32_t)c->world) return fail(c, NE_ERANGE, "n=%u < world=%d", n, c->world);
+    if (nnz >= (1ull << 40)) return fail(c, NE_ERANGE, "nnz=%llu too large", (unsigned long long)nnz);
+    free_all(c);
+    const ne_config& g = c->cfg;
+    const uint32_t P = (uint32_t)c->world, k = g.subparts;
+    c->n = n;
+    c->nnz = nnz;
+
+    // CSR into HBM, validated on the device.
+    NE_TRY(dalloc_t(c, &c->d_off, (size_t)n + 1));
+    NE_TRY(dalloc_t(c, &c->d_tgt, std::max<uint64_t>(nnz, 1)));
+    NE_CUDA(c, cudaMemcpyAsync(c->d_off, offsets, ((size_t)n + 1) * sizeof(uint64_t), cudaMemcpyDefault, c->stream));
+    if (nnz) NE_CUDA(c, cudaMemcpyAsync(c->d_tgt, targets, nnz * sizeof(uint32_t), cudaMemcpyDefault, c->stream));
+    NE_CUDA(c, cudaMemsetAsync(c->d_bad, 0xFF, 2 * sizeof(unsigned long long), c->stream));
+    NE_CUDA(c, ne::launch_validate_csr(c->d_off, c->d_tgt, n, nnz, c->d_bad, c->dev, c->stream));
+    c->launches += 1;
+    unsigned long long bad[2];
+    uint64_t ends[2];
+    NE_CUDA(c, cudaMemcpyAsync(bad, c->d_bad, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+    NE_CUDA(c, cudaMemcpyAsync(&ends[0], c->d_off, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    NE_CUDA(c, cudaMemcpyAsync(&ends[1], c->d_off + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (ends[0] != 0) return fail(c, NE_EINVAL, "offsets[0]=%llu != 0", (unsigned long long)ends[0]);
+    if (bad[0] != ~0ull) {
+        uint64_t pair[2];
+        NE_CUDA(c, cudaMemcpy(pair, c->d_off + bad[0], sizeof pair, cudaMemcpyDeviceToHost));
+        return fail(c, NE_EINVAL, "offsets[%llu]=%llu < offsets[%llu]=%llu", bad[0] + 1,
+                    (unsigned long long)pair[1], bad[0], (unsigned long long)pair[0]);
+    }
+    if (ends[1] != nnz)
+        return fail(c, NE_EINVAL, "offsets[%u]=%llu != nnz=%llu", n, (unsigned long long)ends[1],
+                    (unsigned long long)nnz);
+    if (bad[1] != ~0ull) {
+        uint32_t t;
+        NE_CUDA(c, cudaMemcpy(&t, c->d_tgt + bad[1], sizeof t, cudaMemcpyDeviceToHost));
+        return fail(c, NE_EINVAL, "targets[%llu]=%u >= n=%u", bad[1], t, n);
+    }
+
+    // Partitions (D12): P context parts; each vertex part split into k sub-parts.
+    c->part_bounds.assign(P + 1, 0);
+    partition(0, n, P, c->part_bounds.data());
+    c->sub_bounds.assign((size_t)P * k + 1, 0);
+    c->max_sub_rows = 0;
+    for (uint32_t p = 0; p < P; ++p) {
+        partition(c->part_bounds[p], c->part_bounds[p + 1], k, &c->sub_bounds[(size_t)p * k]);
+        for (uint32_t t = 0; t < k; ++t)
+            c->max_sub_rows = std::max(c->max_sub_rows, c->sub_bounds[(size_t)p * k + t + 1] - c->sub_bounds[(size_t)p * k + t]);
+    }
+    c->sub_bounds[(size_t)P * k] = n;
+    NE_TRY(dalloc_t(c, &c->d_sub_bounds, c->sub_bounds.size()));
+    NE_CUDA(c, cudaMemcpyAsync(c->d_sub_bounds, c->sub_bounds.data(), c->sub_bounds.size() * sizeof(uint64_t),
+                               cudaMemcpyHostToDevice, c->stream));
+
+    // Alias table of this rank's context part (O3, reading D9).
+    c->c_begin = c->part_bounds[c->rank];
+    c->c_count = c->part_bounds[c->rank + 1] - c->c_begin;
+    // Degrees of the context part: read the caller's offsets directly when they
+    // are host memory, else copy that slice back from the device.
+    std::vector<uint64_t> hoff;
+    const uint64_t* deg_src = offsets + c->c_begin;
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, offsets) != cudaSuccess) cudaGetLastError();
+    if (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) {
+        hoff.resize(c->c_count + 1);
+        NE_CUDA(c, cudaMemcpyAsync(hoff.data(), c->d_off + c->c_begin, hoff.size() * sizeof(uint64_t),
+                                   cudaMemcpyDeviceToHost, c->stream));
+        NE_CUDA(c, cudaStreamSynchronize(c->stream));
+        deg_src = hoff.data();
+    }
+    std::vector<uint64_t> deg(c->c_count);
+    for (uint64_t i = 0; i < c->c_count; ++i) deg[i] = deg_src[i + 1] - deg_src[i];
+    std::vector<uint2> tab;
+    build_alias(deg, tab);
+    NE_TRY(dalloc_t(c, &c->d_alias, std::max<uint64_t>(c->c_count, 1)));
+    NE_CUDA(c, cudaMemcpyAsync(c->d_alias, tab.data(), tab.size() * sizeof(uint2), cudaMemcpyHostToDevice, c->stream));
+
+    // Embeddings (O9): context part = 0; home vertex sub-parts initialised.
+    NE_TRY(dalloc_t(c, &c->d_C, std::max<uint64_t>(c->c_count, 1) * g.dim));
+    NE_CUDA(c, cudaMemsetAsync(c->d_C, 0, c->c_count * g.dim * sizeof(float), c->stream));
+    c->vslot.assign(2 * (size_t)k, nullptr);
+    for (size_t i = 0; i < c->vslot.size(); ++i)
+        NE_TRY(dalloc_t(c, &c->vslot[i], std::max<uint64_t>(c->max_sub_rows, 1) * g.dim));
+    c->cur = 0;
+    for (uint32_t t = 0; t < k; ++t) {
+        const size_t vs = (size_t)c->rank * k + t;
+        NE_CUDA(c, ne::launch_init_vertex(c->vslot[t], c->sub_bounds[vs], c->sub_bounds[vs + 1] - c->sub_bounds[vs],
+                                          g.dim, g.seed, c->dev, c->stream));
+        c->launches += 1;
+    }
+
+    // Episode buffers: walks, pi-indexed slots, pool, bucketing scratch.
+    c->units_total = g.walk_len == 0 ? nnz : (uint64_t)n * g.walks_per_node;
+    c->Pw = g.walk_len == 0 ? 1u : (uint32_t)pairs_per_walk(g.walk_len, g.window);
+    c->units_max = (c->units_total + g.episodes - 1) / g.episodes;
+    c->N_max = c->units_max * c->Pw;
+    if (g.walk_len > 0) {
+        NE_TRY(dalloc_t(c, &c->d_walks, std::max<uint64_t>(c->units_max, 1) * (g.walk_len + 1)));
+        std::vector<uint32_t> tab_s;
+        for (uint32_t i = 0; i < g.walk_len; ++i)
+            for (uint32_t dl = 1; dl <= g.window && i + dl <= g.walk_len; ++dl) tab_s.push_back((i << 16) | dl);
+        NE_TRY(dalloc_t(c, &c->d_slot_tab, tab_s.size()));
+        NE_CUDA(c, cudaMemcpyAsync(c->d_slot_tab, tab_s.data(), tab_s.size() * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, c->stream));
+    }
+    NE_TRY(dalloc_t(c, &c->d_slots, std::max<uint64_t>(c->N_max, 1)));
+    NE_TRY(dalloc_t(c, &c->d_pool, std::max<uint64_t>(c->N_max, 1)));
+    NE_TRY(dalloc(c, &c->d_scratch, ne::bucket_scratch_bytes(c->N_max, nb_local(c))));
+    NE_TRY(dalloc_t(c, &c->d_boff, (size_t)nb_local(c) + 1));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->loaded = true;
+    return NE_OK;
+}
+
+int ne_random_walk(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t* host_walks,
+                   size_t cap_u32, uint64_t* walkers_out) {
+    NE_TRY(enter(c));
+    NE_TRY(check_loaded(c));
+    if (c->cfg.walk_len == 0) return fail(c, NE_ESTATE, "LINE mode (walk_len=0) has no walks");
+    if (episode >= c->cfg.episodes) return fail(c, NE_ERANGE, "episode=%u >= episodes=%u", episode, c->cfg.episodes);
+    if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
+    NE_TRY(do_walk(c, epoch, episode));
+    const uint64_t total = c->walked_units * (c->cfg.walk_len + 1);
+    if (walkers_out) *walkers_out = c->walked_units;
+    if (host_walks) {
+        if (cap_u32 < total) return fail(c, NE_ERANGE, "host_walks capacity %zu < %llu", cap_u32, (unsigned long long)total);
+        NE_CUDA(c, cudaMemcpyAsync(host_walks, c->d_walks, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    }
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    return NE_OK;
+}
+
+int ne_build_samples(ne_ctx* c, uint32_t epoch, uint32_t episode, uint64_t* n_samples_out) {
+    NE_TRY(enter(c));
+    NE_TRY(check_loaded(c));
+    if (episode >= c->cfg.episodes) return fail(c, NE_ERANGE, "episode=%u >= episodes=%u", episode, c->cfg.episodes);
+    if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
+    if (c->cfg.walk_len > 0 && (c->walked_epoch != (int64_t)epoch || c->walked_episode != (int64_t)episode))
+        return fail(c, NE_ESTATE, "no walks for epoch %u episode %u (call ne_random_walk)", epoch, episode);
+    NE_TRY(do_build(c, epoch, episode));
+    if (n_samples_out) *n_samples_out = c->boff.back();
+    return NE_OK;
+}
+
+int ne_train_samples(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* stats) {
+    NE_TRY(enter(c));
+    NE_TRY(check_loaded(c));
+    if (c->built_episode != (int64_t)episode)
+        return fail(c, NE_ESTATE, "no sample pool for episode %u (call ne_build_samples)", episode);
+    if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    const uint32_t l0 = c->launches;
+    NE_TRY(do_train(c, epoch, episode, lr, stats));
+    if (stats) stats->kernel_launches = c->launches - l0;
+    return NE_OK;
+}
+
+int ne_train_epoch(ne_ctx* c, uint32_t epoch, float lr, uint32_t flags, ne_stats* stats) {
+    NE_TRY(enter(c));
+    NE_TRY(check_loaded(c));
+    if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
+    ne_stats acc;
+    std::memset(&acc, 0, sizeof acc);
+    const uint32_t l0 = c->launches;
+    if (flags & NE_REUSE_SAMPLES) {
+        if (c->cfg.episodes != 1 || c->built_episode != 0)
+            return fail(c, NE_ESTATE, "NE_REUSE_SAMPLES needs episodes == 1 and a built pool");
+        NE_TRY(do_train(c, epoch, 0, lr, &acc));
+    } else {
+        for (uint32_t e = 0; e < c->cfg.episodes; ++e) {
+            cudaEvent_t a = next_event(c), b = next_event(c), d = next_event(c);
+            NE_CUDA(c, cudaEventRecord(a, c->stream));
+            if (c->cfg.walk_len > 0) NE_TRY(do_walk(c, epoch, e));
+            NE_CUDA(c, cudaEventRecord(b, c->stream));
+            NE_TRY(do_build(c, epoch, e));  // synchronises the stream
+            NE_CUDA(c, cudaEventRecord(d, c->stream));
+            NE_CUDA(c, cudaEventSynchronize(d));
+            float mw = 0.f, mb = 0.f;
+            NE_CUDA(c, cudaEventElapsedTime(&mw, a, b));
+            NE_CUDA(c, cudaEventElapsedTime(&mb, b, d));
+            acc.ms_walk += mw;
+            acc.ms_build += mb;
+            c->ev_used = 0;
+            NE_TRY(do_train(c, epoch, e, lr, &acc));
+        }
+    }
+    acc.kernel_launches = c->launches - l0;
+    if (stats) *stats = acc;
+    return NE_OK;
+}
+
+static int rows_op(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, float* host,
+                   const float* in, size_t cap_floats) {
+    NE_TRY(enter(c));
+    NE_TRY(check_loaded(c));
+    if (which != NE_VERTEX && which != NE_CONTEXT) return fail(c, NE_EINVAL, "which=%d", which);
+    const uint64_t pb = c->part_bounds[c->rank], pe = c->part_bounds[c->rank + 1];
+    if (row_begin > row_end || row_begin < pb || row_end > pe)
+        return fail(c, NE_ERANGE, "rows [%u, %u) not in this rank's part [%llu, %llu)", row_begin, row_end,
+                    (unsigned long long)pb, (unsigned long long)pe);
+    const uint64_t d = c->cfg.dim;
+    if (host && cap_floats < (uint64_t)(row_end - row_begin) * d)
+        return fail(c, NE_ERANGE, "capacity %zu < %llu floats", cap_floats,
+                    (unsigned long long)((row_end - row_begin) * d));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));
+    auto copy = [&](float* dev_base, uint64_t base_row, uint64_t a, uint64_t b) -> int {
+        if (a >= b) return NE_OK;
+        float* dptr = dev_base + (a - base_row) * d;
+        const size_t off = (a - row_begin) * d, bytes = (b - a) * d * sizeof(float);
+        if (host) NE_CUDA(c, cudaMemcpy(host + off, dptr, bytes, cudaMemcpyDefault));
+        else NE_CUDA(c, cudaMemcpy(dptr, in + off, bytes, cudaMemcpyDefault));
+        return NE_OK;
+    };
+    if (which == NE_CONTEXT) return copy(c->d_C, c->c_begin, row_begin, row_end);
+    const uint32_t k = c->cfg.subparts;
+    for (uint32_t t = 0; t < k; ++t) {
+        const size_t vs = (size_t)c->rank * k + t;
+        const uint64_t sb = c->sub_bounds[vs], se = c->sub_bounds[vs + 1];
+        NE_TRY(copy(c->vslot[c->cur * k + t], sb, std::max<uint64_t>(sb, row_begin),
+                    std::min<uint64_t>(se, row_end)));
+    }
+    return NE_OK;
+}
+
+int ne_get_embeddings(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, float* host_out,
+                      size_t cap_floats) {
+    if (!host_out) return c ? fail(c, NE_EINVAL, "null output") : NE_EINVAL;
+    return rows_op(c, which, row_begin, row_end, host_out, nullptr, cap_floats);
+}
+
+int ne_set_embeddings(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, const float* in) {
+    if (!in) return c ? fail(c, NE_EINVAL, "null input") : NE_EINVAL;
+    return rows_op(c, which, row_begin, row_end, nullptr, in, 0);
+}
+
+int ne_export_samples(ne_ctx* c, uint32_t vsub, uint32_t* pairs_out, size_t cap_pairs, uint64_t* count) {
+    NE_TRY(enter(c));
+    NE_TRY(check_loaded(c));
+    if (c->built_episode < 0) return fail(c, NE_ESTATE, "no sample pool built");
+    if (vsub >= nb_local(c)) return fail(c, NE_ERANGE, "vsub=%u >= %u", vsub, nb_local(c));
+    const uint64_t cnt = c->boff[vsub + 1] - c->boff[vsub];
+    if (count) *count = cnt;
+    if (!pairs_out) return NE_OK;
+    if (cap_pairs < cnt) return fail(c, NE_ERANGE, "capacity %zu < %llu pairs", cap_pairs, (unsigned long long)cnt);
+    if (cnt) NE_CUDA(c, cudaMemcpy(pairs_out, c->d_pool + c->boff[vsub], cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return NE_OK;
+}
+
+int ne_export_negatives(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vsub, uint64_t pos_begin,
+                        uint64_t count, uint32_t* out) {
+    NE_TRY(enter(c));
+    NE_TRY(check_loaded(c));
+    if (vsub >= nb_local(c)) return fail(c, NE_ERANGE, "vsub=%u >= %u", vsub, nb_local(c));
+    if (!out && count) return fail(c, NE_EINVAL, "null output");
+    const uint64_t total = count * c->cfg.negatives;
+    if (total == 0) return NE_OK;
+    if (c->tmp_u32_cap < total) {
+        NE_TRY(dalloc_t(c, &c->d_tmp_u32, total));
+        c->tmp_u32_cap = total;
+    }
+    ne::SgnsParams p{};
+    p.c_begin = c->c_begin;
+    p.c_count = c->c_count;
+    p.alias = c->d_alias;
+    p.K = c->cfg.negatives;
+    p.seed = c->cfg.seed;
+    p.epoch = epoch;
+    p.episode = episode;
+    p.block = vsub * (uint32_t)c->world + (uint32_t)c->rank;
+    NE_CUDA(c, ne::launch_export_negatives(p, pos_begin, count, c->d_tmp_u32, c->dev, c->stream));
+    c->launches += 1;
+    NE_CUDA(c, cudaMemcpyAsync(out, c->d_tmp_u32, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    return NE_OK;
+}
+
+const char* ne_last_error(const ne_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+void ne_destroy(ne_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    free_all(c);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->d_loss) cudaFree(c->d_loss);
+    if (c->d_bad) cudaFree(c->d_bad);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,273 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bit-exact for walks, pools and negatives (integer work,
+shared Philox contract), max-abs 1e-4 for deterministic-mode embeddings after
+one epoch (BASELINE.json north_star), AUC within 0.01 for the Hogwild
+production mode."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # north_star: deterministic-mode embeddings within max-abs 1e-4 (fp32)
+
+
+def engine(**kw):
+    from paper_2005_13789_b200.engine import Engine
+    base = dict(dim=128, negatives=5, walk_len=40, window=5, walks_per_node=1, episodes=1,
+                subparts=4, deterministic=True, seed=42, device=0)
+    base.update(kw)
+    return Engine(**base)
+
+
+def ocfg(**kw):
+    base = dict(dim=128, negatives=5, walk_len=40, window=5, walks_per_node=1, episodes=1,
+                subparts=4, parts=1, seed=42)
+    base.update(kw)
+    return oracle.Config(**base)
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return synth.workload_graph("c1")
+
+
+# ---------------------------------------------------------------- O9 init
+def test_init_bit_exact(c1):
+    off, tgt = c1
+    n = len(off) - 1
+    for d in (128, 96, 100):
+        eng = engine(dim=d)
+        eng.load_graph(off, tgt)
+        assert np.array_equal(eng.embeddings(0), oracle.init_vertex(n, d, 42))
+        assert not eng.embeddings(1).any()
+        eng.close()
+
+
+# ---------------------------------------------------------------- O4 walks
+@pytest.mark.parametrize("epoch", [0, 5])
+def test_walks_bit_exact_c1(c1, epoch):
+    off, tgt = c1
+    n = len(off) - 1
+    eng = engine(walks_per_node=2, episodes=3)
+    eng.load_graph(off, tgt)
+    for e in range(3):
+        walks = eng.random_walk(epoch, e, export=True)
+        u0, units = oracle.episode_units(ocfg(walks_per_node=2, episodes=3), n, len(tgt), e)
+        assert walks.shape == (units, 41)
+        for w in range(units):
+            ref = oracle.random_walk(off, tgt, 42, epoch, u0 + w, 40)
+            assert np.array_equal(walks[w, :len(ref)], ref)
+            assert (walks[w, len(ref):] == 0xFFFFFFFF).all()
+    eng.close()
+
+
+# ---------------------------------------------------------------- O5/O6 pools
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_pool_bit_exact_c1(c1, P):
+    off, tgt = c1
+    k = 4
+    ref, boff = oracle.build_episode(ocfg(parts=P, subparts=k), off, tgt, 2, 0)
+    for g in range(P):
+        eng = engine(rank=g, world=P)
+        eng.load_graph(off, tgt)
+        eng.random_walk(2, 0)
+        total = eng.build_samples(2, 0)
+        got_total = 0
+        for vs in range(P * k):
+            B = vs * P + g
+            blk = eng.export_samples(vs)
+            assert np.array_equal(blk, ref[int(boff[B]):int(boff[B + 1])]), (P, g, vs)
+            got_total += len(blk)
+        assert got_total == total
+        eng.close()
+
+
+def test_pool_bit_exact_multi_episode_line(c1):
+    off, tgt = c1
+    for kw in (dict(episodes=3, walks_per_node=2, subparts=2), dict(walk_len=0, window=0, episodes=2)):
+        cfg = ocfg(**kw)
+        for e in range(cfg.episodes):
+            ref, boff = oracle.build_episode(cfg, off, tgt, 1, e)
+            eng = engine(**kw)
+            eng.load_graph(off, tgt)
+            if cfg.walk_len:
+                eng.random_walk(1, e)
+            eng.build_samples(1, e)
+            for vs in range(cfg.subparts):
+                assert np.array_equal(eng.export_samples(vs), ref[int(boff[vs]):int(boff[vs + 1])])
+            eng.close()
+
+
+# ---------------------------------------------------------------- O8 negatives
+@pytest.mark.parametrize("P", [1, 4])
+def test_negatives_bit_exact(c1, P):
+    off, tgt = c1
+    n = len(off) - 1
+    cfg = ocfg(parts=P)
+    thr, al = oracle.build_alias_tables(cfg, off)
+    pb = oracle.partition_bounds(0, n, P).astype(np.int64)
+    rng = np.random.default_rng(0)
+    for g in range(P):
+        eng = engine(rank=g, world=P)
+        eng.load_graph(off, tgt)
+        for vs in (0, P * 4 - 1):
+            got = eng.export_negatives(7, 3, vs, 1000, 2000)
+            for i in rng.integers(0, 2000, 300):
+                ref = oracle.negatives(cfg, thr, al, int(pb[g]), int(pb[g + 1] - pb[g]), 7, 3,
+                                       vs * P + g, 1000 + int(i))
+                assert np.array_equal(got[i], ref)
+        eng.close()
+
+
+# ---------------------------------------------------------------- O10/O11 training
+def _det_epoch(off, tgt, epochs=1, lr=0.025, **kw):
+    n = len(off) - 1
+    cfg = ocfg(**kw)
+    eng = engine(**kw)
+    eng.load_graph(off, tgt)
+    V = oracle.init_vertex(n, cfg.dim, 42)
+    Cm = np.zeros_like(V)
+    for ep in range(epochs):
+        st = eng.train_epoch(ep, lr)
+        ns, loss = oracle.train_epoch(cfg, off, tgt, V, Cm, ep, lr)
+        assert st["samples"] == ns
+        assert abs(st["loss_sum"] - loss) <= 1e-3 * abs(loss) + 1e-6
+    dv = np.abs(eng.embeddings(0) - V).max()
+    dc = np.abs(eng.embeddings(1) - Cm).max()
+    eng.close()
+    return dv, dc
+
+
+def test_deterministic_epoch_c1():
+    off, tgt = synth.workload_graph("c1")
+    dv, dc = _det_epoch(off, tgt)
+    assert dv <= TOL and dc <= TOL, (dv, dc)
+
+
+@pytest.mark.parametrize("kw", [
+    dict(dim=4, negatives=0, walk_len=5, window=2),
+    dict(dim=96, negatives=8, walk_len=12, window=4, subparts=3, episodes=2),
+    dict(dim=256, negatives=2, walk_len=8, window=8, walks_per_node=3),
+    dict(dim=100, negatives=5, walk_len=0, window=0, episodes=2),
+])
+def test_deterministic_shapes(kw):
+    off, tgt = synth.rmat_graph(700, 4000, 3)
+    dv, dc = _det_epoch(off, tgt, epochs=2, **kw)
+    assert dv <= TOL and dc <= TOL, (dv, dc)
+
+
+def test_reuse_samples_and_repeat():
+    off, tgt = synth.rmat_graph(300, 2000, 4)
+    n = len(off) - 1
+    eng = engine(dim=32)
+    eng.load_graph(off, tgt)
+    eng.train_epoch(0, 0.025)
+    eng.train_epoch(1, 0.025, reuse=True)  # walk reuse: same pool, epoch-1 negatives
+    cfg = ocfg(dim=32)
+    V = oracle.init_vertex(n, 32, 42)
+    Cm = np.zeros_like(V)
+    oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025)
+    # replay the epoch-0 pool with epoch-1 negatives
+    pairs, boff = oracle.build_episode(cfg, off, tgt, 0, 0)
+    thr, al = oracle.build_alias_tables(cfg, off)
+    for t in range(4):
+        for p in range(int(boff[t + 1] - boff[t])):
+            s, d = pairs[int(boff[t]) + p]
+            negs = oracle.negatives(cfg, thr, al, 0, n, 1, 0, t, p)
+            oracle.train_sample(V, Cm, int(s), int(d), negs, 0.025)
+    assert np.abs(eng.embeddings(0) - V).max() <= TOL
+    assert np.abs(eng.embeddings(1) - Cm).max() <= TOL
+    eng.close()
+
+
+def test_hogwild_auc_matches_oracle():
+    n = 2000
+    u, v = synth.planted_partition_edges(n, 20, 12.0, 1.0, 17)
+    off, tgt, test = synth.split_edges(n, u, v, 0.1, 7)
+    neg = synth.negative_pairs(n, u, v, len(test), 8)
+    kw = dict(dim=32, walk_len=20, window=3, walks_per_node=4, subparts=1)
+    cfg = ocfg(**kw)
+    V = oracle.init_vertex(n, 32, 42)
+    Cm = np.zeros_like(V)
+    for ep in range(2):
+        oracle.train_epoch(cfg, off, tgt, V, Cm, ep, 0.05)
+    a_ref = oracle.auc(oracle.score_pairs(V, Cm, test), oracle.score_pairs(V, Cm, neg))
+    aucs = []
+    for seed_run in range(3):
+        eng = engine(deterministic=False, **kw)
+        eng.load_graph(off, tgt)
+        for ep in range(2):
+            eng.train_epoch(ep, 0.05)
+        Vg, Cg = eng.embeddings(0), eng.embeddings(1)
+        aucs.append(oracle.auc(oracle.score_pairs(Vg, Cg, test), oracle.score_pairs(Vg, Cg, neg)))
+        eng.close()
+    assert all(abs(a - a_ref) <= 0.01 for a in aucs), (a_ref, aucs)
+
+
+# ---------------------------------------------------------------- edges and errors
+def test_empty_and_isolated_graphs():
+    off = np.zeros(11, np.uint64)
+    tgt = np.zeros(0, np.uint32)
+    eng = engine(dim=8)
+    eng.load_graph(off, tgt)
+    walks = eng.random_walk(0, 0, export=True)
+    assert (walks[:, 0] == np.arange(10)).all() and (walks[:, 1:] == 0xFFFFFFFF).all()
+    assert eng.build_samples(0, 0) == 0
+    st = eng.train_samples(0, 0, 0.025)
+    assert st["samples"] == 0
+    assert np.array_equal(eng.embeddings(0), oracle.init_vertex(10, 8, 42))
+    eng.close()
+
+
+def test_invalid_csr_rejected():
+    from paper_2005_13789_b200 import ne
+    eng = engine(dim=8)
+    with pytest.raises(ne.NEError, match=r"NE_EINVAL: offsets\[2\]=1 < offsets\[1\]=3"):
+        eng.load_graph(np.array([0, 3, 1, 4], np.uint64), np.array([1, 2, 0, 1], np.uint32))
+    with pytest.raises(ne.NEError, match=r"NE_EINVAL: targets\[1\]=7 >= n=3"):
+        eng.load_graph(np.array([0, 1, 2, 2], np.uint64), np.array([1, 7], np.uint32))
+    with pytest.raises(ne.NEError, match=r"NE_EINVAL: offsets\[3\]=2 != nnz=3"):
+        eng.load_graph(np.array([0, 1, 2, 2], np.uint64), np.array([1, 2, 0], np.uint32))
+    with pytest.raises(ne.NEError, match="NE_ESTATE"):
+        eng.train_epoch(0, 0.1)
+    off, tgt = synth.chain_graph(5)
+    eng.load_graph(off, tgt)
+    with pytest.raises(ne.NEError, match="NE_ESTATE"):
+        eng.build_samples(0, 0)  # no walks yet
+    with pytest.raises(ne.NEError, match="NE_ERANGE"):
+        eng.embeddings(0, rows=(0, 6))
+    eng.close()
+
+
+# ---------------------------------------------------------------- full size (C2)
+def test_c2_full_size_sampled():
+    off, tgt = synth.workload_graph("c2")
+    n = len(off) - 1
+    eng = engine(deterministic=False)
+    eng.load_graph(off, tgt)
+    walks = eng.random_walk(0, 0, export=True)
+    rng = np.random.default_rng(1)
+    for w in rng.integers(0, n, 3000):
+        ref = oracle.random_walk(off, tgt, 42, 0, int(w), 40)
+        assert np.array_equal(walks[w, :len(ref)], ref)
+    lens = (walks != 0xFFFFFFFF).sum(1)
+    expect = sum(np.maximum(lens - dl, 0).sum() for dl in range(1, 6))
+    total = eng.build_samples(0, 0)
+    assert total == expect
+    cfg = ocfg()
+    thr, al = oracle.build_alias_tables(cfg, off)
+    for vs in range(4):
+        blk = eng.export_samples(vs)
+        sb = oracle.partition_bounds(0, n, 4).astype(np.int64)
+        assert ((blk[:, 0] >= sb[vs]) & (blk[:, 0] < sb[vs + 1])).all()
+        for p in rng.integers(0, len(blk), 200):
+            got = eng.export_negatives(0, 0, vs, int(p), 1)[0]
+            assert np.array_equal(got, oracle.negatives(cfg, thr, al, 0, n, 0, 0, vs, int(p)))
+    st = eng.train_samples(0, 0, 0.025)
+    assert st["samples"] == total and np.isfinite(st["loss_sum"])
+    V = eng.embeddings(0)
+    assert np.isfinite(V).all()
+    eng.close()

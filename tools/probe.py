@@ -1,0 +1,23 @@
+"""Quick perf probe: time walk/build/train of one epoch on a workload."""
+import sys, time
+sys.path.insert(0, ".")
+import numpy as np
+import synth
+from paper_2005_13789_b200.engine import Engine
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c2"
+epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+t = time.time()
+off, tgt = synth.workload_graph(name)
+print(f"{name}: graph n={len(off)-1} nnz={len(tgt)} gen {time.time()-t:.1f}s", flush=True)
+w = synth.CONFIGS[name]
+eng = Engine(dim=w.dim, deterministic=False)
+t = time.time(); eng.load_graph(off, tgt); print(f"load {time.time()-t:.2f}s", flush=True)
+for ep in range(epochs):
+    t = time.time()
+    st = eng.train_epoch(ep, 0.025)
+    wall = time.time() - t
+    B = 8 + 8 * 5 + 8 * w.dim * 7
+    print(f"epoch {ep}: wall {wall:.3f}s samples {st['samples']} walk {st['ms_walk']:.1f}ms build {st['ms_build']:.1f}ms "
+          f"train {st['ms_train']:.1f}ms -> {st['samples']/st['ms_train']/1e3:.1f} M samples/s kernel, "
+          f"{st['samples']*B/st['ms_train']/1e6:.0f} GB/s alg; loss/sample {st['loss_sum']/max(st['samples'],1)/6:.4f}", flush=True)
