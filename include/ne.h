@@ -56,6 +56,9 @@ enum {
                               walking anew (walk reuse); needs episodes == 1 */
 };
 
+/* ne_config.writeback */
+enum { NE_WB_ATOMIC_DELTA = 0, NE_WB_STORE = 1 };
+
 /* ne_get_embeddings / ne_set_embeddings: which matrix. */
 enum { NE_VERTEX = 0, NE_CONTEXT = 1 };
 
@@ -80,11 +83,18 @@ typedef struct {
     uint32_t subparts;       /* vertex sub-parts per GPU, the paper's k = 4    */
     uint32_t deterministic;  /* 1: one warp per block in canonical order (parity mode);
                                 0: Hogwild production mode (lock-free warps)            */
-    uint32_t rows_per_warp;  /* Hogwild concurrency cap: at most min(vertex rows, context
-                                rows) / rows_per_warp warps train a block at once, so
-                                small blocks are not swamped by lost updates (0 = 64);
-                                blocks of large graphs fill the GPU regardless          */
-    uint32_t reserved;       /* must be 0                                               */
+    uint32_t conflict_permille; /* Hogwild concurrency cap: at most
+                                (permille/1000) / ((1+K)^2/ctx_rows + 1/vertex_rows)
+                                warps train a block at once -- the expected share of
+                                in-flight samples sharing a row with another one under
+                                uniform access.  0 = 300 (30 %); >= 1000000 = no cap.
+                                Large graphs fill the GPU below the cap.            */
+    uint32_t writeback;      /* Hogwild row write-back: NE_WB_ATOMIC_DELTA (0, default)
+                                adds each update's delta with a vector reduction
+                                (red.global.add.v4.f32), so concurrent updates of a
+                                row are never erased; NE_WB_STORE (1) stores the new
+                                rows (word2vec-style, loses concurrent updates).
+                                Deterministic mode always stores.                   */
     uint64_t seed;           /* Philox key (contract R1)                                */
 } ne_config;
 
@@ -202,6 +212,17 @@ int ne_export_samples(ne_ctx *ctx, uint32_t vsub, uint32_t *pairs_out, size_t ca
  * SGNS kernel uses (O8); out = count*K u32 (global node ids). */
 int ne_export_negatives(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint32_t vsub,
                         uint64_t pos_begin, uint64_t count, uint32_t *out);
+
+/* Single-GPU emulation of the P-rank ring for parity tests: ctxs[g] are
+ * layout-only contexts (ne_init_dist(ctx, g, world, NULL)) on ONE device, each
+ * with the pool of `episode` built.  Runs the same plan as ne_train_samples
+ * (round r, slot t, rank g, in that order, all on ctxs[0]'s stream) with the
+ * send to rank g+1 replaced by handing the trained sub-part buffer to context
+ * g+1.  After the call every sub-part is home again.  stats (nullable) sums all
+ * ranks.  Errors: NE_EINVAL (contexts not ranks 0..world-1 of one device),
+ * NE_ESTATE (pool missing). */
+int ne_train_samples_local_ring(ne_ctx *const *ctxs, uint32_t world, uint32_t epoch,
+                                uint32_t episode, float lr, ne_stats *stats);
 
 /* The host-side ring schedule (O7), no device needed: the vertex sub-part
  * rank g trains at round r, slot t, with `world` ranks and `subparts` slots.

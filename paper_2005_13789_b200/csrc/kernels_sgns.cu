@@ -12,7 +12,9 @@
 // are written once.  Repeated context ids inside a sample are forwarded in
 // registers so the result equals the sequential Alg. 1 order (reading D2).
 // Negatives (O8) are drawn by lanes 0..K-1 in parallel (one Philox each) and
-// broadcast with shuffles.
+// broadcast with shuffles.  The next sample's pair and negatives (pool load,
+// Philox, alias load) are fetched while the current sample's rows are in
+// flight, so the dependent chain pair -> alias -> rows is off the critical path.
 //
 // Production mode: a persistent grid of warps strides over the block's
 // samples, updating rows in place without locks (Hogwild; races only between
@@ -20,6 +22,7 @@
 // block in canonical order -- the same device code, so parity of the
 // deterministic mode is parity of the production arithmetic.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ne_device.cuh"
 #include "ne_internal.h"
@@ -47,36 +50,51 @@ __device__ __forceinline__ float warp_sum(float x) {
     return x;
 }
 
-template <int R>
-__global__ void __launch_bounds__(kSgnsThreads) sgns_kernel(SgnsParams p) {
+// R: float4 per lane per row.  KT: compile-time K (0 = runtime K <= kMaxK).
+// MINB: min resident CTAs per SM for __launch_bounds__ (register budget).
+// ADD: Hogwild write-back by vector reduction (red.global.add.v4.f32) of each
+// row's delta instead of a plain store of the new row, so concurrent samples
+// sharing a row never erase each other's updates (they only read stale values).
+template <int R, int KT, int MINB, bool ADD>
+__global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) {
+    constexpr int KM = KT > 0 ? KT : kMaxK;
+    const int K = KT > 0 ? KT : (int)p.K;
     const uint32_t lane = lane_id();
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t q = p.d >> 2;  // float4 per row
     const uint2 key = key_of(p.seed);
     const uint32_t tagw = tag_word(kTagNeg, p.epoch);
-    const int K = (int)p.K;
     double loss = 0.0;  // lane 0
 
-    for (uint64_t pos = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; pos < p.count;
-         pos += nwarps) {
-        const uint2 pr = p.pool[pos];  // (src, dst), one broadcast transaction
-        const uint32_t my_neg = lane < p.K ? draw_negative(p, key, tagw, pos, lane) : 0u;
-
-        uint32_t ids[kMaxK + 1];
-        ids[0] = pr.y;
+    uint64_t pos = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint2 pr = make_uint2(0, 0);
+    uint32_t my_neg = 0;
+    if (pos < p.count) {
+        pr = p.pool[pos];
+        my_neg = (int)lane < K ? draw_negative(p, key, tagw, pos, lane) : 0u;
+    }
+    for (; pos < p.count; pos += nwarps) {
+        // ids[0] = positive context, ids[1..K] = negatives; lane j < 1+K holds ids[j]
+        const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, my_neg, 1);
+        const uint32_t my_id = lane == 0 ? pr.y : up;
+        uint32_t ids[KM + 1];
 #pragma unroll
-        for (int j = 0; j < kMaxK; ++j) ids[j + 1] = __shfl_sync(0xFFFFFFFFu, my_neg, j);
+        for (int j = 0; j <= KM; ++j) ids[j] = __shfl_sync(0xFFFFFFFFu, my_id, j);
+        // a repeated context id inside the sample is rare: detect it once per sample
+        const uint64_t mkey = (int)lane <= K ? (uint64_t)my_id : ((1ull << 32) | lane);
+        const bool dup = __any_sync(0xFFFFFFFFu, __popc(__match_any_sync(0xFFFFFFFFu, mkey)) > 1);
 
         float4* vrow = reinterpret_cast<float4*>(p.V + (uint64_t)(pr.x - p.v_begin) * p.d);
-        float4 v[R];
-        float4 c[kMaxK + 1][R];
+        float4 v[R], v0[ADD ? R : 1];
+        float4 c[KM + 1][R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t e = lane + 32u * r;
             v[r] = e < q ? vrow[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+            if constexpr (ADD) v0[r] = v[r];
         }
 #pragma unroll
-        for (int j = 0; j <= kMaxK; ++j) {
+        for (int j = 0; j <= KM; ++j) {
             if (j <= K) {
                 const float4* crow = reinterpret_cast<const float4*>(p.C + (uint64_t)(ids[j] - p.c_begin) * p.d);
 #pragma unroll
@@ -87,16 +105,29 @@ __global__ void __launch_bounds__(kSgnsThreads) sgns_kernel(SgnsParams p) {
             }
         }
 
+        // Prefetch the next sample's pair and negatives while the rows load.
+        const uint64_t nxt = pos + nwarps;
+        if (nxt < p.count) {
+            pr = p.pool[nxt];
+            my_neg = (int)lane < K ? draw_negative(p, key, tagw, nxt, lane) : 0u;
+        }
+
         // Alg. 1 lines 10 and 12: positive, then the K negatives, in order.
 #pragma unroll
-        for (int j = 0; j <= kMaxK; ++j) {
+        for (int j = 0; j <= KM; ++j) {
             if (j <= K) {
+                bool last = true;  // no later occurrence of ids[j] in this sample
+                if (dup) {
 #pragma unroll
-                for (int i = 0; i < j; ++i)  // forward the latest copy of a repeated id
-                    if (ids[i] == ids[j]) {
+                    for (int i = 0; i < j; ++i)  // forward the latest copy of a repeated id
+                        if (ids[i] == ids[j]) {
 #pragma unroll
-                        for (int r = 0; r < R; ++r) c[j][r] = c[i][r];
-                    }
+                            for (int r = 0; r < R; ++r) c[j][r] = c[i][r];
+                        }
+#pragma unroll
+                    for (int i = j + 1; i <= KM; ++i)
+                        if (i <= K && ids[i] == ids[j]) last = false;
+                }
                 float part = 0.f;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
@@ -111,6 +142,7 @@ __global__ void __launch_bounds__(kSgnsThreads) sgns_kernel(SgnsParams p) {
                 const float a = p.lr * g;
                 if (lane == 0)  // -log s (y = 1) or -log(1 - s) (y = 0), as softplus
                     loss += (double)__logf(1.f + __expf(j == 0 ? -x : x));
+                float4* crow = reinterpret_cast<float4*>(p.C + (uint64_t)(ids[j] - p.c_begin) * p.d);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const float4 vo = v[r], co = c[j][r];
@@ -118,59 +150,82 @@ __global__ void __launch_bounds__(kSgnsThreads) sgns_kernel(SgnsParams p) {
                                        fmaf(-a, co.z, vo.z), fmaf(-a, co.w, vo.w));
                     c[j][r] = make_float4(fmaf(-a, vo.x, co.x), fmaf(-a, vo.y, co.y),
                                           fmaf(-a, vo.z, co.z), fmaf(-a, vo.w, co.w));
+                    const uint32_t e = lane + 32u * r;
+                    if (e < q) {
+                        if constexpr (ADD)  // this update's delta, at every occurrence
+                            atomicAdd(crow + e, make_float4(-a * vo.x, -a * vo.y, -a * vo.z, -a * vo.w));
+                        else if (last)      // the row's final value, once
+                            crow[e] = c[j][r];
+                    }
                 }
             }
         }
-
-        // Fused write-back of 2+K rows (the last copy of a repeated id wins).
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t e = lane + 32u * r;
-            if (e < q) vrow[e] = v[r];
-        }
-#pragma unroll
-        for (int j = 0; j <= kMaxK; ++j) {
-            if (j <= K) {
-                bool last = true;
-#pragma unroll
-                for (int i = j + 1; i <= kMaxK; ++i)
-                    if (i <= K && ids[i] == ids[j]) last = false;
-                if (last) {
-                    float4* crow = reinterpret_cast<float4*>(p.C + (uint64_t)(ids[j] - p.c_begin) * p.d);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const uint32_t e = lane + 32u * r;
-                        if (e < q) crow[e] = c[j][r];
-                    }
-                }
+            if (e < q) {
+                if constexpr (ADD)
+                    atomicAdd(vrow + e, make_float4(v[r].x - v0[r].x, v[r].y - v0[r].y,
+                                                    v[r].z - v0[r].z, v[r].w - v0[r].w));
+                else
+                    vrow[e] = v[r];
             }
         }
     }
     if (lane == 0 && loss != 0.0) atomicAdd(p.loss, loss);
 }
 
-template <int R>
-static cudaError_t launch_sgns_r(const SgnsParams& p, const Device& dev, cudaStream_t s) {
-    if (p.deterministic) {
-        sgns_kernel<R><<<1, 32, 0, s>>>(p);
-    } else {
-        int per_sm = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sgns_kernel<R>,
-                                                                      kSgnsThreads, 0);
-        if (e != cudaSuccess) return e;
-        per_sm = std::max(per_sm, 1);
-        const uint64_t warps = std::min<uint64_t>(p.count, std::max<uint64_t>(p.max_warps, 1));
-        const uint64_t full = (uint64_t)dev.sm_count * per_sm;
-        const int wpb = kSgnsThreads / 32;
-        if (warps >= full * wpb) {
-            sgns_kernel<R><<<(unsigned)full, kSgnsThreads, 0, s>>>(p);
-        } else if (warps >= (uint64_t)dev.sm_count * wpb) {
-            sgns_kernel<R><<<(unsigned)((warps + wpb - 1) / wpb), kSgnsThreads, 0, s>>>(p);
-        } else {  // small capped grids: spread single warps over the SMs
-            sgns_kernel<R><<<(unsigned)warps, 32, 0, s>>>(p);
-        }
+template <int R, int KT, int MINB>
+static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStream_t s) {
+    if (p.deterministic) {  // one warp, canonical order, plain stores
+        sgns_kernel<R, KT, MINB, false><<<1, 32, 0, s>>>(p);
+        return cudaGetLastError();
+    }
+    auto kern = p.atomic_writeback ? sgns_kernel<R, KT, MINB, true> : sgns_kernel<R, KT, MINB, false>;
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSgnsThreads, 0);
+    if (e != cudaSuccess) return e;
+    per_sm = std::max(per_sm, 1);
+    const uint64_t warps = std::min<uint64_t>(p.count, std::max<uint64_t>(p.max_warps, 1));
+    const uint64_t full = (uint64_t)dev.sm_count * per_sm;
+    const int wpb = kSgnsThreads / 32;
+    if (warps >= full * wpb) {
+        kern<<<(unsigned)full, kSgnsThreads, 0, s>>>(p);
+    } else if (warps >= (uint64_t)dev.sm_count * wpb) {
+        kern<<<(unsigned)((warps + wpb - 1) / wpb), kSgnsThreads, 0, s>>>(p);
+    } else {  // small capped grids: spread single warps over the SMs
+        kern<<<(unsigned)warps, 32, 0, s>>>(p);
     }
     return cudaGetLastError();
+}
+
+// Occupancy variant (developer knob NE_SGNS_MINB = 1..4, default 3): the
+// register budget __launch_bounds__(256, MINB) gives the compiler.
+static int sgns_minb() {
+    static int v = [] {
+        const char* e = std::getenv("NE_SGNS_MINB");
+        const int x = e ? std::atoi(e) : 3;
+        return (x >= 1 && x <= 4) ? x : 3;
+    }();
+    return v;
+}
+
+template <int R, int KT>
+static cudaError_t launch_sgns_k(const SgnsParams& p, const Device& dev, cudaStream_t s) {
+    // a runtime K keeps kMaxK+1 context rows live: cap the budget so it does not spill
+    const int minb = KT == 0 ? std::min(sgns_minb(), 2) : sgns_minb();
+    switch (minb) {
+        case 1: return launch_sgns_v<R, KT, 1>(p, dev, s);
+        case 2: return launch_sgns_v<R, KT, 2>(p, dev, s);
+        case 4: return launch_sgns_v<R, KT, 4>(p, dev, s);
+        default: return launch_sgns_v<R, KT, 3>(p, dev, s);
+    }
+}
+
+template <int R>
+static cudaError_t launch_sgns_r(const SgnsParams& p, const Device& dev, cudaStream_t s) {
+    if (p.K == 5) return launch_sgns_k<R, 5>(p, dev, s);  // the paper's K (tab:perf)
+    return launch_sgns_k<R, 0>(p, dev, s);
 }
 
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s) {

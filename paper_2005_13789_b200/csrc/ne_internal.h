@@ -67,6 +67,7 @@ struct SgnsParams {
     double* loss;               // += sum of loss terms (device)
     int deterministic;          // 1: one warp, canonical order
     uint64_t max_warps;         // Hogwild concurrency cap (>= 1)
+    int atomic_writeback;       // Hogwild: red.add row deltas instead of storing rows
 };
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s);
 cudaError_t launch_export_negatives(const SgnsParams& p, uint64_t pos_begin, uint64_t count,

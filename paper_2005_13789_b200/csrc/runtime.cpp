@@ -311,9 +311,13 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
     p.block = vsub * (uint32_t)c->world + (uint32_t)c->rank;
     p.loss = c->d_loss;
     p.deterministic = (int)c->cfg.deterministic;
-    const uint64_t rpw = c->cfg.rows_per_warp ? c->cfg.rows_per_warp : 64;
-    const uint64_t rows = std::min<uint64_t>(c->sub_bounds[vsub + 1] - c->sub_bounds[vsub], c->c_count);
-    p.max_warps = std::max<uint64_t>(1, rows / rpw);
+    const double eps = (c->cfg.conflict_permille ? c->cfg.conflict_permille : 300) / 1000.0;
+    const double kk = (1.0 + c->cfg.negatives) * (1.0 + c->cfg.negatives);
+    const double vr = (double)std::max<uint64_t>(1, c->sub_bounds[vsub + 1] - c->sub_bounds[vsub]);
+    const double cr = (double)std::max<uint64_t>(1, c->c_count);
+    const double cap = eps / (kk / cr + 1.0 / vr);
+    p.max_warps = cap >= 1e15 ? ~0ull : std::max<uint64_t>(1, (uint64_t)cap);
+    p.atomic_writeback = c->cfg.writeback == NE_WB_ATOMIC_DELTA ? 1 : 0;
     return p;
 }
 
@@ -440,7 +444,7 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
         return bad(fail(c, NE_EINVAL, "walks_per_node must be >= 1"));
     if (g.episodes == 0 || g.episodes > 4095)
         return bad(fail(c, NE_EINVAL, "episodes=%u not in [1, 4095]", g.episodes));
-    if (g.reserved != 0) return bad(fail(c, NE_EINVAL, "reserved field must be 0"));
+    if (g.writeback > NE_WB_STORE) return bad(fail(c, NE_EINVAL, "writeback=%u not in {0, 1}", g.writeback));
     if (g.subparts == 0 || g.subparts > 256)
         return bad(fail(c, NE_EINVAL, "subparts=%u not in [1, 256]", g.subparts));
     int ndev = 0;
@@ -776,6 +780,46 @@ int ne_export_negatives(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vs
     c->launches += 1;
     NE_CUDA(c, cudaMemcpyAsync(out, c->d_tmp_u32, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    return NE_OK;
+}
+
+int ne_train_samples_local_ring(ne_ctx* const* ctxs, uint32_t world, uint32_t epoch,
+                                uint32_t episode, float lr, ne_stats* stats) {
+    if (!ctxs || world == 0) return NE_EINVAL;
+    ne_ctx* c0 = ctxs[0];
+    NE_TRY(enter(c0));
+    const uint32_t k = c0->cfg.subparts;
+    for (uint32_t g = 0; g < world; ++g) {
+        ne_ctx* c = ctxs[g];
+        if (!c || !c->loaded || c->comm || c->world != (int)world || c->rank != (int)g ||
+            c->device != c0->device || c->cfg.subparts != k || c->cfg.dim != c0->cfg.dim)
+            return fail(c0, NE_EINVAL, "context %u is not layout-only rank %u of %u on device %d", g, g, world,
+                        c0->device);
+        if (c->built_episode != (int64_t)episode)
+            return fail(c0, NE_ESTATE, "context %u has no pool for episode %u", g, episode);
+    }
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    NE_CUDA(c0, cudaMemsetAsync(c0->d_loss, 0, sizeof(double), c0->stream));
+    // Every rank's launches go to rank 0's stream, in plan order: round r, slot t,
+    // rank g; the "send to g+1" is a pointer hand-over of the trained slot.
+    std::vector<float*> moved(world);
+    for (uint32_t r = 0; r < world; ++r)
+        for (uint32_t t = 0; t < k; ++t) {
+            for (uint32_t g = 0; g < world; ++g) {
+                ne_ctx* c = ctxs[g];
+                const uint32_t vs = (uint32_t)plan_vsub(world, k, r, t, g);
+                ne::SgnsParams sp = sgns_params(c, vs, c->vslot[c->cur * k + t], epoch, episode, lr);
+                sp.loss = c0->d_loss;
+                NE_CUDA(c0, ne::launch_sgns(sp, c->dev, c0->stream));
+                if (stats) { stats->samples += sp.count; if (sp.count) stats->train_launches += 1; }
+            }
+            for (uint32_t g = 0; g < world; ++g) moved[(g + 1) % world] = ctxs[g]->vslot[ctxs[g]->cur * k + t];
+            for (uint32_t g = 0; g < world; ++g) ctxs[g]->vslot[ctxs[g]->cur * k + t] = moved[g];
+        }
+    double loss = 0.0;
+    NE_CUDA(c0, cudaMemcpyAsync(&loss, c0->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c0->stream));
+    NE_CUDA(c0, cudaStreamSynchronize(c0->stream));
+    if (stats) { stats->loss_sum = loss; stats->kernel_launches = stats->train_launches; }
     return NE_OK;
 }
 

@@ -24,13 +24,14 @@ _lib = C.CDLL(LIB_PATH)
 NE_OK, NE_EINVAL, NE_ERANGE, NE_ENOMEM, NE_ESTATE, NE_ECUDA, NE_ENCCL, NE_ESCHED = 0, -1, -2, -3, -4, -5, -6, -7
 NE_REUSE_SAMPLES = 1
 NE_VERTEX, NE_CONTEXT = 0, 1
+NE_WB_ATOMIC_DELTA, NE_WB_STORE = 0, 1
 
 
 class ne_config(C.Structure):
     _fields_ = [("dim", C.c_uint32), ("negatives", C.c_uint32), ("walk_len", C.c_uint32),
                 ("window", C.c_uint32), ("walks_per_node", C.c_uint32), ("episodes", C.c_uint32),
-                ("subparts", C.c_uint32), ("deterministic", C.c_uint32), ("rows_per_warp", C.c_uint32),
-                ("reserved", C.c_uint32), ("seed", C.c_uint64)]
+                ("subparts", C.c_uint32), ("deterministic", C.c_uint32), ("conflict_permille", C.c_uint32),
+                ("writeback", C.c_uint32), ("seed", C.c_uint64)]
 
 
 class ne_stats(C.Structure):
@@ -63,6 +64,8 @@ _sig = {
     "ne_destroy": (None, [_P]),
     "ne_export_samples": (C.c_int, [_P, C.c_uint32, _P, C.c_size_t, C.POINTER(C.c_uint64)]),
     "ne_export_negatives": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, _P]),
+    "ne_train_samples_local_ring": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
+                                             C.POINTER(ne_stats)]),
     "ne_plan_vsub": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
     "ne_partition_bounds": (C.c_int, [C.c_uint64, C.c_uint32, _P]),
 }
@@ -183,6 +186,13 @@ def ne_export_samples(ctx, vsub: int, out: np.ndarray | None = None) -> int:
 def ne_export_negatives(ctx, epoch: int, episode: int, vsub: int, pos_begin: int, count: int,
                         out: np.ndarray) -> None:
     _check(ctx, _lib.ne_export_negatives(ctx, epoch, episode, vsub, pos_begin, count, _ptr(out)))
+
+
+def ne_train_samples_local_ring(ctxs, epoch: int, episode: int, lr: float) -> ne_stats:
+    arr = (_P * len(ctxs))(*[c.value for c in ctxs])
+    st = ne_stats()
+    _check(ctxs[0], _lib.ne_train_samples_local_ring(arr, len(ctxs), epoch, episode, lr, C.byref(st)))
+    return st
 
 
 def ne_plan_vsub(world: int, subparts: int, r: int, t: int, g: int) -> int:

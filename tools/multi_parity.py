@@ -1,0 +1,58 @@
+"""torchrun worker: deterministic P-rank training over the real NCCL ring on P
+GPUs, compared with the oracle's P-part epoch (run by rank 0)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import oracle
+import synth
+from paper_2005_13789_b200 import ne
+from paper_2005_13789_b200.engine import Engine
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    mode = sys.argv[1] if len(sys.argv) > 1 else "det"
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    obj = [ne.ne_get_nccl_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    off, tgt = synth.workload_graph("c1")
+    n = len(off) - 1
+    eng = Engine(dim=128, deterministic=(mode == "det"), device=local, rank=rank, world=world,
+                 nccl_id=obj[0], episodes=2)
+    eng.load_graph(off, tgt)
+    stats = [eng.train_epoch(ep, 0.025) for ep in range(2)]
+    a, b = eng.part
+    V, Cm = eng.embeddings(0), eng.embeddings(1)
+    parts = [None] * world
+    dist.all_gather_object(parts, (a, b, V, Cm, stats))
+    if rank == 0:
+        cfg = oracle.Config(dim=128, negatives=5, walk_len=40, window=5, walks_per_node=1, episodes=2,
+                            subparts=4, parts=world, seed=42)
+        Vr = oracle.init_vertex(n, 128, 42)
+        Cr = np.zeros_like(Vr)
+        ns = 0
+        for ep in range(2):
+            ns += oracle.train_epoch(cfg, off, tgt, Vr, Cr, ep, 0.025)[0]
+        got_ns = sum(st["samples"] for p in parts for st in p[4])
+        assert got_ns == ns, (got_ns, ns)
+        dv = max(np.abs(p[2] - Vr[p[0]:p[1]]).max() for p in parts)
+        dc = max(np.abs(p[3] - Cr[p[0]:p[1]]).max() for p in parts)
+        print(f"MULTI {mode} world={world} samples={ns} max|dV|={dv:.3e} max|dC|={dc:.3e}", flush=True)
+        if mode == "det":
+            assert dv <= 1e-4 and dc <= 1e-4, (dv, dc)
+        else:
+            assert np.isfinite(dv) and np.isfinite(dc)
+    eng.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
