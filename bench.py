@@ -94,7 +94,8 @@ class Clocks:
 def workload_desc(name):
     import synth
     w = synth.CONFIGS[name]
-    return w, (f"{w.name} R-MAT (Graph500 a,b,c=.57,.19,.19) {w.n:,} nodes / {w.m:,} undirected edges "
+    gen = "R-MAT (Graph500 a,b,c=.57,.19,.19)" if w.kind == "rmat" else "uniform G(n,m)"
+    return w, (f"{w.name} {gen} {w.n:,} nodes / {w.m:,} undirected edges "
                f"(nnz {2 * w.m:,}), DeepWalk k={w.walk_len} l={w.window} w=1, d={w.dim}, K={w.negatives}")
 
 

@@ -44,44 +44,65 @@ __device__ __forceinline__ uint32_t draw_negative(const SgnsParams& p, uint2 key
     return (uint32_t)(p.c_begin + (x.z < ta.x ? col : (uint64_t)ta.y));
 }
 
-__device__ __forceinline__ float warp_sum(float x) {
+template <int G>
+__device__ __forceinline__ float group_sum(float x) {  // all-reduce inside aligned groups of G lanes
 #pragma unroll
-    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    for (int o = G / 2; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
     return x;
 }
 
-// R: float4 per lane per row.  KT: compile-time K (0 = runtime K <= kMaxK).
-// MINB: min resident CTAs per SM for __launch_bounds__ (register budget).
+// G: lanes per sample (16 or 32); a warp trains S = 32/G samples side by side,
+// each lane owning R float4 of every row (d <= 4 G R).  KT: compile-time K
+// (0 = runtime K <= kMaxK).  MINB: min resident CTAs per SM (register budget).
 // ADD: Hogwild write-back by vector reduction (red.global.add.v4.f32) of each
-// row's delta instead of a plain store of the new row, so concurrent samples
+// update's delta instead of a plain store of the new row, so concurrent samples
 // sharing a row never erase each other's updates (they only read stale values).
-template <int R, int KT, int MINB, bool ADD>
+// p.deterministic: only group 0 of the (single) warp works, one sample at a
+// time in canonical order -- the same arithmetic as the production mapping.
+// AM: draw the negatives of several iterations in one Philox pass (lane L of
+// the warp draws negative L % K of sample L / K of the next 32/(S K) iterations),
+// amortising the Philox + alias latency chain over up to 6 samples.
+template <int G, int R, int KT, int MINB, bool ADD, bool AM>
 __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) {
+    constexpr int S = 32 / G;
     constexpr int KM = KT > 0 ? KT : kMaxK;
     const int K = KT > 0 ? KT : (int)p.K;
-    const uint32_t lane = lane_id();
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = lane_id(), sub = lane % G, h = lane / G;
+    const uint32_t spw = p.deterministic ? 1u : (uint32_t)S;  // samples per warp-iteration
+    const uint64_t stride = (((uint64_t)gridDim.x * blockDim.x) >> 5) * spw;
     const uint32_t q = p.d >> 2;  // float4 per row
     const uint2 key = key_of(p.seed);
     const uint32_t tagw = tag_word(kTagNeg, p.epoch);
-    double loss = 0.0;  // lane 0
+    double loss = 0.0;  // lane sub == 0 of each group
 
-    uint64_t pos = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint64_t base = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * spw;
+    // negatives per iteration spw*K; iterations per Philox pass nit (AM) or 1
+    const uint32_t per_it = spw * (uint32_t)(K > 0 ? K : 1);
+    const uint32_t nit = AM ? 32u / per_it : 1u;
+    // lane L < nit*per_it draws negative j = L % K of sample h = (L % per_it) / K
+    // of iteration it = L / per_it, i.e. position b + it*stride + h
+    auto draw = [&](uint64_t b) -> uint32_t {
+        const uint32_t it = lane / per_it, r = lane % per_it;
+        const uint64_t ps = b + it * stride + r / (uint32_t)K;
+        return (K > 0 && lane < nit * per_it && ps < p.count) ? draw_negative(p, key, tagw, ps, r % K) : 0u;
+    };
     uint2 pr = make_uint2(0, 0);
-    uint32_t my_neg = 0;
-    if (pos < p.count) {
-        pr = p.pool[pos];
-        my_neg = (int)lane < K ? draw_negative(p, key, tagw, pos, lane) : 0u;
+    uint32_t my_neg = 0, slot_it = 0;  // iteration of the current Philox pass
+    if (base < p.count) {
+        if (h < spw && base + h < p.count) pr = p.pool[base + h];
+        my_neg = draw(base);
     }
-    for (; pos < p.count; pos += nwarps) {
-        // ids[0] = positive context, ids[1..K] = negatives; lane j < 1+K holds ids[j]
-        const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, my_neg, 1);
-        const uint32_t my_id = lane == 0 ? pr.y : up;
+    for (; base < p.count; base += stride) {
+        const uint64_t pos = base + h;
+        const bool act = h < spw && pos < p.count;
+        // ids[0] = positive context, ids[1..K] = negatives; lane sub = j <= K of the group holds ids[j]
+        const uint32_t nj = __shfl_sync(0xFFFFFFFFu, my_neg, (slot_it * per_it + h * K + sub + 31) & 31);
+        const uint32_t my_id = sub == 0 ? pr.y : nj;
         uint32_t ids[KM + 1];
 #pragma unroll
-        for (int j = 0; j <= KM; ++j) ids[j] = __shfl_sync(0xFFFFFFFFu, my_id, j);
-        // a repeated context id inside the sample is rare: detect it once per sample
-        const uint64_t mkey = (int)lane <= K ? (uint64_t)my_id : ((1ull << 32) | lane);
+        for (int j = 0; j <= KM; ++j) ids[j] = __shfl_sync(0xFFFFFFFFu, my_id, h * G + j);
+        // a repeated context id inside a sample is rare: detect it once per iteration
+        const uint64_t mkey = (act && (int)sub <= K) ? (((uint64_t)h << 33) | my_id) : ((1ull << 32) | lane);
         const bool dup = __any_sync(0xFFFFFFFFu, __popc(__match_any_sync(0xFFFFFFFFu, mkey)) > 1);
 
         float4* vrow = reinterpret_cast<float4*>(p.V + (uint64_t)(pr.x - p.v_begin) * p.d);
@@ -89,8 +110,8 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
         float4 c[KM + 1][R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const uint32_t e = lane + 32u * r;
-            v[r] = e < q ? vrow[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const uint32_t e = sub + G * r;
+            v[r] = (act && e < q) ? vrow[e] : make_float4(0.f, 0.f, 0.f, 0.f);
             if constexpr (ADD) v0[r] = v[r];
         }
 #pragma unroll
@@ -99,17 +120,21 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
                 const float4* crow = reinterpret_cast<const float4*>(p.C + (uint64_t)(ids[j] - p.c_begin) * p.d);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const uint32_t e = lane + 32u * r;
-                    c[j][r] = e < q ? crow[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const uint32_t e = sub + G * r;
+                    c[j][r] = (act && e < q) ? crow[e] : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
         }
 
-        // Prefetch the next sample's pair and negatives while the rows load.
-        const uint64_t nxt = pos + nwarps;
-        if (nxt < p.count) {
-            pr = p.pool[nxt];
-            my_neg = (int)lane < K ? draw_negative(p, key, tagw, nxt, lane) : 0u;
+        // Prefetch the next iteration's pairs (and, after the last iteration of a
+        // Philox pass, the next pass's negatives) while the rows load.
+        const uint64_t nb = base + stride;
+        if (nb < p.count) {
+            if (h < spw && nb + h < p.count) pr = p.pool[nb + h];
+            if (++slot_it == nit) {
+                my_neg = draw(nb);
+                slot_it = 0;
+            }
         }
 
         // Alg. 1 lines 10 and 12: positive, then the K negatives, in order.
@@ -136,12 +161,12 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
                     part = fmaf(v[r].z, c[j][r].z, part);
                     part = fmaf(v[r].w, c[j][r].w, part);
                 }
-                const float x = fminf(fmaxf(warp_sum(part), -30.f), 30.f);
-                const float s = __fdividef(1.f, 1.f + __expf(-x));
-                const float g = s - (j == 0 ? 1.f : 0.f);
-                const float a = p.lr * g;
-                if (lane == 0)  // -log s (y = 1) or -log(1 - s) (y = 0), as softplus
-                    loss += (double)__logf(1.f + __expf(j == 0 ? -x : x));
+                const float x = fminf(fmaxf(group_sum<G>(part), -30.f), 30.f);
+                const float ex = __expf(-x);
+                const float s = __fdividef(1.f, 1.f + ex);
+                const float a = p.lr * (s - (j == 0 ? 1.f : 0.f));
+                if (sub == 0 && act)  // -log s = log(1+e^-x) (y = 1); -log(1-s) = x + log(1+e^-x) (y = 0)
+                    loss += (double)(__logf(1.f + ex) + (j == 0 ? 0.f : x));
                 float4* crow = reinterpret_cast<float4*>(p.C + (uint64_t)(ids[j] - p.c_begin) * p.d);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
@@ -150,8 +175,8 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
                                        fmaf(-a, co.z, vo.z), fmaf(-a, co.w, vo.w));
                     c[j][r] = make_float4(fmaf(-a, vo.x, co.x), fmaf(-a, vo.y, co.y),
                                           fmaf(-a, vo.z, co.z), fmaf(-a, vo.w, co.w));
-                    const uint32_t e = lane + 32u * r;
-                    if (e < q) {
+                    const uint32_t e = sub + G * r;
+                    if (act && e < q) {
                         if constexpr (ADD)  // this update's delta, at every occurrence
                             atomicAdd(crow + e, make_float4(-a * vo.x, -a * vo.y, -a * vo.z, -a * vo.w));
                         else if (last)      // the row's final value, once
@@ -162,8 +187,8 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const uint32_t e = lane + 32u * r;
-            if (e < q) {
+            const uint32_t e = sub + G * r;
+            if (act && e < q) {
                 if constexpr (ADD)
                     atomicAdd(vrow + e, make_float4(v[r].x - v0[r].x, v[r].y - v0[r].y,
                                                     v[r].z - v0[r].z, v[r].w - v0[r].w));
@@ -172,21 +197,38 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
             }
         }
     }
-    if (lane == 0 && loss != 0.0) atomicAdd(p.loss, loss);
+    if (sub == 0 && loss != 0.0) atomicAdd(p.loss, loss);
 }
 
-template <int R, int KT, int MINB>
+static int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
+template <int G, int R, int KT, int MINB>
 static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStream_t s) {
-    if (p.deterministic) {  // one warp, canonical order, plain stores
-        sgns_kernel<R, KT, MINB, false><<<1, 32, 0, s>>>(p);
+    static const bool am = env_int("NE_SGNS_AMORT", 0) != 0;  // developer knob (measured: no gain)
+    if (p.deterministic) {  // one warp, one sample at a time, canonical order, plain stores
+        if (am) sgns_kernel<G, R, KT, MINB, false, true><<<1, 32, 0, s>>>(p);
+        else sgns_kernel<G, R, KT, MINB, false, false><<<1, 32, 0, s>>>(p);
         return cudaGetLastError();
     }
-    auto kern = p.atomic_writeback ? sgns_kernel<R, KT, MINB, true> : sgns_kernel<R, KT, MINB, false>;
+    auto kern = p.atomic_writeback ? (am ? sgns_kernel<G, R, KT, MINB, true, true> : sgns_kernel<G, R, KT, MINB, true, false>)
+                                   : (am ? sgns_kernel<G, R, KT, MINB, false, true> : sgns_kernel<G, R, KT, MINB, false, false>);
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSgnsThreads, 0);
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
-    const uint64_t warps = std::min<uint64_t>(p.count, std::max<uint64_t>(p.max_warps, 1));
+    constexpr int S = 32 / G;
+    // concurrency cap counts samples in flight: warps = cap / S
+    const uint64_t want = std::min<uint64_t>(p.count, std::max<uint64_t>(p.max_warps, 1));
+    if (want < (uint64_t)S) {  // fewer samples in flight than a warp carries: one at a time
+        SgnsParams q = p;
+        q.deterministic = 1;  // sequential canonical order, production write-back
+        kern<<<1, 32, 0, s>>>(q);
+        return cudaGetLastError();
+    }
+    const uint64_t warps = want / S;
     const uint64_t full = (uint64_t)dev.sm_count * per_sm;
     const int wpb = kSgnsThreads / 32;
     if (warps >= full * wpb) {
@@ -199,44 +241,48 @@ static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStr
     return cudaGetLastError();
 }
 
-// Occupancy variant (developer knob NE_SGNS_MINB = 1..4, default 3): the
-// register budget __launch_bounds__(256, MINB) gives the compiler.
-static int sgns_minb() {
-    static int v = [] {
-        const char* e = std::getenv("NE_SGNS_MINB");
-        const int x = e ? std::atoi(e) : 3;
-        return (x >= 1 && x <= 4) ? x : 3;
-    }();
-    return v;
-}
+// Occupancy variant (developer knob NE_SGNS_MINB = 1..4): the register budget
+// __launch_bounds__(256, MINB) gives the compiler.  Defaults: 16-lane groups
+// carry two samples' rows per lane (MINB 2); 32-lane groups MINB 3.
 
-template <int R, int KT>
+template <int G, int R, int KT>
 static cudaError_t launch_sgns_k(const SgnsParams& p, const Device& dev, cudaStream_t s) {
-    // a runtime K keeps kMaxK+1 context rows live: cap the budget so it does not spill
-    const int minb = KT == 0 ? std::min(sgns_minb(), 2) : sgns_minb();
+    if constexpr (R > 2) {  // wide rows (d > 256): the register file holds 2+K rows of up to 2 KB
+        return launch_sgns_v<G, R, KT, 1>(p, dev, s);
+    }
+    static const int knob = env_int("NE_SGNS_MINB", 0);
+    int minb = knob >= 1 && knob <= 4 ? knob : (G == 16 ? 2 : 3);
+    if (KT == 0) minb = std::min(minb, 2);  // runtime K keeps kMaxK+1 rows live: stay spill-free
     switch (minb) {
-        case 1: return launch_sgns_v<R, KT, 1>(p, dev, s);
-        case 2: return launch_sgns_v<R, KT, 2>(p, dev, s);
-        case 4: return launch_sgns_v<R, KT, 4>(p, dev, s);
-        default: return launch_sgns_v<R, KT, 3>(p, dev, s);
+        case 1: return launch_sgns_v<G, R, KT, 1>(p, dev, s);
+        case 2: return launch_sgns_v<G, R, KT, 2>(p, dev, s);
+        case 4: return launch_sgns_v<G, R, KT, 4>(p, dev, s);
+        default: return launch_sgns_v<G, R, KT, 3>(p, dev, s);
     }
 }
 
-template <int R>
+template <int G, int R>
 static cudaError_t launch_sgns_r(const SgnsParams& p, const Device& dev, cudaStream_t s) {
-    if (p.K == 5) return launch_sgns_k<R, 5>(p, dev, s);  // the paper's K (tab:perf)
-    return launch_sgns_k<R, 0>(p, dev, s);
+    if (p.K == 5) return launch_sgns_k<G, R, 5>(p, dev, s);  // the paper's K (tab:perf)
+    return launch_sgns_k<G, R, 0>(p, dev, s);
 }
 
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s) {
     if (p.count == 0) return cudaSuccess;
     if (p.K > (uint32_t)kMaxK || p.d % 4 != 0 || p.d == 0 || p.d > 512) return cudaErrorInvalidValue;
-    const uint32_t R = (p.d / 4 + 31) / 32;
-    switch (R) {
-        case 1: return launch_sgns_r<1>(p, dev, s);
-        case 2: return launch_sgns_r<2>(p, dev, s);
-        case 3: return launch_sgns_r<3>(p, dev, s);
-        default: return launch_sgns_r<4>(p, dev, s);
+    const uint32_t q = p.d / 4;
+    // d <= 128: 16 lanes x 2 float4 (two samples per warp; developer knob
+    // NE_SGNS_LANES=32 selects one sample per warp); d > 128: 32 lanes x R.
+    static const int lanes = env_int("NE_SGNS_LANES", 16);
+    if (q <= 32 && lanes == 16) {
+        if (q <= 16) return launch_sgns_r<16, 1>(p, dev, s);
+        return launch_sgns_r<16, 2>(p, dev, s);
+    }
+    switch ((q + 31) / 32) {
+        case 1: return launch_sgns_r<32, 1>(p, dev, s);
+        case 2: return launch_sgns_r<32, 2>(p, dev, s);
+        case 3: return launch_sgns_r<32, 3>(p, dev, s);
+        default: return launch_sgns_r<32, 4>(p, dev, s);
     }
 }
 

@@ -35,6 +35,7 @@ class Workload:
     walk_len: int = 40
     window: int = 5
     negatives: int = 5
+    kind: str = "rmat"  # "rmat" | "uniform" (G(n, m) control without hubs)
 
 
 # BASELINE.json configs; SURVEY.md section 8 "C1".."C5".
@@ -44,6 +45,8 @@ CONFIGS = {
     "c3": Workload("livejournal-shaped", 4_847_571, 68_993_773, 128, 3),
     "c4": Workload("friendster-shaped", 65_608_366, 1_806_067_135, 96, 4),
     "c5": Workload("hyperlink-pld-shaped", 39_497_204, 623_056_313, 256, 5),
+    # L2-reuse control: C3's n and m, uniform degrees (no hubs)
+    "c3u": Workload("livejournal-size-uniform", 4_847_571, 68_993_773, 128, 3, kind="uniform"),
 }
 TRAIN_SEED = 42
 EVAL_SEED = 7
@@ -132,6 +135,8 @@ def uniform_graph(n: int, m: int, seed: int):
 
 def workload_graph(name: str):
     w = CONFIGS[name]
+    if w.kind == "uniform":
+        return uniform_graph(w.n, w.m, w.graph_seed)
     return rmat_graph(w.n, w.m, w.graph_seed)
 
 
