@@ -32,6 +32,9 @@ import numpy as np  # noqa: E402
 METRIC = "positive edge samples/sec at d=128, K=5 (1/2/4/8 B200); HBM GB/s vs peak"
 UNIT = "positive samples/s"
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+SGNS_KERNEL = ("ne::sgns_tma_kernel (rows staged by TMA bulk copies, 16 lanes/sample)"
+               if os.environ.get("NE_SGNS_TMA", "0") != "0" else
+               "ne::sgns_kernel<16,2,5,2,ADD> (16 lanes/sample, 2 samples/warp, red.v4 write-back)")
 
 
 def alg_bytes_per_sample(d: int, K: int) -> int:
@@ -286,7 +289,7 @@ def main():
                        "mode": "hogwild", "parallelism": f"2D ring x{world}",
                        "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * 4 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "ne::sgns_kernel<1>",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": SGNS_KERNEL,
                          "bytes_per_sample": B, "launches": train_launches,
                          "avg_launch_ms": ms_train / max(train_launches, 1), "peak_source": peak_src},
             "phases_ms_per_step": {"walk": float(tsum[4]) / world / args.steps,

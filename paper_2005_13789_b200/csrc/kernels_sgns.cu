@@ -24,32 +24,11 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include "ne_device.cuh"
-#include "ne_internal.h"
+#include "sgns_common.cuh"
 
 namespace ne {
 
-constexpr int kMaxK = 8;
 constexpr int kSgnsThreads = 256;
-
-// O8: negative j of the sample at canonical position pos of the block:
-// Philox(ctr = (pos_lo, pos_hi, episode<<20 | block<<8 | j, NEG<<24 | epoch)),
-// column R2(x0|x1<<32, c_count), coin x2 < thr ? column : alias.
-__device__ __forceinline__ uint32_t draw_negative(const SgnsParams& p, uint2 key, uint32_t tagw,
-                                                  uint64_t pos, uint32_t j) {
-    const uint4 x = philox(make_uint4((uint32_t)pos, (uint32_t)(pos >> 32),
-                                      (p.episode << 20) | (p.block << 8) | j, tagw), key);
-    const uint64_t col = uniform_index(x.x, x.y, p.c_count);
-    const uint2 ta = __ldg(p.alias + col);
-    return (uint32_t)(p.c_begin + (x.z < ta.x ? col : (uint64_t)ta.y));
-}
-
-template <int G>
-__device__ __forceinline__ float group_sum(float x) {  // all-reduce inside aligned groups of G lanes
-#pragma unroll
-    for (int o = G / 2; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
-    return x;
-}
 
 // G: lanes per sample (16 or 32); a warp trains S = 32/G samples side by side,
 // each lane owning R float4 of every row (d <= 4 G R).  KT: compile-time K
@@ -57,12 +36,15 @@ __device__ __forceinline__ float group_sum(float x) {  // all-reduce inside alig
 // ADD: Hogwild write-back by vector reduction (red.global.add.v4.f32) of each
 // update's delta instead of a plain store of the new row, so concurrent samples
 // sharing a row never erase each other's updates (they only read stale values).
+// PF: the ids of iteration i+1 are known one iteration early (pairs and
+// negatives are fetched two iterations ahead), so at the top of iteration i
+// every lane prefetches ~2 of the 128-byte lines of iteration i+1's rows into
+// L2 (prefetch.global.L2); the next iteration's row loads then hit L2.  A
+// prefetch never changes values (L2 is the point of coherence), so it is valid
+// in deterministic mode too.
 // p.deterministic: only group 0 of the (single) warp works, one sample at a
 // time in canonical order -- the same arithmetic as the production mapping.
-// AM: draw the negatives of several iterations in one Philox pass (lane L of
-// the warp draws negative L % K of sample L / K of the next 32/(S K) iterations),
-// amortising the Philox + alias latency chain over up to 6 samples.
-template <int G, int R, int KT, int MINB, bool ADD, bool AM>
+template <int G, int R, int KT, int MINB, bool ADD, bool PF>
 __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) {
     constexpr int S = 32 / G;
     constexpr int KM = KT > 0 ? KT : kMaxK;
@@ -75,29 +57,30 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
     const uint32_t tagw = tag_word(kTagNeg, p.epoch);
     double loss = 0.0;  // lane sub == 0 of each group
 
-    uint64_t base = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * spw;
-    // negatives per iteration spw*K; iterations per Philox pass nit (AM) or 1
-    const uint32_t per_it = spw * (uint32_t)(K > 0 ? K : 1);
-    const uint32_t nit = AM ? 32u / per_it : 1u;
-    // lane L < nit*per_it draws negative j = L % K of sample h = (L % per_it) / K
-    // of iteration it = L / per_it, i.e. position b + it*stride + h
-    auto draw = [&](uint64_t b) -> uint32_t {
-        const uint32_t it = lane / per_it, r = lane % per_it;
-        const uint64_t ps = b + it * stride + r / (uint32_t)K;
-        return (K > 0 && lane < nit * per_it && ps < p.count) ? draw_negative(p, key, tagw, ps, r % K) : 0u;
+    // pair + negatives of the iteration starting at sample b (lane L < spw*K
+    // draws negative L % K of sample b + L / K)
+    auto fetch = [&](uint64_t b, uint2& pr, uint32_t& neg) {
+        pr = (h < spw && b + h < p.count) ? p.pool[b + h] : make_uint2(0, 0);
+        const uint64_t ps = b + lane / (uint32_t)(K > 0 ? K : 1);
+        neg = (K > 0 && lane < spw * (uint32_t)K && ps < p.count) ? draw_negative(p, key, tagw, ps, lane % K) : 0u;
     };
-    uint2 pr = make_uint2(0, 0);
-    uint32_t my_neg = 0, slot_it = 0;  // iteration of the current Philox pass
-    if (base < p.count) {
-        if (h < spw && base + h < p.count) pr = p.pool[base + h];
-        my_neg = draw(base);
-    }
+    // lane sub = j <= K of group h gets ids[j] (0: positive context, 1..K: negatives)
+    auto group_id = [&](const uint2& pr, uint32_t neg) -> uint32_t {
+        const uint32_t nj = __shfl_sync(0xFFFFFFFFu, neg, (h * K + sub + 31) & 31);
+        return sub == 0 ? pr.y : nj;
+    };
+
+    uint64_t base = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * spw;
+    uint2 prA, prB = make_uint2(0, 0);
+    uint32_t negA, negB = 0;
+    fetch(base, prA, negA);
+    if (PF) fetch(base + stride, prB, negB);
+    const uint32_t lines = p.d >> 5;                 // 128-byte lines per row
+    const uint32_t plines = (2u + (uint32_t)K) * lines;  // per sample
     for (; base < p.count; base += stride) {
         const uint64_t pos = base + h;
         const bool act = h < spw && pos < p.count;
-        // ids[0] = positive context, ids[1..K] = negatives; lane sub = j <= K of the group holds ids[j]
-        const uint32_t nj = __shfl_sync(0xFFFFFFFFu, my_neg, (slot_it * per_it + h * K + sub + 31) & 31);
-        const uint32_t my_id = sub == 0 ? pr.y : nj;
+        const uint32_t my_id = group_id(prA, negA);
         uint32_t ids[KM + 1];
 #pragma unroll
         for (int j = 0; j <= KM; ++j) ids[j] = __shfl_sync(0xFFFFFFFFu, my_id, h * G + j);
@@ -105,7 +88,7 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
         const uint64_t mkey = (act && (int)sub <= K) ? (((uint64_t)h << 33) | my_id) : ((1ull << 32) | lane);
         const bool dup = __any_sync(0xFFFFFFFFu, __popc(__match_any_sync(0xFFFFFFFFu, mkey)) > 1);
 
-        float4* vrow = reinterpret_cast<float4*>(p.V + (uint64_t)(pr.x - p.v_begin) * p.d);
+        float4* vrow = reinterpret_cast<float4*>(p.V + (uint64_t)(prA.x - p.v_begin) * p.d);
         float4 v[R], v0[ADD ? R : 1];
         float4 c[KM + 1][R];
 #pragma unroll
@@ -126,15 +109,25 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
             }
         }
 
-        // Prefetch the next iteration's pairs (and, after the last iteration of a
-        // Philox pass, the next pass's negatives) while the rows load.
-        const uint64_t nb = base + stride;
-        if (nb < p.count) {
-            if (h < spw && nb + h < p.count) pr = p.pool[nb + h];
-            if (++slot_it == nit) {
-                my_neg = draw(nb);
-                slot_it = 0;
+        uint2 prC = make_uint2(0, 0);
+        uint32_t negC = 0;
+        if constexpr (PF) {
+            // L2-prefetch the rows of iteration i+1 (ids known since iteration i-1)
+            const uint64_t nb = base + stride;
+            const bool nact = h < spw && nb + h < p.count;
+            const uint32_t nid = group_id(prB, negB);
+            for (uint32_t L = sub; L < ((plines + G - 1) / G) * G; L += G) {
+                const uint32_t row = L / lines, line = L % lines;
+                const uint32_t rid = __shfl_sync(0xFFFFFFFFu, nid, h * G + (row == 0 ? 0u : row - 1u));
+                if (nact && L < plines) {
+                    const float* a = row == 0 ? p.V + (uint64_t)(prB.x - p.v_begin) * p.d
+                                              : p.C + (uint64_t)(rid - p.c_begin) * p.d;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a + line * 32));
+                }
             }
+            fetch(base + 2 * stride, prC, negC);  // ids two iterations ahead
+        } else {
+            fetch(base + stride, prB, negB);     // ids one iteration ahead
         }
 
         // Alg. 1 lines 10 and 12: positive, then the K negatives, in order.
@@ -153,32 +146,17 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
                     for (int i = j + 1; i <= KM; ++i)
                         if (i <= K && ids[i] == ids[j]) last = false;
                 }
-                float part = 0.f;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    part = fmaf(v[r].x, c[j][r].x, part);
-                    part = fmaf(v[r].y, c[j][r].y, part);
-                    part = fmaf(v[r].z, c[j][r].z, part);
-                    part = fmaf(v[r].w, c[j][r].w, part);
-                }
-                const float x = fminf(fmaxf(group_sum<G>(part), -30.f), 30.f);
-                const float ex = __expf(-x);
-                const float s = __fdividef(1.f, 1.f + ex);
-                const float a = p.lr * (s - (j == 0 ? 1.f : 0.f));
-                if (sub == 0 && act)  // -log s = log(1+e^-x) (y = 1); -log(1-s) = x + log(1+e^-x) (y = 0)
-                    loss += (double)(__logf(1.f + ex) + (j == 0 ? 0.f : x));
+                float4 vo[R];
+                float lt;
+                const float a = sgns_step<G, R>(v, c[j], vo, p.lr, j == 0, lt);
+                if (sub == 0 && act) loss += (double)lt;
                 float4* crow = reinterpret_cast<float4*>(p.C + (uint64_t)(ids[j] - p.c_begin) * p.d);
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const float4 vo = v[r], co = c[j][r];
-                    v[r] = make_float4(fmaf(-a, co.x, vo.x), fmaf(-a, co.y, vo.y),
-                                       fmaf(-a, co.z, vo.z), fmaf(-a, co.w, vo.w));
-                    c[j][r] = make_float4(fmaf(-a, vo.x, co.x), fmaf(-a, vo.y, co.y),
-                                          fmaf(-a, vo.z, co.z), fmaf(-a, vo.w, co.w));
                     const uint32_t e = sub + G * r;
                     if (act && e < q) {
                         if constexpr (ADD)  // this update's delta, at every occurrence
-                            atomicAdd(crow + e, make_float4(-a * vo.x, -a * vo.y, -a * vo.z, -a * vo.w));
+                            atomicAdd(crow + e, scaled(-a, vo[r]));
                         else if (last)      // the row's final value, once
                             crow[e] = c[j][r];
                     }
@@ -196,6 +174,12 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
                     vrow[e] = v[r];
             }
         }
+        prA = prB;
+        negA = negB;
+        if constexpr (PF) {
+            prB = prC;
+            negB = negC;
+        }
     }
     if (sub == 0 && loss != 0.0) atomicAdd(p.loss, loss);
 }
@@ -207,14 +191,14 @@ static int env_int(const char* name, int dflt) {
 
 template <int G, int R, int KT, int MINB>
 static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStream_t s) {
-    static const bool am = env_int("NE_SGNS_AMORT", 0) != 0;  // developer knob (measured: no gain)
+    static const bool pf = env_int("NE_SGNS_PF", 0) != 0;  // developer knob: L2 row prefetch (measured: no gain)
     if (p.deterministic) {  // one warp, one sample at a time, canonical order, plain stores
-        if (am) sgns_kernel<G, R, KT, MINB, false, true><<<1, 32, 0, s>>>(p);
+        if (pf) sgns_kernel<G, R, KT, MINB, false, true><<<1, 32, 0, s>>>(p);
         else sgns_kernel<G, R, KT, MINB, false, false><<<1, 32, 0, s>>>(p);
         return cudaGetLastError();
     }
-    auto kern = p.atomic_writeback ? (am ? sgns_kernel<G, R, KT, MINB, true, true> : sgns_kernel<G, R, KT, MINB, true, false>)
-                                   : (am ? sgns_kernel<G, R, KT, MINB, false, true> : sgns_kernel<G, R, KT, MINB, false, false>);
+    auto kern = p.atomic_writeback ? (pf ? sgns_kernel<G, R, KT, MINB, true, true> : sgns_kernel<G, R, KT, MINB, true, false>)
+                                   : (pf ? sgns_kernel<G, R, KT, MINB, false, true> : sgns_kernel<G, R, KT, MINB, false, false>);
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSgnsThreads, 0);
     if (e != cudaSuccess) return e;
@@ -270,6 +254,15 @@ static cudaError_t launch_sgns_r(const SgnsParams& p, const Device& dev, cudaStr
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s) {
     if (p.count == 0) return cudaSuccess;
     if (p.K > (uint32_t)kMaxK || p.d % 4 != 0 || p.d == 0 || p.d > 512) return cudaErrorInvalidValue;
+    // NE_SGNS_TMA=1 (developer knob) stages rows in shared memory by TMA bulk
+    // copies (kernels_sgns_tma.cu); measured slower than the register kernel
+    // with L2 prefetch (smem caps it at 12 warps/SM), so it is off by default
+    static const int tma = env_int("NE_SGNS_TMA", 0);
+    if (tma) {
+        const cudaError_t e = launch_sgns_tma(p, dev, s);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+    }
     const uint32_t q = p.d / 4;
     // d <= 128: 16 lanes x 2 float4 (two samples per warp; developer knob
     // NE_SGNS_LANES=32 selects one sample per warp); d > 128: 32 lanes x R.

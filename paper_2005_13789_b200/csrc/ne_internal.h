@@ -70,6 +70,7 @@ struct SgnsParams {
     int atomic_writeback;       // Hogwild: red.add row deltas instead of storing rows
 };
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s);
+cudaError_t launch_sgns_tma(const SgnsParams& p, const Device& dev, cudaStream_t s);  // kernels_sgns_tma.cu
 cudaError_t launch_export_negatives(const SgnsParams& p, uint64_t pos_begin, uint64_t count,
                                     uint32_t* out, const Device& dev, cudaStream_t s);
 

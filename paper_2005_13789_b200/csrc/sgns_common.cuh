@@ -1,0 +1,71 @@
+// sgns_common.cuh -- device pieces shared by the SGNS kernels: the negative
+// draw (O8), the group all-reduce and one SGNS update (O10, Alg. 1 Train).
+// Every kernel variant calls sgns_step, so they share one arithmetic.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ne_device.cuh"
+#include "ne_internal.h"
+
+namespace ne {
+
+constexpr int kMaxK = 8;
+
+// O8: negative j of the sample at canonical position pos of the block:
+// Philox(ctr = (pos_lo, pos_hi, episode<<20 | block<<8 | j, NEG<<24 | epoch)),
+// column R2(x0|x1<<32, c_count), coin x2 < thr ? column : alias.
+__device__ __forceinline__ uint32_t draw_negative(const SgnsParams& p, uint2 key, uint32_t tagw,
+                                                  uint64_t pos, uint32_t j) {
+    const uint4 x = philox(make_uint4((uint32_t)pos, (uint32_t)(pos >> 32),
+                                      (p.episode << 20) | (p.block << 8) | j, tagw), key);
+    const uint64_t col = uniform_index(x.x, x.y, p.c_count);
+    const uint2 ta = __ldg(p.alias + col);
+    return (uint32_t)(p.c_begin + (x.z < ta.x ? col : (uint64_t)ta.y));
+}
+
+template <int G>
+__device__ __forceinline__ float group_sum(float x) {  // all-reduce inside aligned groups of G lanes
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+    return x;
+}
+
+// One Train(v, c, y) of Alg. 1 on the lane's R float4 of the two
+// rows: x = v.c (per-lane FMA chain + group all-reduce), s = sigma(clamp(x, +-30)),
+// a = lr (s - y), (v, c) <- (v - a c, c - a v) from the pre-update values.
+// Returns a; vo receives the pre-update v (for delta write-back); loss gets
+// -log s (y = 1) or -log(1 - s) (y = 0) as softplus of the same exponential.
+template <int G, int R>
+__device__ __forceinline__ float sgns_step(float4 (&v)[R], float4 (&c)[R], float4 (&vo)[R], float lr,
+                                           bool positive, float& loss) {
+    float part = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        part = fmaf(v[r].x, c[r].x, part);
+        part = fmaf(v[r].y, c[r].y, part);
+        part = fmaf(v[r].z, c[r].z, part);
+        part = fmaf(v[r].w, c[r].w, part);
+    }
+    const float x = fminf(fmaxf(group_sum<G>(part), -30.f), 30.f);
+    const float ex = __expf(-x);
+    const float s = __fdividef(1.f, 1.f + ex);
+    const float a = lr * (s - (positive ? 1.f : 0.f));
+    loss = __logf(1.f + ex) + (positive ? 0.f : x);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        vo[r] = v[r];
+        const float4 co = c[r];
+        v[r] = make_float4(fmaf(-a, co.x, vo[r].x), fmaf(-a, co.y, vo[r].y),
+                           fmaf(-a, co.z, vo[r].z), fmaf(-a, co.w, vo[r].w));
+        c[r] = make_float4(fmaf(-a, vo[r].x, co.x), fmaf(-a, vo[r].y, co.y),
+                           fmaf(-a, vo[r].z, co.z), fmaf(-a, vo[r].w, co.w));
+    }
+    return a;
+}
+
+__device__ __forceinline__ float4 scaled(float a, const float4& x) {
+    return make_float4(a * x.x, a * x.y, a * x.z, a * x.w);
+}
+
+}  // namespace ne
