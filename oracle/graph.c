@@ -39,14 +39,16 @@ double or_weight075(uint64_t deg)
     return sqrt(sqrt(d3));
 }
 
-/* O3 steps 2-3: integer Vose construction.  Returns the scaled column
- * numerators num[i] (in units where a full column is W), alias[i] and W.
+/* O3 steps 2-3: integer Vose construction (Vose 1991, worklists as stacks).
+ * Returns the scaled column numerators num[i] (in units where a full column is
+ * W), alias[i] and W.
  *   q_i = floor(w_i * 2^20 + 0.5)   (0 for deg 0);  all q = 0 -> q = 1 (uniform)
  *   m_i = q_i * n, column capacity W = sum q.
- *   small = {i : m_i < W}, large = {i : m_i >= W}, FIFO, ascending index.
+ *   small = {i : m_i < W}, large = {i : m_i >= W}, each a stack filled in
+ *   ascending index order.
  *   while both non-empty: s = pop(small), g = pop(large);
  *       num[s] = m_s, alias[s] = g;  m_g -= W - m_s;
- *       push g to the back of small if m_g < W else to the back of large.
+ *       push g on small if m_g < W else on large.
  *   leftovers: num = W, alias = self.
  * Invariant (exact): num[i] + sum_{c: alias[c]=i, c!=i} (W - num[c]) = q_i * n. */
 int or_alias_masses(const uint64_t *deg, uint64_t n, uint64_t *num_out,
@@ -55,14 +57,13 @@ int or_alias_masses(const uint64_t *deg, uint64_t n, uint64_t *num_out,
     uint64_t i, W = 0;
     uint64_t *q, *small, *large;
     unsigned __int128 *m;
-    uint64_t s_head = 0, s_tail = 0, l_head = 0, l_tail = 0;
+    uint64_t ns = 0, nl = 0;
     if (n == 0) { if (W_out) *W_out = 0; return 0; }
     q = (uint64_t *)malloc(n * sizeof(uint64_t));
     m = (unsigned __int128 *)malloc(n * sizeof(unsigned __int128));
-    /* each index is pushed at most twice over the whole run (once initially,
-     * plus re-queues of the same large item), so 2n+1 slots bound each FIFO */
-    small = (uint64_t *)malloc((2 * n + 1) * sizeof(uint64_t));
-    large = (uint64_t *)malloc((2 * n + 1) * sizeof(uint64_t));
+    /* every index is on at most one stack at a time */
+    small = (uint64_t *)malloc(n * sizeof(uint64_t));
+    large = (uint64_t *)malloc(n * sizeof(uint64_t));
     if (!q || !m || !small || !large) { free(q); free(m); free(small); free(large); return -1; }
     for (i = 0; i < n; ++i) {
         q[i] = deg[i] == 0 ? 0 : (uint64_t)floor(or_weight075(deg[i]) * 1048576.0 + 0.5);
@@ -74,20 +75,20 @@ int or_alias_masses(const uint64_t *deg, uint64_t n, uint64_t *num_out,
     }
     for (i = 0; i < n; ++i) {
         m[i] = (unsigned __int128)q[i] * (unsigned __int128)n;
-        if (m[i] < (unsigned __int128)W) small[s_tail++] = i;
-        else large[l_tail++] = i;
+        if (m[i] < (unsigned __int128)W) small[ns++] = i;
+        else large[nl++] = i;
     }
-    while (s_head < s_tail && l_head < l_tail) {
-        uint64_t s = small[s_head++];
-        uint64_t g = large[l_head++];
+    while (ns > 0 && nl > 0) {
+        uint64_t s = small[--ns];
+        uint64_t g = large[--nl];
         num_out[s] = (uint64_t)m[s];
         alias_out[s] = (uint32_t)g;
         m[g] -= (unsigned __int128)W - m[s];
-        if (m[g] < (unsigned __int128)W) small[s_tail++] = g;
-        else large[l_tail++] = g;
+        if (m[g] < (unsigned __int128)W) small[ns++] = g;
+        else large[nl++] = g;
     }
-    while (s_head < s_tail) { uint64_t s = small[s_head++]; num_out[s] = W; alias_out[s] = (uint32_t)s; }
-    while (l_head < l_tail) { uint64_t g = large[l_head++]; num_out[g] = W; alias_out[g] = (uint32_t)g; }
+    while (ns > 0) { uint64_t s = small[--ns]; num_out[s] = W; alias_out[s] = (uint32_t)s; }
+    while (nl > 0) { uint64_t g = large[--nl]; num_out[g] = W; alias_out[g] = (uint32_t)g; }
     if (W_out) *W_out = W;
     free(q); free(m); free(small); free(large);
     return 0;

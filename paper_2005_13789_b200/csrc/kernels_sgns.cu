@@ -58,21 +58,23 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
     double loss = 0.0;  // lane sub == 0 of each group
 
     // pair + negatives of the iteration starting at sample b (lane L < spw*K
-    // draws negative L % K of sample b + L / K)
-    auto fetch = [&](uint64_t b, uint2& pr, uint32_t& neg) {
+    // draws negative L % K of sample b + L / K); the alias entry is loaded here
+    // and the coin decided at first use (finish_negative in group_id)
+    auto fetch = [&](uint64_t b, uint2& pr, NegDraw& neg) {
         pr = (h < spw && b + h < p.count) ? p.pool[b + h] : make_uint2(0, 0);
         const uint64_t ps = b + lane / (uint32_t)(K > 0 ? K : 1);
-        neg = (K > 0 && lane < spw * (uint32_t)K && ps < p.count) ? draw_negative(p, key, tagw, ps, lane % K) : 0u;
+        if (K > 0 && lane < spw * (uint32_t)K && ps < p.count) neg = issue_negative(p, key, tagw, ps, lane % K);
+        else neg = NegDraw{0u, 0u, make_uint2(0u, 0u)};
     };
     // lane sub = j <= K of group h gets ids[j] (0: positive context, 1..K: negatives)
-    auto group_id = [&](const uint2& pr, uint32_t neg) -> uint32_t {
-        const uint32_t nj = __shfl_sync(0xFFFFFFFFu, neg, (h * K + sub + 31) & 31);
+    auto group_id = [&](const uint2& pr, const NegDraw& neg) -> uint32_t {
+        const uint32_t nj = __shfl_sync(0xFFFFFFFFu, finish_negative(p, neg), (h * K + sub + 31) & 31);
         return sub == 0 ? pr.y : nj;
     };
 
     uint64_t base = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * spw;
     uint2 prA, prB = make_uint2(0, 0);
-    uint32_t negA, negB = 0;
+    NegDraw negA, negB = NegDraw{0u, 0u, make_uint2(0u, 0u)};
     fetch(base, prA, negA);
     if (PF) fetch(base + stride, prB, negB);
     const uint32_t lines = p.d >> 5;                 // 128-byte lines per row
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
         }
 
         uint2 prC = make_uint2(0, 0);
-        uint32_t negC = 0;
+        NegDraw negC = NegDraw{0u, 0u, make_uint2(0u, 0u)};
         if constexpr (PF) {
             // L2-prefetch the rows of iteration i+1 (ids known since iteration i-1)
             const uint64_t nb = base + stride;

@@ -12,10 +12,12 @@
 //   pool          u64[N]   (src, dst) grouped by vertex sub-part, pi order
 #include <algorithm>
 #include <cmath>
+#include <memory>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -73,6 +75,8 @@ struct ne_ctx {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     uint32_t launches = 0;
+    std::shared_ptr<void> alias_scratch;  // host buffers reused across ne_load_graph calls
+    std::vector<uint2> alias_host;
 };
 
 namespace {
@@ -170,51 +174,104 @@ cudaEvent_t next_event(ne_ctx* c) {
     return c->ev_pool[c->ev_used++];
 }
 
-// O3 on the host, integer Vose (an implementation independent of oracle/):
-// weights q_i = round(deg_i^0.75 * 2^20), columns of capacity W = sum q over
-// n_j = part size, FIFO small/large queues in index order.
-void build_alias(const std::vector<uint64_t>& deg, std::vector<uint2>& out) {
-    const size_t n = deg.size();
-    out.assign(n, make_uint2(0xFFFFFFFFu, 0));
+// O3 on the host (an implementation independent of oracle/): weights
+// q_i = round(deg_i^0.75 * 2^20), integer Vose (1991) with stack worklists
+// over masses m_i = q_i * n_j against column capacity W = sum q.  The weights
+// are computed by all host threads; masses use 64-bit arithmetic whenever
+// max(q) * n fits (always for the BASELINE graphs), 128-bit otherwise.
+struct AliasScratch {
+    std::vector<uint64_t> q, m64, num;
+    std::vector<unsigned __int128> m128;
+    std::vector<uint32_t> small, large, alias;
+};
+
+template <typename M>
+static void vose(const std::vector<uint64_t>& q, std::vector<M>& m, unsigned __int128 W,
+                 AliasScratch& a) {
+    const size_t n = q.size();
+    size_t ns = 0, nl = 0;
+    for (size_t i = 0; i < n; ++i) {
+        m[i] = (M)q[i] * (M)n;
+        if ((unsigned __int128)m[i] < W) a.small[ns++] = (uint32_t)i;
+        else a.large[nl++] = (uint32_t)i;
+    }
+    const M w = (M)W;
+    while (ns && nl) {
+        const uint32_t sm = a.small[--ns], g = a.large[--nl];
+        a.num[sm] = (uint64_t)m[sm];
+        a.alias[sm] = g;
+        m[g] -= w - m[sm];
+        if (m[g] < w) a.small[ns++] = g;
+        else a.large[nl++] = g;
+    }
+    while (ns) { const uint32_t x = a.small[--ns]; a.num[x] = (uint64_t)W; a.alias[x] = x; }
+    while (nl) { const uint32_t x = a.large[--nl]; a.num[x] = (uint64_t)W; a.alias[x] = x; }
+}
+
+void build_alias(const uint64_t* deg, size_t n, std::vector<uint2>& out, AliasScratch& a) {
+    out.resize(n);
     if (n == 0) return;
-    std::vector<uint64_t> q(n);
+    a.q.resize(n);
+    const unsigned nt = std::max(1u, std::min(std::thread::hardware_concurrency(), 32u));
+    std::vector<std::thread> th;
+    std::vector<uint64_t> part_sum(nt, 0), part_max(nt, 0);
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            const size_t b = n * t / nt, e = n * (t + 1) / nt;
+            uint64_t sum = 0, mx = 0;
+            for (size_t i = b; i < e; ++i) {
+                uint64_t qi = 0;
+                if (deg[i]) {
+                    const double d = (double)deg[i];
+                    double d3 = d * d;
+                    d3 = d3 * d;
+                    qi = (uint64_t)std::floor(std::sqrt(std::sqrt(d3)) * 1048576.0 + 0.5);
+                }
+                a.q[i] = qi;
+                sum += qi;
+                mx = std::max(mx, qi);
+            }
+            part_sum[t] = sum;
+            part_max[t] = mx;
+        });
+    for (auto& x : th) x.join();
     unsigned __int128 W = 0;
-    for (size_t i = 0; i < n; ++i) {
-        if (deg[i] == 0) { q[i] = 0; continue; }
-        const double d = (double)deg[i];
-        double d3 = d * d;
-        d3 = d3 * d;
-        q[i] = (uint64_t)std::floor(std::sqrt(std::sqrt(d3)) * 1048576.0 + 0.5);
-        W += q[i];
-    }
-    if (W == 0) {
-        std::fill(q.begin(), q.end(), 1);
+    uint64_t qmax = 0;
+    for (unsigned t = 0; t < nt; ++t) { W += part_sum[t]; qmax = std::max(qmax, part_max[t]); }
+    if (W == 0) {  // all weights zero: uniform
+        std::fill(a.q.begin(), a.q.end(), 1);
         W = n;
+        qmax = 1;
     }
-    std::vector<unsigned __int128> mass(n);
-    std::vector<uint64_t> num(n);
-    std::vector<uint32_t> alias(n);
-    std::vector<size_t> small, large;
-    small.reserve(2 * n);
-    large.reserve(2 * n);
-    for (size_t i = 0; i < n; ++i) {
-        mass[i] = (unsigned __int128)q[i] * n;
-        (mass[i] < W ? small : large).push_back(i);
+    a.num.resize(n);
+    a.alias.resize(n);
+    a.small.resize(n);
+    a.large.resize(n);
+    if ((unsigned __int128)qmax * n < ((unsigned __int128)1 << 64) && (W >> 64) == 0) {
+        a.m64.resize(n);
+        vose(a.q, a.m64, W, a);
+    } else {
+        a.m128.resize(n);
+        vose(a.q, a.m128, W, a);
     }
-    size_t sh = 0, lh = 0;
-    while (sh < small.size() && lh < large.size()) {
-        const size_t s = small[sh++], g = large[lh++];
-        num[s] = (uint64_t)mass[s];
-        alias[s] = (uint32_t)g;
-        mass[g] -= W - mass[s];
-        (mass[g] < W ? small : large).push_back(g);
-    }
-    for (; sh < small.size(); ++sh) { num[small[sh]] = (uint64_t)W; alias[small[sh]] = (uint32_t)small[sh]; }
-    for (; lh < large.size(); ++lh) { num[large[lh]] = (uint64_t)W; alias[large[lh]] = (uint32_t)large[lh]; }
-    for (size_t i = 0; i < n; ++i) {
-        const unsigned __int128 t = ((unsigned __int128)num[i] << 32) / W;
-        out[i] = make_uint2(t > 0xFFFFFFFFu ? 0xFFFFFFFFu : (uint32_t)t, alias[i]);
-    }
+    // thr = min(2^32-1, floor(num * 2^32 / W)), exact: a double-precision
+    // estimate (error < 1 since the quotient has <= 33 bits) corrected with
+    // 128-bit products -- no integer division; all host threads.
+    const double inv = 4294967296.0 / (double)W;
+    th.clear();
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            const size_t b = n * t / nt, e = n * (t + 1) / nt;
+            for (size_t i = b; i < e; ++i) {
+                const unsigned __int128 x = (unsigned __int128)a.num[i] << 32;
+                uint64_t est = (uint64_t)((double)a.num[i] * inv);
+                unsigned __int128 prod = (unsigned __int128)est * W;
+                while (prod > x) { --est; prod -= W; }
+                while (prod + W <= x) { ++est; prod += W; }
+                out[i] = make_uint2(est > 0xFFFFFFFFu ? 0xFFFFFFFFu : (uint32_t)est, a.alias[i]);
+            }
+        });
+    for (auto& x : th) x.join();
 }
 
 uint64_t pairs_per_walk(uint32_t k, uint32_t l) {
@@ -509,15 +566,21 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     if (n == 0xFFFFFFFFu) return fail(c, NE_ERANGE, "n=%u reserves the sentinel id", n);
     if (n < (uint32_t)c->world) return fail(c, NE_ERANGE, "n=%u < world=%d", n, c->world);
     if (nnz >= (1ull << 40)) return fail(c, NE_ERANGE, "nnz=%llu too large", (unsigned long long)nnz);
-    free_all(c);
+    // A graph of the same shape reuses every device buffer (repeated loads, e2e).
+    const bool reuse = c->loaded && c->n == n && c->nnz == nnz;
+    if (!reuse) free_all(c);
+    c->loaded = false;
+    c->walked_epoch = c->walked_episode = c->built_epoch = c->built_episode = -1;
     const ne_config& g = c->cfg;
     const uint32_t P = (uint32_t)c->world, k = g.subparts;
     c->n = n;
     c->nnz = nnz;
+#define NE_ALLOC(ptr, count) \
+    do { if (!reuse) NE_TRY(dalloc_t(c, &(ptr), (count))); } while (0)
 
     // CSR into HBM, validated on the device.
-    NE_TRY(dalloc_t(c, &c->d_off, (size_t)n + 1));
-    NE_TRY(dalloc_t(c, &c->d_tgt, std::max<uint64_t>(nnz, 1)));
+    NE_ALLOC(c->d_off, (size_t)n + 1);
+    NE_ALLOC(c->d_tgt, std::max<uint64_t>(nnz, 1));
     NE_CUDA(c, cudaMemcpyAsync(c->d_off, offsets, ((size_t)n + 1) * sizeof(uint64_t), cudaMemcpyDefault, c->stream));
     if (nnz) NE_CUDA(c, cudaMemcpyAsync(c->d_tgt, targets, nnz * sizeof(uint32_t), cudaMemcpyDefault, c->stream));
     NE_CUDA(c, cudaMemsetAsync(c->d_bad, 0xFF, 2 * sizeof(unsigned long long), c->stream));
@@ -556,7 +619,7 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
             c->max_sub_rows = std::max(c->max_sub_rows, c->sub_bounds[(size_t)p * k + t + 1] - c->sub_bounds[(size_t)p * k + t]);
     }
     c->sub_bounds[(size_t)P * k] = n;
-    NE_TRY(dalloc_t(c, &c->d_sub_bounds, c->sub_bounds.size()));
+    NE_ALLOC(c->d_sub_bounds, c->sub_bounds.size());
     NE_CUDA(c, cudaMemcpyAsync(c->d_sub_bounds, c->sub_bounds.data(), c->sub_bounds.size() * sizeof(uint64_t),
                                cudaMemcpyHostToDevice, c->stream));
 
@@ -578,17 +641,18 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     }
     std::vector<uint64_t> deg(c->c_count);
     for (uint64_t i = 0; i < c->c_count; ++i) deg[i] = deg_src[i + 1] - deg_src[i];
-    std::vector<uint2> tab;
-    build_alias(deg, tab);
-    NE_TRY(dalloc_t(c, &c->d_alias, std::max<uint64_t>(c->c_count, 1)));
-    NE_CUDA(c, cudaMemcpyAsync(c->d_alias, tab.data(), tab.size() * sizeof(uint2), cudaMemcpyHostToDevice, c->stream));
+    if (!c->alias_scratch) c->alias_scratch = std::make_shared<AliasScratch>();
+    build_alias(deg.data(), deg.size(), c->alias_host, *static_cast<AliasScratch*>(c->alias_scratch.get()));
+    NE_ALLOC(c->d_alias, std::max<uint64_t>(c->c_count, 1));
+    NE_CUDA(c, cudaMemcpyAsync(c->d_alias, c->alias_host.data(), c->alias_host.size() * sizeof(uint2),
+                               cudaMemcpyHostToDevice, c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));  // alias_host is reused by the next load
 
     // Embeddings (O9): context part = 0; home vertex sub-parts initialised.
-    NE_TRY(dalloc_t(c, &c->d_C, std::max<uint64_t>(c->c_count, 1) * g.dim));
+    NE_ALLOC(c->d_C, std::max<uint64_t>(c->c_count, 1) * g.dim);
     NE_CUDA(c, cudaMemsetAsync(c->d_C, 0, c->c_count * g.dim * sizeof(float), c->stream));
-    c->vslot.assign(2 * (size_t)k, nullptr);
-    for (size_t i = 0; i < c->vslot.size(); ++i)
-        NE_TRY(dalloc_t(c, &c->vslot[i], std::max<uint64_t>(c->max_sub_rows, 1) * g.dim));
+    if (!reuse) c->vslot.assign(2 * (size_t)k, nullptr);
+    for (size_t i = 0; i < c->vslot.size(); ++i) NE_ALLOC(c->vslot[i], std::max<uint64_t>(c->max_sub_rows, 1) * g.dim);
     c->cur = 0;
     for (uint32_t t = 0; t < k; ++t) {
         const size_t vs = (size_t)c->rank * k + t;
@@ -603,18 +667,19 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     c->units_max = (c->units_total + g.episodes - 1) / g.episodes;
     c->N_max = c->units_max * c->Pw;
     if (g.walk_len > 0) {
-        NE_TRY(dalloc_t(c, &c->d_walks, std::max<uint64_t>(c->units_max, 1) * (g.walk_len + 1)));
+        NE_ALLOC(c->d_walks, std::max<uint64_t>(c->units_max, 1) * (g.walk_len + 1));
         std::vector<uint32_t> tab_s;
         for (uint32_t i = 0; i < g.walk_len; ++i)
             for (uint32_t dl = 1; dl <= g.window && i + dl <= g.walk_len; ++dl) tab_s.push_back((i << 16) | dl);
-        NE_TRY(dalloc_t(c, &c->d_slot_tab, tab_s.size()));
+        NE_ALLOC(c->d_slot_tab, tab_s.size());
         NE_CUDA(c, cudaMemcpyAsync(c->d_slot_tab, tab_s.data(), tab_s.size() * sizeof(uint32_t),
                                    cudaMemcpyHostToDevice, c->stream));
     }
-    NE_TRY(dalloc_t(c, &c->d_slots, std::max<uint64_t>(c->N_max, 1)));
-    NE_TRY(dalloc_t(c, &c->d_pool, std::max<uint64_t>(c->N_max, 1)));
-    NE_TRY(dalloc(c, &c->d_scratch, ne::bucket_scratch_bytes(c->N_max, nb_local(c))));
-    NE_TRY(dalloc_t(c, &c->d_boff, (size_t)nb_local(c) + 1));
+    NE_ALLOC(c->d_slots, std::max<uint64_t>(c->N_max, 1));
+    NE_ALLOC(c->d_pool, std::max<uint64_t>(c->N_max, 1));
+    if (!reuse) NE_TRY(dalloc(c, &c->d_scratch, ne::bucket_scratch_bytes(c->N_max, nb_local(c))));
+    NE_ALLOC(c->d_boff, (size_t)nb_local(c) + 1);
+#undef NE_ALLOC
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
     c->loaded = true;
     return NE_OK;

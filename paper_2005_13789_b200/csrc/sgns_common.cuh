@@ -15,13 +15,29 @@ constexpr int kMaxK = 8;
 // O8: negative j of the sample at canonical position pos of the block:
 // Philox(ctr = (pos_lo, pos_hi, episode<<20 | block<<8 | j, NEG<<24 | epoch)),
 // column R2(x0|x1<<32, c_count), coin x2 < thr ? column : alias.
-__device__ __forceinline__ uint32_t draw_negative(const SgnsParams& p, uint2 key, uint32_t tagw,
+// Split in two so a kernel can issue the alias-table load one iteration early
+// and take the coin decision only when the id is needed (the load latency then
+// overlaps a whole iteration instead of stalling the prefetch).
+struct NegDraw {
+    uint32_t col, coin;
+    uint2 ta;  // (thr, alias) of column col
+};
+__device__ __forceinline__ NegDraw issue_negative(const SgnsParams& p, uint2 key, uint32_t tagw,
                                                   uint64_t pos, uint32_t j) {
     const uint4 x = philox(make_uint4((uint32_t)pos, (uint32_t)(pos >> 32),
                                       (p.episode << 20) | (p.block << 8) | j, tagw), key);
-    const uint64_t col = uniform_index(x.x, x.y, p.c_count);
-    const uint2 ta = __ldg(p.alias + col);
-    return (uint32_t)(p.c_begin + (x.z < ta.x ? col : (uint64_t)ta.y));
+    NegDraw d;
+    d.col = (uint32_t)uniform_index(x.x, x.y, p.c_count);
+    d.coin = x.z;
+    d.ta = __ldg(p.alias + d.col);
+    return d;
+}
+__device__ __forceinline__ uint32_t finish_negative(const SgnsParams& p, const NegDraw& d) {
+    return (uint32_t)(p.c_begin + (d.coin < d.ta.x ? d.col : d.ta.y));
+}
+__device__ __forceinline__ uint32_t draw_negative(const SgnsParams& p, uint2 key, uint32_t tagw,
+                                                  uint64_t pos, uint32_t j) {
+    return finish_negative(p, issue_negative(p, key, tagw, pos, j));
 }
 
 template <int G>

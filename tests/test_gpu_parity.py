@@ -309,3 +309,25 @@ def test_deterministic_ring_emulation_c1(c1, P):
         assert np.abs(e.embeddings(0) - V[a:b]).max() <= TOL
         assert np.abs(e.embeddings(1) - Cm[a:b]).max() <= TOL
         e.close()
+
+
+def test_reload_same_shape_graph_reuses_buffers():
+    """ne_load_graph of a second graph with the same n and nnz reuses every
+    device buffer; the result must be that of a fresh context."""
+    offA, tgtA = synth.rmat_graph(600, 3000, 21)
+    offB, tgtB = synth.uniform_graph(600, 3000, 22)
+    assert len(tgtA) == len(tgtB)
+    eng = engine(dim=32)
+    eng.load_graph(offA, tgtA)
+    eng.train_epoch(0, 0.025)
+    eng.load_graph(offB, tgtB)
+    assert np.array_equal(eng.embeddings(0), oracle.init_vertex(600, 32, 42))
+    assert not eng.embeddings(1).any()
+    eng.train_epoch(0, 0.025)
+    cfg = ocfg(dim=32)
+    V = oracle.init_vertex(600, 32, 42)
+    Cm = np.zeros_like(V)
+    oracle.train_epoch(cfg, offB, tgtB, V, Cm, 0, 0.025)
+    assert np.abs(eng.embeddings(0) - V).max() <= TOL
+    assert np.abs(eng.embeddings(1) - Cm).max() <= TOL
+    eng.close()
