@@ -168,6 +168,7 @@ def main():
     ap.add_argument("--cpu-episodes", type=int, default=384)
     ap.add_argument("--ref-episodes", type=int, default=1536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--episodes", type=int, default=0, help="episodes per epoch (0 = workload default)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -188,8 +189,9 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w, desc = workload_desc(args.workload)
-    off, tgt = synth.workload_graph(args.workload)
+    off, tgt = synth.workload_graph(args.workload, device=f"cuda:{local}")
     n = len(off) - 1
+    episodes = args.episodes or w.episodes
     nccl_id = None
     if world > 1:
         obj = [ne.ne_get_nccl_id() if rank == 0 else None]
@@ -197,7 +199,7 @@ def main():
         nccl_id = obj[0]
     stream = torch.cuda.current_stream()
     eng = Engine(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
-                 walks_per_node=1, episodes=1, subparts=4, deterministic=False, seed=42,
+                 walks_per_node=1, episodes=episodes, subparts=4, deterministic=False, seed=42,
                  device=local, rank=rank, world=world, nccl_id=nccl_id, torch_allocator=True,
                  stream=stream.cuda_stream)
     eng.load_graph(off, tgt)
@@ -251,9 +253,15 @@ def main():
             traffic = tr.get("dram_bytes_per_launch")
 
     # end-to-end through the public API with host buffers (pinned)
-    off_h = torch.from_numpy(off.view(np.int64)).pin_memory()
-    tgt_h = torch.from_numpy(tgt.view(np.int32)).pin_memory()
-    h2d = off.nbytes + tgt.nbytes
+    if isinstance(off, np.ndarray):
+        off_h = torch.from_numpy(off.view(np.int64)).pin_memory()
+        tgt_h = torch.from_numpy(tgt.view(np.int32)).pin_memory()
+    else:  # GPU-generated workload: stage it in pinned host memory for the e2e leg
+        off_h, tgt_h = off.cpu().pin_memory(), tgt.cpu().pin_memory()
+        del off, tgt
+        torch.cuda.empty_cache()
+        off, tgt = off_h.numpy().view(np.uint64), tgt_h.numpy().view(np.uint32)
+    h2d = off_h.numel() * 8 + tgt_h.numel() * 4
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_samples = 0
@@ -275,7 +283,7 @@ def main():
         e_value = e_samples / (float(e_ms[0]) / 1e3)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and w.m <= 200_000_000:
         cpu = cpu_baseline(args, off, tgt, w)
     eng.close()
     if rank == 0:
@@ -285,9 +293,10 @@ def main():
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": desc, "step": "one epoch: walk + augment + order/bucket + SGNS (+ ring)",
-                       "samples_per_step": samples_all / args.steps, "episodes": 1, "subparts": 4,
+                       "samples_per_step": samples_all / args.steps, "episodes": episodes, "subparts": 4,
                        "mode": "hogwild", "parallelism": f"2D ring x{world}",
-                       "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * 4 / 1e9)},
+                       "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * 4 / 1e9),
+                       "graph_generator": "numpy Philox (host)" if w.m <= 200_000_000 else "torch CUDA generator"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": SGNS_KERNEL,
                          "bytes_per_sample": B, "launches": train_launches,
@@ -299,7 +308,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     # CSR validation flags + offsets ends (32 B), block offsets (5 x 8 B), loss (8 B)
-                    "d2h_bytes_per_step": 32 + 8 * (4 * world + 1) + 8},
+                    "d2h_bytes_per_step": 32 + episodes * (8 * (4 * world + 1) + 8)},
             "clocks": clk.summary(),
             "gpu_launches": int(tsum[3]),
         }

@@ -72,7 +72,8 @@ typedef void (*ne_free_fn)(void *ptr, size_t bytes, int device, void *stream, vo
  * ne_create (NE_EINVAL): dim % 4 == 0 and 4 <= dim <= 512; negatives <= 8;
  * walk_len <= 255 (0 selects LINE mode: the pool is the CSR edge list);
  * 1 <= window <= walk_len when walk_len > 0; walks_per_node >= 1;
- * 1 <= episodes <= 4095; 1 <= subparts and world*subparts*world <= 4096. */
+ * 1 <= episodes <= 4095; 1 <= subparts and world*subparts*world <= 4096;
+ * p, q > 0 (or 0 for 1). */
 typedef struct {
     uint32_t dim;            /* d, embedding dimension (tab:perf d = 96..128)     */
     uint32_t negatives;      /* K negatives per positive sample (tab:perf K = 5)  */
@@ -95,6 +96,10 @@ typedef struct {
                                 row are never erased; NE_WB_STORE (1) stores the new
                                 rows (word2vec-style, loses concurrent updates).
                                 Deterministic mode always stores.                   */
+    float    p, q;           /* node2vec return / in-out parameters (NEXT-1; node2vec,
+                                P:355; rejection sampling as in KnightKing).
+                                p = q = 1 (or 0) = first-order DeepWalk walk.  Other
+                                values need every CSR row sorted by target.         */
     uint64_t seed;           /* Philox key (contract R1)                                */
 } ne_config;
 
@@ -140,6 +145,8 @@ int ne_init_dist(ne_ctx *ctx, int rank, int world, const uint8_t id[128]);
  * (deg^0.75 over its context part, O3/D9) and initialises the embeddings
  * (O9: vertex U(-0.5/d, 0.5/d), context 0).  May be called again to replace
  * the graph (re-initialises).  Errors: NE_EINVAL (+ first offending index),
+ * With node2vec parameters (p, q != 1) rows must also be sorted by target
+ * (NE_EINVAL "targets[e]=... < targets[e-1]=... in row r").
  * NE_ERANGE (n >= 2^32 - 1 or n < world), NE_ENOMEM, NE_ECUDA. */
 int ne_load_graph(ne_ctx *ctx, uint32_t n, uint64_t nnz,
                   const uint64_t *offsets, const uint32_t *targets);
@@ -147,7 +154,8 @@ int ne_load_graph(ne_ctx *ctx, uint32_t n, uint64_t nnz,
 /* Walk engine, one episode (Alg. 1 "parallel random walk"; O4):
  * walkers omega of the episode's contiguous range, start = omega mod n, k
  * steps, Philox(ctr = (omega, t, WALK|epoch)) per step, stop at a node
- * without out-edges.  Kept on the device; if host_walks != NULL also copied
+ * without out-edges.  With node2vec parameters, step t >= 2 repeats trials r
+ * with ctr word 2 = t | r << 8 until the candidate passes its threshold.  Kept on the device; if host_walks != NULL also copied
  * out as [walkers][walk_len+1] u32, 0xFFFFFFFF after the walk's end
  * (cap_u32 = capacity in u32).  walkers_out (nullable) receives the count.
  * Errors: NE_ESTATE (no graph; LINE mode), NE_ERANGE (episode, epoch >= 2^24,

@@ -46,7 +46,8 @@ def build(force: bool = False) -> str:
 class _Config(C.Structure):
     _fields_ = [("dim", C.c_uint32), ("negatives", C.c_uint32), ("walk_len", C.c_uint32),
                 ("window", C.c_uint32), ("walks_per_node", C.c_uint32), ("episodes", C.c_uint32),
-                ("subparts", C.c_uint32), ("parts", C.c_uint32), ("seed", C.c_uint64)]
+                ("subparts", C.c_uint32), ("parts", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
+                ("seed", C.c_uint64)]
 
 
 class _Stats(C.Structure):
@@ -65,10 +66,12 @@ class Config:
     subparts: int = 4
     parts: int = 1
     seed: int = 42
+    p: float = 1.0   # node2vec return parameter (NEXT-1); p = q = 1: first order
+    q: float = 1.0   # node2vec in-out parameter
 
     def c(self) -> _Config:
         return _Config(self.dim, self.negatives, self.walk_len, self.window, self.walks_per_node,
-                       self.episodes, self.subparts, self.parts, self.seed)
+                       self.episodes, self.subparts, self.parts, self.p, self.q, self.seed)
 
 
 _lib = None
@@ -99,6 +102,10 @@ def lib():
     L.or_random_walk.argtypes = [C.c_uint64, _u64p, _u32p, C.c_uint64, C.c_uint32, C.c_uint64,
                                  C.c_uint32, _u32p]
     L.or_random_walk.restype = C.c_uint32
+    L.or_node2vec_thresholds.argtypes = [C.c_float, C.c_float, _u64p]
+    L.or_node2vec_walk.argtypes = [C.c_uint64, _u64p, _u32p, C.c_uint64, C.c_uint32, C.c_uint64,
+                                   C.c_uint32, C.c_float, C.c_float, _u32p]
+    L.or_node2vec_walk.restype = C.c_uint32
     L.or_pairs_per_walk.argtypes = [C.c_uint32, C.c_uint32]
     L.or_pairs_per_walk.restype = C.c_uint64
     L.or_pair_slot.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.POINTER(C.c_uint32),
@@ -214,6 +221,22 @@ def random_walk(offsets, targets, seed: int, epoch: int, omega: int, k: int) -> 
         targets = np.zeros(1, np.uint32)
     path = np.zeros(k + 1, np.uint32)
     ln = lib().or_random_walk(len(offsets) - 1, offsets, targets, seed, epoch, omega, k, path)
+    return path[:ln].copy()
+
+
+def node2vec_thresholds(p: float, q: float) -> np.ndarray:
+    thr = np.zeros(3, np.uint64)
+    lib().or_node2vec_thresholds(p, q, thr)
+    return thr
+
+
+def node2vec_walk(offsets, targets, seed: int, epoch: int, omega: int, k: int, p: float, q: float) -> np.ndarray:
+    offsets = np.ascontiguousarray(offsets, np.uint64)
+    targets = np.ascontiguousarray(targets, np.uint32)
+    if len(targets) == 0:
+        targets = np.zeros(1, np.uint32)
+    path = np.zeros(k + 1, np.uint32)
+    ln = lib().or_node2vec_walk(len(offsets) - 1, offsets, targets, seed, epoch, omega, k, p, q, path)
     return path[:ln].copy()
 
 

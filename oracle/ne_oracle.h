@@ -33,6 +33,7 @@ typedef struct {
     uint32_t episodes;       /* episodes per epoch                      */
     uint32_t subparts;       /* vertex sub-parts per part, k=4         */
     uint32_t parts;          /* P context/vertex parts (GPUs)   */
+    float    p, q;           /* node2vec return / in-out parameters; 1, 1 (or 0) = first order */
     uint64_t seed;           /* Philox key                                      */
 } or_config;
 
@@ -61,6 +62,11 @@ uint64_t or_alias_pick(const uint32_t *thr, const uint32_t *alias, uint64_t n,
 uint32_t or_random_walk(uint64_t n, const uint64_t *offsets, const uint32_t *targets,
                         uint64_t seed, uint32_t epoch, uint64_t omega, uint32_t k,
                         uint32_t *path);
+
+void     or_node2vec_thresholds(float p, float q, uint64_t thr[3]);
+uint32_t or_node2vec_walk(uint64_t n, const uint64_t *offsets, const uint32_t *targets,
+                          uint64_t seed, uint32_t epoch, uint64_t omega, uint32_t k,
+                          float p, float q, uint32_t *path);
 
 /* ---- O5 / O6 pairs, canonical order ------------------------------------ */
 uint64_t or_pairs_per_walk(uint32_t k, uint32_t l);

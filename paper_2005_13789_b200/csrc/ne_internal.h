@@ -15,17 +15,20 @@ struct Device {
 
 // ---- graph / init / walks (kernels_graph.cu) -------------------------------
 // S:24 invariants; bad[0] = first i with offsets[i+1] < offsets[i] (or ~0),
-// bad[1] = first e with targets[e] >= n (or ~0).
+// bad[1] = first e with targets[e] >= n (or ~0); with check_sorted, bad[2] =
+// first e > offsets[row] with targets[e] < targets[e-1] inside its row (or ~0).
 cudaError_t launch_validate_csr(const uint64_t* off, const uint32_t* tgt, uint64_t n,
-                                uint64_t nnz, unsigned long long* bad, const Device& dev,
-                                cudaStream_t s);
+                                uint64_t nnz, unsigned long long* bad, bool check_sorted,
+                                const Device& dev, cudaStream_t s);
 // O9: rows [row_begin, row_begin + rows) of the vertex matrix into V (row-major).
 cudaError_t launch_init_vertex(float* V, uint64_t row_begin, uint64_t rows, uint32_t d,
                                uint64_t seed, const Device& dev, cudaStream_t s);
-// O4: walkers [omega0, omega0 + count) -> walks[count][k+1].
+// O4: walkers [omega0, omega0 + count) -> walks[count][k+1].  node2vec
+// (NEXT-1) when n2v_thr != nullptr: thresholds (return, neighbour, farther),
+// each <= 2^32, of the rejection step.
 cudaError_t launch_walk(const uint64_t* off, const uint32_t* tgt, uint64_t n, uint64_t omega0,
                         uint64_t count, uint32_t k, uint64_t seed, uint32_t epoch,
-                        uint32_t* walks, const Device& dev, cudaStream_t s);
+                        const uint64_t* n2v_thr, uint32_t* walks, const Device& dev, cudaStream_t s);
 
 // ---- sample pool (kernels_samples.cu) ---------------------------------------
 struct PoolParams {

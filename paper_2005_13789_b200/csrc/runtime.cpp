@@ -65,6 +65,8 @@ struct ne_ctx {
     std::vector<uint64_t> boff;
     double* d_loss = nullptr;
     unsigned long long* d_bad = nullptr;
+    bool n2v = false;           // node2vec walks (p, q != 1)
+    uint64_t n2v_thr[3] = {0, 0, 0};
     uint32_t* d_tmp_u32 = nullptr;
     size_t tmp_u32_cap = 0;
 
@@ -305,7 +307,8 @@ int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     uint64_t u0, units;
     episode_range(c, episode, &u0, &units);
     NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0, units, c->cfg.walk_len,
-                               c->cfg.seed, epoch, c->d_walks, c->dev, c->stream));
+                               c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr, c->d_walks, c->dev,
+                               c->stream));
     if (units) c->launches += 1;
     c->walked_epoch = epoch;
     c->walked_episode = episode;
@@ -502,6 +505,17 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     if (g.episodes == 0 || g.episodes > 4095)
         return bad(fail(c, NE_EINVAL, "episodes=%u not in [1, 4095]", g.episodes));
     if (g.writeback > NE_WB_STORE) return bad(fail(c, NE_EINVAL, "writeback=%u not in {0, 1}", g.writeback));
+    if (!(g.p >= 0.f) || !(g.q >= 0.f))
+        return bad(fail(c, NE_EINVAL, "node2vec p=%g q=%g must be > 0 (0 = 1)", g.p, g.q));
+    {
+        // node2vec thresholds (NEXT-1): alpha = 1/p, 1, 1/q scaled by their max to 2^32
+        const double pp = g.p == 0.f ? 1.0 : (double)g.p, qq = g.q == 0.f ? 1.0 : (double)g.q;
+        c->n2v = !(pp == 1.0 && qq == 1.0);
+        const double w[3] = {1.0 / pp, 1.0, 1.0 / qq};
+        const double mx = std::max(std::max(w[0], w[1]), w[2]);
+        for (int i = 0; i < 3; ++i)
+            c->n2v_thr[i] = w[i] == mx ? (1ull << 32) : (uint64_t)(w[i] / mx * 4294967296.0);
+    }
     if (g.subparts == 0 || g.subparts > 256)
         return bad(fail(c, NE_EINVAL, "subparts=%u not in [1, 256]", g.subparts));
     int ndev = 0;
@@ -521,7 +535,7 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
         cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&c->d_loss, sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&c->d_bad, 2 * sizeof(unsigned long long)) != cudaSuccess)
+        cudaMalloc(&c->d_bad, 3 * sizeof(unsigned long long)) != cudaSuccess)
         return bad(fail(c, NE_ECUDA, "stream/scratch setup failed on device %d", device));
     c->stream = c->own_stream;
     *out = c;
@@ -583,10 +597,10 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     NE_ALLOC(c->d_tgt, std::max<uint64_t>(nnz, 1));
     NE_CUDA(c, cudaMemcpyAsync(c->d_off, offsets, ((size_t)n + 1) * sizeof(uint64_t), cudaMemcpyDefault, c->stream));
     if (nnz) NE_CUDA(c, cudaMemcpyAsync(c->d_tgt, targets, nnz * sizeof(uint32_t), cudaMemcpyDefault, c->stream));
-    NE_CUDA(c, cudaMemsetAsync(c->d_bad, 0xFF, 2 * sizeof(unsigned long long), c->stream));
-    NE_CUDA(c, ne::launch_validate_csr(c->d_off, c->d_tgt, n, nnz, c->d_bad, c->dev, c->stream));
+    NE_CUDA(c, cudaMemsetAsync(c->d_bad, 0xFF, 3 * sizeof(unsigned long long), c->stream));
+    NE_CUDA(c, ne::launch_validate_csr(c->d_off, c->d_tgt, n, nnz, c->d_bad, c->n2v, c->dev, c->stream));
     c->launches += 1;
-    unsigned long long bad[2];
+    unsigned long long bad[3];
     uint64_t ends[2];
     NE_CUDA(c, cudaMemcpyAsync(bad, c->d_bad, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
     NE_CUDA(c, cudaMemcpyAsync(&ends[0], c->d_off, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -606,6 +620,12 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
         uint32_t t;
         NE_CUDA(c, cudaMemcpy(&t, c->d_tgt + bad[1], sizeof t, cudaMemcpyDeviceToHost));
         return fail(c, NE_EINVAL, "targets[%llu]=%u >= n=%u", bad[1], t, n);
+    }
+    if (bad[2] != ~0ull) {
+        uint32_t t[2];
+        NE_CUDA(c, cudaMemcpy(t, c->d_tgt + bad[2] - 1, sizeof t, cudaMemcpyDeviceToHost));
+        return fail(c, NE_EINVAL, "targets[%llu]=%u < targets[%llu]=%u: node2vec needs rows sorted by target",
+                    bad[2], t[1], bad[2] - 1, t[0]);
     }
 
     // Partitions (D12): P context parts; each vertex part split into k sub-parts.

@@ -31,7 +31,8 @@ class ne_config(C.Structure):
     _fields_ = [("dim", C.c_uint32), ("negatives", C.c_uint32), ("walk_len", C.c_uint32),
                 ("window", C.c_uint32), ("walks_per_node", C.c_uint32), ("episodes", C.c_uint32),
                 ("subparts", C.c_uint32), ("deterministic", C.c_uint32), ("conflict_permille", C.c_uint32),
-                ("writeback", C.c_uint32), ("seed", C.c_uint64)]
+                ("writeback", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
+                ("seed", C.c_uint64)]
 
 
 class ne_stats(C.Structure):

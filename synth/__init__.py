@@ -36,6 +36,7 @@ class Workload:
     window: int = 5
     negatives: int = 5
     kind: str = "rmat"  # "rmat" | "uniform" (G(n, m) control without hubs)
+    episodes: int = 1   # episodes per epoch at 1 GPU (HBM budget for the pool)
 
 
 # BASELINE.json configs; SURVEY.md section 8 "C1".."C5".
@@ -43,8 +44,8 @@ CONFIGS = {
     "c1": Workload("rmat-10k-100k", 10_000, 100_000, 128, 1),
     "c2": Workload("youtube-shaped", 1_138_499, 4_945_382, 128, 2),
     "c3": Workload("livejournal-shaped", 4_847_571, 68_993_773, 128, 3),
-    "c4": Workload("friendster-shaped", 65_608_366, 1_806_067_135, 96, 4),
-    "c5": Workload("hyperlink-pld-shaped", 39_497_204, 623_056_313, 256, 5),
+    "c4": Workload("friendster-shaped", 65_608_366, 1_806_067_135, 96, 4, episodes=4),
+    "c5": Workload("hyperlink-pld-shaped", 39_497_204, 623_056_313, 256, 5, episodes=4),
     # L2-reuse control: C3's n and m, uniform degrees (no hubs)
     "c3u": Workload("livejournal-size-uniform", 4_847_571, 68_993_773, 128, 3, kind="uniform"),
 }
@@ -133,11 +134,78 @@ def uniform_graph(n: int, m: int, seed: int):
     return csr_from_undirected(n, u, v)
 
 
-def workload_graph(name: str):
+def workload_graph(name: str, device=None):
+    """CSR of a workload.  Graphs above 200M edges are generated on the GPU
+    (`device`, torch) -- see rmat_graph_torch -- and returned as device tensors."""
     w = CONFIGS[name]
+    if w.m > 200_000_000:
+        return rmat_graph_torch(w.n, w.m, w.graph_seed, device or "cuda")
     if w.kind == "uniform":
         return uniform_graph(w.n, w.m, w.graph_seed)
     return rmat_graph(w.n, w.m, w.graph_seed)
+
+
+def rmat_graph_torch(n: int, m: int, seed: int, device="cuda", abc=RMAT_ABC, batch: int = 1 << 27,
+                     chunk_edges: int = 1 << 28):
+    """R-MAT as rmat_graph, for billion-edge workloads, with torch's generator
+    on `device` (deterministic for a seed on a given GPU type; a different
+    stream from the numpy generator).  Returns (offsets int64[n+1],
+    targets int32[2m]) on `device`; ids are u32 values (n < 2^31 here)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    s = max(1, math.ceil(math.log2(max(n, 2))))
+    a, b, c = abc
+    us, vs, kept = [], [], 0
+    while kept < m:
+        B = min(batch, max(1 << 10, int((m - kept) * 1.6)))
+        u = torch.zeros(B, dtype=torch.int64, device=device)
+        v = torch.zeros(B, dtype=torch.int64, device=device)
+        for lvl in range(s):
+            r = torch.rand(B, generator=g, device=device)
+            u |= (r >= a + b).to(torch.int64) << lvl
+            v |= (((r >= a) & (r < a + b)) | (r >= a + b + c)).to(torch.int64) << lvl
+            del r
+        ok = (u < n) & (v < n) & (u != v)
+        u, v = u[ok], v[ok]
+        take = min(u.numel(), m - kept)
+        us.append(u[:take].to(torch.int32))
+        vs.append(v[:take].to(torch.int32))
+        kept += take
+        del u, v, ok
+    u = torch.cat(us)
+    v = torch.cat(vs)
+    del us, vs
+    perm = torch.randperm(n, generator=g, device=device).to(torch.int32)
+    u = perm[u.long()]
+    v = perm[v.long()]
+    del perm
+    src = torch.cat([u, v])
+    dst = torch.cat([v, u])
+    del u, v
+    nnz = src.numel()
+    counts = torch.bincount(src, minlength=n)
+    offsets = torch.zeros(n + 1, dtype=torch.int64, device=device)
+    torch.cumsum(counts, 0, out=offsets[1:])
+    del counts
+    targets = torch.empty(nnz, dtype=torch.int32, device=device)
+    # sort by (src, dst) one source-id range at a time (bounded temporaries)
+    chunks = max(1, nnz // chunk_edges)
+    cuts = torch.searchsorted(offsets, torch.arange(1, chunks, device=device) * (nnz // chunks)).tolist()
+    bounds = [0] + sorted(set(min(max(int(x), 0), n) for x in cuts)) + [n]
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        if hi <= lo:
+            continue
+        mask = (src >= lo) & (src < hi)
+        keys = (src[mask].to(torch.int64) << 32) | dst[mask].to(torch.int64)
+        del mask
+        keys = torch.sort(keys).values
+        targets[int(offsets[lo]):int(offsets[hi])] = (keys & 0xFFFFFFFF).to(torch.int32)
+        del keys
+    del src, dst
+    if str(device).startswith("cuda"):
+        torch.cuda.empty_cache()
+    return offsets, targets
 
 
 # ------------------------------------------------------------------ small graphs

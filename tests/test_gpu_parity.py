@@ -331,3 +331,43 @@ def test_reload_same_shape_graph_reuses_buffers():
     assert np.abs(eng.embeddings(0) - V).max() <= TOL
     assert np.abs(eng.embeddings(1) - Cm).max() <= TOL
     eng.close()
+
+
+# ---------------------------------------------------------------- NEXT-1 node2vec
+@pytest.mark.parametrize("pq", [(0.5, 2.0), (4.0, 0.25), (1.0, 1.0)])
+def test_node2vec_walks_and_pool_bit_exact(c1, pq):
+    p, q = pq
+    off, tgt = c1
+    n = len(off) - 1
+    eng = engine(p=p, q=q, walks_per_node=2, episodes=2, subparts=2)
+    eng.load_graph(off, tgt)
+    walks = eng.random_walk(3, 1, export=True)
+    u0, units = oracle.episode_units(ocfg(walks_per_node=2, episodes=2), n, len(tgt), 1)
+    for w in range(0, units, 3):
+        ref = oracle.node2vec_walk(off, tgt, 42, 3, u0 + w, 40, p, q)
+        assert np.array_equal(walks[w, :len(ref)], ref)
+        assert (walks[w, len(ref):] == 0xFFFFFFFF).all()
+    eng.build_samples(3, 1)
+    ref, boff = oracle.build_episode(ocfg(p=p, q=q, walks_per_node=2, episodes=2, subparts=2), off, tgt, 3, 1)
+    for vs in range(2):
+        assert np.array_equal(eng.export_samples(vs), ref[int(boff[vs]):int(boff[vs + 1])])
+    eng.close()
+
+
+def test_node2vec_deterministic_epoch():
+    off, tgt = synth.rmat_graph(900, 6000, 35)
+    dv, dc = _det_epoch(off, tgt, epochs=1, dim=64, walk_len=20, window=4, p=0.25, q=4.0)
+    assert dv <= TOL and dc <= TOL, (dv, dc)
+
+
+def test_node2vec_requires_sorted_rows():
+    from paper_2005_13789_b200 import ne
+    off = np.array([0, 3, 4, 5, 6], np.uint64)
+    tgt = np.array([3, 1, 2, 0, 0, 0], np.uint32)   # row 0 = [3, 1, 2] not sorted
+    eng = engine(dim=8, p=0.5, q=2.0, walk_len=5, window=2)
+    with pytest.raises(ne.NEError, match=r"NE_EINVAL: targets\[1\]=1 < targets\[0\]=3"):
+        eng.load_graph(off, tgt)
+    eng.close()
+    eng = engine(dim=8, walk_len=5, window=2)      # first order: order does not matter
+    eng.load_graph(off, tgt)
+    eng.close()

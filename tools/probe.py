@@ -8,11 +8,14 @@ from paper_2005_13789_b200.engine import Engine
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 t = time.time()
-off, tgt = synth.workload_graph(name)
+off, tgt = synth.workload_graph(name, device="cuda")
 print(f"{name}: graph n={len(off)-1} nnz={len(tgt)} gen {time.time()-t:.1f}s", flush=True)
 w = synth.CONFIGS[name]
-eng = Engine(dim=w.dim, deterministic=False)
-t = time.time(); eng.load_graph(off, tgt); print(f"load {time.time()-t:.2f}s", flush=True)
+import torch
+eng = Engine(dim=w.dim, deterministic=False, episodes=w.episodes)
+t = time.time(); eng.load_graph(off, tgt); print(f"load {time.time()-t:.2f}s  mem {torch.cuda.mem_get_info()[0]/1e9:.1f} GB free", flush=True)
+del off, tgt
+torch.cuda.empty_cache()
 for ep in range(epochs):
     t = time.time()
     st = eng.train_epoch(ep, 0.025)
