@@ -99,7 +99,8 @@ def workload_desc(name):
     w = synth.CONFIGS[name]
     gen = "R-MAT (Graph500 a,b,c=.57,.19,.19)" if w.kind == "rmat" else "uniform G(n,m)"
     return w, (f"{w.name} {gen} {w.n:,} nodes / {w.m:,} undirected edges "
-               f"(nnz {2 * w.m:,}), DeepWalk k={w.walk_len} l={w.window} w=1, d={w.dim}, K={w.negatives}")
+               f"(nnz {2 * w.m:,}), {'DeepWalk' if (w.p, w.q) == (1.0, 1.0) else f'node2vec p={w.p} q={w.q}'} "
+               f"k={w.walk_len} l={w.window} w=1, d={w.dim}, K={w.negatives}")
 
 
 def run_reference(args, rank, world):
@@ -199,7 +200,7 @@ def main():
         nccl_id = obj[0]
     stream = torch.cuda.current_stream()
     eng = Engine(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
-                 walks_per_node=1, episodes=episodes, subparts=4, deterministic=False, seed=42,
+                 walks_per_node=1, episodes=episodes, subparts=4, deterministic=False, seed=42, p=w.p, q=w.q,
                  device=local, rank=rank, world=world, nccl_id=nccl_id, torch_allocator=True,
                  stream=stream.cuda_stream)
     eng.load_graph(off, tgt)

@@ -2,11 +2,13 @@
 // (sm_100a): window pairs, canonical Feistel order (O6) and
 // the stable bucketing into 2D blocks.
 //
-// Layout: the pi-indexed slot array (u64 per generation slot, ~0 = hole) is a
-// counting sort by construction -- pi is a bijection, so writing each kept
-// pair to slots[pi(x)] orders the whole episode with one scattered 8-byte
-// store per pair.  A stable multi-way partition then groups the non-hole slots
-// by vertex sub-part while keeping pi order inside each block.
+// Each rank handles only the pairs whose context node it owns: a count pass
+// and an exclusive scan give every kept pair its part-local index x (its rank
+// in generation order); pi over [0, N_g) is a bijection, so writing each pair
+// to slots[pi(x)] orders the rank's pairs with one scattered 8-byte store per
+// pair into a dense N_g-slot array (O(N/P) memory traffic per rank, no holes).
+// A stable multi-way partition then groups the slots by vertex sub-part while
+// keeping pi order inside each block.
 #include <algorithm>
 
 #include "ne_device.cuh"
@@ -30,11 +32,11 @@ Feistel make_feistel(const PoolParams& p) {
     uint32_t b = 0;
     while (b < 64 && (1ull << b) < p.N) ++b;
     if (b < 2) b = 2;
-    if (b & 1) ++b;
     Feistel f;
     f.N = p.N;
-    f.h = b / 2;
-    f.mask = (f.h >= 64) ? ~0ull : ((1ull << f.h) - 1);
+    f.c = b / 2;
+    f.mask_lo = (1ull << f.c) - 1;
+    f.mask_hi = (1ull << (b - f.c)) - 1;
     f.episode = p.episode;
     f.tagw = (kTagShuf << 24) | p.epoch;
     f.key = make_uint2((uint32_t)p.seed, (uint32_t)(p.seed >> 32));
@@ -47,13 +49,10 @@ unsigned grid_cap(uint64_t blocks, const Device& dev, int per_sm) {
 
 }  // namespace
 
-// Warp per walker: the walk (k+1 ids) is staged in shared memory, the Pw
-// window slots are spread over the lanes, and every kept pair is written to
-// slots[pi(x)] with x = (omega - omega0) * Pw + s its local generation index.
-__global__ void __launch_bounds__(kThreads) pairs_walk_kernel(const uint32_t* __restrict__ walks,
+// O5 count, warp per walker: pairs of the walk whose context node is in the part.
+__global__ void __launch_bounds__(kThreads) count_walk_kernel(const uint32_t* __restrict__ walks,
                                                               const uint32_t* __restrict__ slot_tab,
-                                                              PoolParams p, Feistel f,
-                                                              uint64_t* __restrict__ slots) {
+                                                              PoolParams p, uint32_t* __restrict__ counts) {
     extern __shared__ uint32_t smem_path[];
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     uint32_t* path = smem_path + warp * (p.k + 1);
@@ -62,25 +61,91 @@ __global__ void __launch_bounds__(kThreads) pairs_walk_kernel(const uint32_t* __
         const uint32_t* src = walks + w * (uint64_t)(p.k + 1);
         for (uint32_t i = lane; i <= p.k; i += 32) path[i] = src[i];
         __syncwarp();
-        for (uint32_t s = lane; s < p.Pw; s += 32) {
-            const uint32_t t = __ldg(slot_tab + s);
-            const uint32_t i = t >> 16, d = t & 0xFFFFu;
-            const uint32_t b = path[i + d];
-            if (b == kSentinel || b < p.c_begin || b >= p.c_end) continue;  // hole / other part
-            const uint64_t y = f(w * (uint64_t)p.Pw + s);
-            slots[y] = (uint64_t)path[i] | ((uint64_t)b << 32);
+        uint32_t cnt = 0;
+        for (uint32_t s0 = 0; s0 < p.Pw; s0 += 32) {
+            const uint32_t s = s0 + lane;
+            bool kept = false;
+            if (s < p.Pw) {
+                const uint32_t t = __ldg(slot_tab + s);
+                const uint32_t b = path[(t >> 16) + (t & 0xFFFFu)];
+                kept = b != kSentinel && b >= p.c_begin && b < p.c_end;
+            }
+            cnt += __popc(__ballot_sync(0xFFFFFFFFu, kept));
+        }
+        if (lane == 0) counts[w] = cnt;
+        __syncwarp();
+    }
+}
+
+cudaError_t launch_count_walk(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
+                              uint32_t* counts, const Device& dev, cudaStream_t s) {
+    if (p.units == 0) return cudaSuccess;
+    const size_t smem = (size_t)kWarps * (p.k + 1) * sizeof(uint32_t);
+    count_walk_kernel<<<grid_cap(ceil_div(p.units, kWarps), dev, 8), kThreads, smem, s>>>(walks, slot_tab, p, counts);
+    return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kThreads) count_line_kernel(const uint32_t* __restrict__ tgt,
+                                                              PoolParams p, uint32_t* __restrict__ counts) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < p.units; x += stride) {
+        const uint32_t dst = __ldg(tgt + p.u0 + x);
+        counts[x] = (dst >= p.c_begin && dst < p.c_end) ? 1u : 0u;
+    }
+}
+
+cudaError_t launch_count_line(const uint32_t* tgt, const PoolParams& p, uint32_t* counts,
+                              const Device& dev, cudaStream_t s) {
+    if (p.units == 0) return cudaSuccess;
+    count_line_kernel<<<grid_cap(ceil_div(p.units, kThreads), dev, 8), kThreads, 0, s>>>(tgt, p, counts);
+    return cudaGetLastError();
+}
+
+// O5 + O6, warp per walker: the walk is staged in shared memory, the Pw window
+// slots are taken 32 at a time in generation order; a kept pair's local index
+// is base[w] + (kept pairs of earlier rounds) + (kept lanes below it), and the
+// pair lands at slots[pi(x)].
+__global__ void __launch_bounds__(kThreads) pairs_walk_kernel(const uint32_t* __restrict__ walks,
+                                                              const uint32_t* __restrict__ slot_tab,
+                                                              PoolParams p, Feistel f,
+                                                              const uint64_t* __restrict__ base,
+                                                              uint64_t* __restrict__ slots) {
+    extern __shared__ uint32_t smem_path[];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t* path = smem_path + warp * (p.k + 1);
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < p.units; w += nwarps) {
+        const uint32_t* src = walks + w * (uint64_t)(p.k + 1);
+        for (uint32_t i = lane; i <= p.k; i += 32) path[i] = src[i];
+        __syncwarp();
+        uint64_t x = base[w];
+        for (uint32_t s0 = 0; s0 < p.Pw; s0 += 32) {
+            const uint32_t s = s0 + lane;
+            bool kept = false;
+            uint32_t a = 0, b = 0;
+            if (s < p.Pw) {
+                const uint32_t t = __ldg(slot_tab + s);
+                const uint32_t i = t >> 16;
+                b = path[i + (t & 0xFFFFu)];
+                kept = b != kSentinel && b >= p.c_begin && b < p.c_end;
+                a = path[i];
+            }
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, kept);
+            if (kept) slots[f(x + __popc(bal & lt))] = (uint64_t)a | ((uint64_t)b << 32);
+            x += __popc(bal);
         }
         __syncwarp();
     }
 }
 
 cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
-                              uint64_t* slots, const Device& dev, cudaStream_t s) {
-    if (p.units == 0) return cudaSuccess;
+                              const uint64_t* base, uint64_t* slots, const Device& dev, cudaStream_t s) {
+    if (p.units == 0 || p.N == 0) return cudaSuccess;
     const Feistel f = make_feistel(p);
     const size_t smem = (size_t)kWarps * (p.k + 1) * sizeof(uint32_t);
     pairs_walk_kernel<<<grid_cap(ceil_div(p.units, kWarps), dev, 8), kThreads, smem, s>>>(
-        walks, slot_tab, p, f, slots);
+        walks, slot_tab, p, f, base, slots);
     return cudaGetLastError();
 }
 
@@ -88,6 +153,7 @@ cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, c
 __global__ void __launch_bounds__(kThreads) pairs_line_kernel(const uint64_t* __restrict__ off,
                                                               const uint32_t* __restrict__ tgt,
                                                               uint64_t n, PoolParams p, Feistel f,
+                                                              const uint64_t* __restrict__ base,
                                                               uint64_t* __restrict__ slots) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < p.units; x += stride) {
@@ -95,17 +161,17 @@ __global__ void __launch_bounds__(kThreads) pairs_line_kernel(const uint64_t* __
         const uint32_t dst = __ldg(tgt + e);
         if (dst < p.c_begin || dst >= p.c_end) continue;
         const uint32_t src = range_of(off, (uint32_t)n, e);
-        slots[f(x)] = (uint64_t)src | ((uint64_t)dst << 32);
+        slots[f(base[x])] = (uint64_t)src | ((uint64_t)dst << 32);
     }
 }
 
 cudaError_t launch_pairs_line(const uint64_t* off, const uint32_t* tgt, uint64_t n,
-                              const PoolParams& p, uint64_t* slots, const Device& dev,
-                              cudaStream_t s) {
-    if (p.units == 0) return cudaSuccess;
+                              const PoolParams& p, const uint64_t* base, uint64_t* slots,
+                              const Device& dev, cudaStream_t s) {
+    if (p.units == 0 || p.N == 0) return cudaSuccess;
     const Feistel f = make_feistel(p);
     pairs_line_kernel<<<grid_cap(ceil_div(p.units, kThreads), dev, 8), kThreads, 0, s>>>(
-        off, tgt, n, p, f, slots);
+        off, tgt, n, p, f, base, slots);
     return cudaGetLastError();
 }
 
@@ -264,6 +330,22 @@ __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const uint64_t
         }
         __syncthreads();
     }
+}
+
+size_t scan_scratch_bytes(uint64_t M) {
+    const uint64_t nchunks = std::max<uint64_t>(1, ceil_div(M, kScanChunk));
+    return (nchunks + 2) * sizeof(uint64_t) + 64;
+}
+
+cudaError_t launch_scan(const uint32_t* in, uint64_t M, uint64_t* out, uint64_t* total, void* scratch,
+                        cudaStream_t s, uint32_t* launches) {
+    const uint64_t nchunks = std::max<uint64_t>(1, ceil_div(M, kScanChunk));
+    uint64_t* sums = reinterpret_cast<uint64_t*>(scratch);
+    scan_sums_kernel<<<(unsigned)nchunks, kThreads, 0, s>>>(in, M, sums);
+    scan_partials_kernel<<<1, 32, 0, s>>>(sums, nchunks, total);
+    scan_chunks_kernel<<<(unsigned)nchunks, kThreads, 0, s>>>(in, M, sums, out);
+    if (launches) *launches += 3;
+    return cudaGetLastError();
 }
 
 size_t bucket_scratch_bytes(uint64_t N, uint32_t nb) {

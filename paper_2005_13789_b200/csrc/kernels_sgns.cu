@@ -237,7 +237,9 @@ static cudaError_t launch_sgns_k(const SgnsParams& p, const Device& dev, cudaStr
         return launch_sgns_v<G, R, KT, 1>(p, dev, s);
     }
     static const int knob = env_int("NE_SGNS_MINB", 0);
-    int minb = knob >= 1 && knob <= 4 ? knob : (G == 16 ? 2 : 3);
+    // 16-lane groups hold two samples' rows per lane, 32-lane groups with R = 2
+    // (d <= 256) hold 2 float4 per row: both need the 128-register budget of 2 CTAs
+    int minb = knob >= 1 && knob <= 4 ? knob : (G == 16 || R == 2 ? 2 : 3);
     if (KT == 0) minb = std::min(minb, 2);  // runtime K keeps kMaxK+1 rows live: stay spill-free
     switch (minb) {
         case 1: return launch_sgns_v<G, R, KT, 1>(p, dev, s);

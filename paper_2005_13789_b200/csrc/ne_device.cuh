@@ -41,25 +41,27 @@ __device__ __forceinline__ uint64_t uniform_index(uint32_t lo, uint32_t hi, uint
     return __umul64hi(((uint64_t)hi << 32) | lo, n);
 }
 
-// O6: Feistel network on b = 2h bits, 4 rounds, cycle-walked into [0, N).
+// O6: alternating Feistel network on b = max(2, ceil(log2 N)) bits split into
+// hi (b - b/2 bits) and lo (b/2 bits); rounds 0..3 alternate hi ^= F(lo) and
+// lo ^= F(hi), F = Philox(v, episode, round, SHUF|epoch).x0 masked; cycle-walked
+// into [0, N) (domain < 2N: < 2 passes on average).
 struct Feistel {
     uint64_t N;
-    uint32_t h;
-    uint64_t mask;
+    uint32_t c;                 // lo bits
+    uint64_t mask_lo, mask_hi;
     uint32_t episode, tagw;
     uint2 key;
     __device__ __forceinline__ uint64_t operator()(uint64_t x) const {
         uint64_t y = x;
         do {
-            uint64_t L = y >> h, R = y & mask;
+            uint64_t hi = y >> c, lo = y & mask_lo;
 #pragma unroll
             for (uint32_t i = 0; i < 4; ++i) {
-                const uint4 o = philox(make_uint4((uint32_t)R, episode, i, tagw), key);
-                const uint64_t nl = R;
-                R = L ^ ((uint64_t)o.x & mask);
-                L = nl;
+                const uint4 o = philox(make_uint4((uint32_t)((i & 1) ? hi : lo), episode, i, tagw), key);
+                if (i & 1) lo ^= (uint64_t)o.x & mask_lo;
+                else hi ^= (uint64_t)o.x & mask_hi;
             }
-            y = (L << h) | R;
+            y = (hi << c) | lo;
         } while (y >= N);
         return y;
     }

@@ -32,7 +32,7 @@ cudaError_t launch_walk(const uint64_t* off, const uint32_t* tgt, uint64_t n, ui
 
 // ---- sample pool (kernels_samples.cu) ---------------------------------------
 struct PoolParams {
-    uint64_t N;           // slots of the episode (units * Pw)
+    uint64_t N;           // this rank's pairs in the episode (Feistel domain, O6)
     uint64_t units;       // walkers (DeepWalk) or edges (LINE) of the episode
     uint64_t u0;          // first unit (edge id in LINE mode)
     uint32_t k, l, Pw;    // walk steps, window, pairs per full walk (1 in LINE mode)
@@ -40,15 +40,26 @@ struct PoolParams {
     uint64_t seed;
     uint64_t c_begin, c_end;   // this rank's context part
 };
-// O5 + O6: kept pairs (dst in the context part) -> slots[pi(x)], holes = ~0.
-// slot_tab[s] = (i << 16) | delta for s < Pw.
+// O5 count: counts[u] = pairs of unit u whose context node lies in this
+// rank's part.  slot_tab[s] = (i << 16) | delta for s < Pw.
+cudaError_t launch_count_walk(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
+                              uint32_t* counts, const Device& dev, cudaStream_t s);
+cudaError_t launch_count_line(const uint32_t* tgt, const PoolParams& p, uint32_t* counts,
+                              const Device& dev, cudaStream_t s);
+// Exclusive scan u32 -> u64 over M values; *total = sum.  scratch >= scan_scratch_bytes(M).
+size_t scan_scratch_bytes(uint64_t M);
+cudaError_t launch_scan(const uint32_t* in, uint64_t M, uint64_t* out, uint64_t* total, void* scratch,
+                        cudaStream_t s, uint32_t* launches);
+// O5 + O6: the kept pairs of unit u get part-local indices base[u] + rank
+// (generation order) and land at slots[pi(x)], pi the Feistel bijection over
+// [0, p.N): a dense array, no holes.
 cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
-                              uint64_t* slots, const Device& dev, cudaStream_t s);
+                              const uint64_t* base, uint64_t* slots, const Device& dev, cudaStream_t s);
 cudaError_t launch_pairs_line(const uint64_t* off, const uint32_t* tgt, uint64_t n,
-                              const PoolParams& p, uint64_t* slots, const Device& dev,
-                              cudaStream_t s);
-// Stable partition of the non-hole slots by vertex sub-part (bounds over
-// nb+1 entries, device pointer): pool[block_offsets[b] ...] in slot order.
+                              const PoolParams& p, const uint64_t* base, uint64_t* slots,
+                              const Device& dev, cudaStream_t s);
+// Stable partition of the slots by vertex sub-part (bounds over nb+1 entries,
+// device pointer): pool[block_offsets[b] ...] in slot order.
 size_t bucket_scratch_bytes(uint64_t N, uint32_t nb);
 cudaError_t launch_bucket(const uint64_t* slots, uint64_t N, const uint64_t* sub_bounds,
                           uint32_t nb, void* scratch, uint64_t* pool, uint64_t* block_offsets,

@@ -61,6 +61,10 @@ struct ne_ctx {
     uint64_t* d_slots = nullptr;
     uint64_t* d_pool = nullptr;
     void* d_scratch = nullptr;
+    uint32_t* d_counts = nullptr;   // per-unit kept-pair counts (O5)
+    uint64_t* d_base = nullptr;     // their exclusive scan: part-local index bases
+    void* d_scan_scratch = nullptr;
+    uint64_t* d_total = nullptr;    // N_g of the episode
     uint64_t* d_boff = nullptr;
     std::vector<uint64_t> boff;
     double* d_loss = nullptr;
@@ -326,21 +330,36 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     p.k = c->cfg.walk_len;
     p.l = c->cfg.window;
     p.Pw = c->Pw;
-    p.N = units * c->Pw;
     p.episode = episode;
     p.epoch = epoch;
     p.seed = c->cfg.seed;
     p.c_begin = c->c_begin;
     p.c_end = c->c_begin + c->c_count;
-    if (p.N) {
-        NE_CUDA(c, cudaMemsetAsync(c->d_slots, 0xFF, p.N * sizeof(uint64_t), c->stream));
+    // O5: kept pairs per unit, exclusive scan -> part-local index bases, N_g
+    uint64_t N = 0;
+    if (units) {
         if (c->cfg.walk_len > 0)
-            NE_CUDA(c, ne::launch_pairs_walk(c->d_walks, c->d_slot_tab, p, c->d_slots, c->dev, c->stream));
+            NE_CUDA(c, ne::launch_count_walk(c->d_walks, c->d_slot_tab, p, c->d_counts, c->dev, c->stream));
         else
-            NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_slots, c->dev, c->stream));
+            NE_CUDA(c, ne::launch_count_line(c->d_tgt, p, c->d_counts, c->dev, c->stream));
+        c->launches += 1;
+        NE_CUDA(c, ne::launch_scan(c->d_counts, units, c->d_base, c->d_total, c->d_scan_scratch, c->stream,
+                                   &c->launches));
+        NE_CUDA(c, cudaMemcpyAsync(&N, c->d_total, sizeof N, cudaMemcpyDeviceToHost, c->stream));
+        NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > capacity %llu", (unsigned long long)N,
+                                  (unsigned long long)c->N_max);
+    // O6: every kept pair to slots[pi(x)] (dense [0, N)), then stable bucketing
+    p.N = N;
+    if (N) {
+        if (c->cfg.walk_len > 0)
+            NE_CUDA(c, ne::launch_pairs_walk(c->d_walks, c->d_slot_tab, p, c->d_base, c->d_slots, c->dev, c->stream));
+        else
+            NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_base, c->d_slots, c->dev, c->stream));
         c->launches += 1;
     }
-    NE_CUDA(c, ne::launch_bucket(c->d_slots, p.N, c->d_sub_bounds, nb_local(c), c->d_scratch,
+    NE_CUDA(c, ne::launch_bucket(c->d_slots, N, c->d_sub_bounds, nb_local(c), c->d_scratch,
                                  c->d_pool, c->d_boff, c->dev, c->stream, &c->launches));
     c->boff.assign(nb_local(c) + 1, 0);
     NE_CUDA(c, cudaMemcpyAsync(c->boff.data(), c->d_boff, c->boff.size() * sizeof(uint64_t),
@@ -695,6 +714,10 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
         NE_CUDA(c, cudaMemcpyAsync(c->d_slot_tab, tab_s.data(), tab_s.size() * sizeof(uint32_t),
                                    cudaMemcpyHostToDevice, c->stream));
     }
+    NE_ALLOC(c->d_counts, std::max<uint64_t>(c->units_max, 1));
+    NE_ALLOC(c->d_base, std::max<uint64_t>(c->units_max, 1));
+    if (!reuse) NE_TRY(dalloc(c, &c->d_scan_scratch, ne::scan_scratch_bytes(c->units_max)));
+    NE_ALLOC(c->d_total, 1);
     NE_ALLOC(c->d_slots, std::max<uint64_t>(c->N_max, 1));
     NE_ALLOC(c->d_pool, std::max<uint64_t>(c->N_max, 1));
     if (!reuse) NE_TRY(dalloc(c, &c->d_scratch, ne::bucket_scratch_bytes(c->N_max, nb_local(c))));

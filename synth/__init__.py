@@ -37,6 +37,8 @@ class Workload:
     negatives: int = 5
     kind: str = "rmat"  # "rmat" | "uniform" (G(n, m) control without hubs)
     episodes: int = 1   # episodes per epoch at 1 GPU (HBM budget for the pool)
+    p: float = 1.0      # node2vec return parameter (1, 1 = first-order DeepWalk)
+    q: float = 1.0      # node2vec in-out parameter
 
 
 # BASELINE.json configs; SURVEY.md section 8 "C1".."C5".
@@ -45,7 +47,9 @@ CONFIGS = {
     "c2": Workload("youtube-shaped", 1_138_499, 4_945_382, 128, 2),
     "c3": Workload("livejournal-shaped", 4_847_571, 68_993_773, 128, 3),
     "c4": Workload("friendster-shaped", 65_608_366, 1_806_067_135, 96, 4, episodes=4),
-    "c5": Workload("hyperlink-pld-shaped", 39_497_204, 623_056_313, 256, 5, episodes=4),
+    # BASELINE configs[4]: "node2vec-style walks"; p = 1, q = 0.5 (outward-biased,
+    # a common node2vec setting -- the paper gives none)
+    "c5": Workload("hyperlink-pld-shaped", 39_497_204, 623_056_313, 256, 5, episodes=4, q=0.5),
     # L2-reuse control: C3's n and m, uniform degrees (no hubs)
     "c3u": Workload("livejournal-size-uniform", 4_847_571, 68_993_773, 128, 3, kind="uniform"),
 }

@@ -113,7 +113,7 @@ def test_augment_worked_example(orc):
 # ---------------------------------------------------------------- O6 order
 def test_feistel_bits(orc):
     assert [orc.feistel_bits(N) for N in (1, 2, 3, 4, 5, 16, 17, 1 << 20, (1 << 20) + 1)] == \
-           [2, 2, 2, 2, 4, 4, 6, 20, 22]
+           [2, 2, 2, 2, 3, 4, 5, 20, 21]
 
 
 @pytest.mark.parametrize("N", list(range(1, 130)) + [255, 256, 257, 1000, 4097])
@@ -174,23 +174,56 @@ def test_episode_pool_counts_reachability_blocks(orc):
         assert ((blk[:, 1] >= pb[cp]) & (blk[:, 1] < pb[cp + 1])).all()
 
 
-def test_canonical_order_is_global(orc):
-    # the order inside a block is the subsequence of the P=1, k=1 order (one
-    # global permutation per episode, independent of the partitioning)
+def _generation_order(orc, off, tgt, cfg, epoch, episode):
+    """The episode's pairs in generation order (O5): walkers ascending, window
+    slots i-major / delta-minor, holes skipped -- from the pinned walk."""
+    n = len(off) - 1
+    u0, units = orc.episode_units(cfg, n, len(tgt), episode)
+    out = []
+    for w in range(u0, u0 + units):
+        path = orc.random_walk(off, tgt, cfg.seed, epoch, w, cfg.walk_len)
+        for i in range(cfg.walk_len):
+            for d in range(1, cfg.window + 1):
+                if i + d <= cfg.walk_len and i + d < len(path):
+                    out.append((int(path[i]), int(path[i + d])))
+    return out
+
+
+def test_canonical_order_single_part(orc):
+    # P = 1, one sub-part: pool[pi(x)] is the x-th generated pair, pi the
+    # Feistel bijection over the episode's N pairs (O6)
+    off, tgt = synth.rmat_graph(200, 1000, 5)
+    cfg = _cfg(orc, walk_len=6, window=2)
+    gen = _generation_order(orc, off, tgt, cfg, 4, 0)
+    pool, _ = orc.build_episode(cfg, off, tgt, 4, 0)
+    N = len(gen)
+    assert len(pool) == N
+    for x, pair in enumerate(gen):
+        assert tuple(pool[orc.feistel(x, N, 0, 4, cfg.seed)]) == pair
+
+
+def test_canonical_order_per_part(orc):
+    # P = 2, k = 2: pairs of context part g, in generation order, get local
+    # indices 0..N_g-1; inside every block the order is ascending pi_g(index)
     n = 200
     off, tgt = synth.rmat_graph(n, 1000, 5)
-    one, _ = orc.build_episode(_cfg(orc, walk_len=6, window=2), off, tgt, 0, 0)
-    many, boff = orc.build_episode(_cfg(orc, walk_len=6, window=2, parts=2, subparts=2), off, tgt, 0, 0)
-    assert sorted(map(tuple, one.tolist())) == sorted(map(tuple, many.tolist()))
+    cfg = _cfg(orc, walk_len=6, window=2, parts=2, subparts=2)
+    gen = _generation_order(orc, off, tgt, cfg, 0, 0)
+    pool, boff = orc.build_episode(cfg, off, tgt, 0, 0)
     pb = orc.partition_bounds(0, n, 2).astype(np.int64)
-    for B in range(8):
-        blk = many[int(boff[B]):int(boff[B + 1])]
-        vs, cp = divmod(B, 2)
-        vp, t = divmod(vs, 2)
+    part = [int(np.searchsorted(pb, d, side="right") - 1) for _, d in gen]
+    Ng = [part.count(0), part.count(1)]
+    nxt, keyed = [0, 0], []
+    for (s_, d), g in zip(gen, part):
+        vp = int(np.searchsorted(pb, s_, side="right") - 1)
         sb = orc.partition_bounds(int(pb[vp]), int(pb[vp + 1]), 2).astype(np.int64)
-        sel = one[(one[:, 0] >= sb[t]) & (one[:, 0] < sb[t + 1]) &
-                  (one[:, 1] >= pb[cp]) & (one[:, 1] < pb[cp + 1])]
-        assert np.array_equal(sel, blk)
+        t = int(np.searchsorted(sb, s_, side="right") - 1)
+        B = (vp * 2 + t) * 2 + g
+        keyed.append((B, orc.feistel(nxt[g], Ng[g], 0, 0, cfg.seed), (s_, d)))
+        nxt[g] += 1
+    keyed.sort()
+    assert [k[2] for k in keyed] == [tuple(p) for p in pool.tolist()]
+    assert [int(x) for x in boff] == [sum(1 for k in keyed if k[0] < B) for B in range(9)]
 
 
 def test_episodes_partition_the_epoch(orc):

@@ -10,9 +10,11 @@ epochs = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 t = time.time()
 off, tgt = synth.workload_graph(name, device="cuda")
 print(f"{name}: graph n={len(off)-1} nnz={len(tgt)} gen {time.time()-t:.1f}s", flush=True)
+import torch
+if torch.cuda.is_available(): print(f"after gen: {torch.cuda.mem_get_info()[0]/1e9:.1f} GB free", flush=True)
 w = synth.CONFIGS[name]
 import torch
-eng = Engine(dim=w.dim, deterministic=False, episodes=w.episodes)
+eng = Engine(dim=w.dim, deterministic=False, episodes=w.episodes, p=w.p, q=w.q)
 t = time.time(); eng.load_graph(off, tgt); print(f"load {time.time()-t:.2f}s  mem {torch.cuda.mem_get_info()[0]/1e9:.1f} GB free", flush=True)
 del off, tgt
 torch.cuda.empty_cache()
