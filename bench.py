@@ -99,8 +99,9 @@ def workload_desc(name):
     w = synth.CONFIGS[name]
     gen = "R-MAT (Graph500 a,b,c=.57,.19,.19)" if w.kind == "rmat" else "uniform G(n,m)"
     return w, (f"{w.name} {gen} {w.n:,} nodes / {w.m:,} undirected edges "
-               f"(nnz {2 * w.m:,}), {'DeepWalk' if (w.p, w.q) == (1.0, 1.0) else f'node2vec p={w.p} q={w.q}'} "
-               f"k={w.walk_len} l={w.window} w=1, d={w.dim}, K={w.negatives}")
+               f"(nnz {2 * w.m:,}), " + (f"LINE edge pool, d={w.dim}, K={w.negatives}" if w.walk_len == 0 else
+               f"{'DeepWalk' if (w.p, w.q) == (1.0, 1.0) else f'node2vec p={w.p} q={w.q}'} "
+               f"k={w.walk_len} l={w.window} w=1, d={w.dim}, K={w.negatives}"))
 
 
 def run_reference(args, rank, world):

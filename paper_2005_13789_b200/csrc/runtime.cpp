@@ -310,10 +310,25 @@ uint32_t nb_local(const ne_ctx* c) { return (uint32_t)c->world * c->cfg.subparts
 int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     uint64_t u0, units;
     episode_range(c, episode, &u0, &units);
-    NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0, units, c->cfg.walk_len,
-                               c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr, c->d_walks, c->dev,
-                               c->stream));
-    if (units) c->launches += 1;
+    const uint64_t row = c->cfg.walk_len + 1;
+    if (c->world > 1 && c->comm && units) {
+        // Walkers sharded over the ranks, walks all-gathered over NVLink: each
+        // rank walks ceil(units/P) walkers into its slice (in place).
+        const uint64_t P = (uint64_t)c->world, chunk = (units + P - 1) / P;
+        const uint64_t mine_b = std::min<uint64_t>(units, (uint64_t)c->rank * chunk);
+        const uint64_t mine = std::min<uint64_t>(units, mine_b + chunk) - mine_b;
+        NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0 + mine_b, mine, c->cfg.walk_len,
+                                   c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr,
+                                   c->d_walks + mine_b * row, c->dev, c->stream));
+        if (mine) c->launches += 1;
+        NE_NCCL(c, ncclAllGather(c->d_walks + (uint64_t)c->rank * chunk * row, c->d_walks, chunk * row,
+                                 ncclUint32, c->comm, c->stream));
+    } else {
+        NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0, units, c->cfg.walk_len,
+                                   c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr, c->d_walks, c->dev,
+                                   c->stream));
+        if (units) c->launches += 1;
+    }
     c->walked_epoch = epoch;
     c->walked_episode = episode;
     c->walked_units = units;
@@ -706,7 +721,9 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     c->units_max = (c->units_total + g.episodes - 1) / g.episodes;
     c->N_max = c->units_max * c->Pw;
     if (g.walk_len > 0) {
-        NE_ALLOC(c->d_walks, std::max<uint64_t>(c->units_max, 1) * (g.walk_len + 1));
+        // rows padded to a multiple of world for the sharded walk's all-gather
+        const uint64_t wrows = (c->units_max + P - 1) / P * P;
+        NE_ALLOC(c->d_walks, std::max<uint64_t>(wrows, 1) * (g.walk_len + 1));
         std::vector<uint32_t> tab_s;
         for (uint32_t i = 0; i < g.walk_len; ++i)
             for (uint32_t dl = 1; dl <= g.window && i + dl <= g.walk_len; ++dl) tab_s.push_back((i << 16) | dl);

@@ -50,6 +50,8 @@ CONFIGS = {
     # BASELINE configs[4]: "node2vec-style walks"; p = 1, q = 0.5 (outward-biased,
     # a common node2vec setting -- the paper gives none)
     "c5": Workload("hyperlink-pld-shaped", 39_497_204, 623_056_313, 256, 5, episodes=4, q=0.5),
+    # BASELINE configs[2] "LINE/DeepWalk": the LINE edge-list pool on the C3 graph
+    "c3l": Workload("livejournal-shaped-line", 4_847_571, 68_993_773, 128, 3, walk_len=0, window=0),
     # L2-reuse control: C3's n and m, uniform degrees (no hubs)
     "c3u": Workload("livejournal-size-uniform", 4_847_571, 68_993_773, 128, 3, kind="uniform"),
 }

@@ -371,3 +371,29 @@ def test_node2vec_requires_sorted_rows():
     eng = engine(dim=8, walk_len=5, window=2)      # first order: order does not matter
     eng.load_graph(off, tgt)
     eng.close()
+
+
+def test_hogwild_auc_gate_c1():
+    """SURVEY 8(c) gate: production (Hogwild) AUC within 0.01 of the oracle on
+    C1 with 10% held-out edges after 5 epochs (several production runs)."""
+    w = synth.CONFIGS["c1"]
+    u, v = synth.rmat_edges(w.n, w.m, w.graph_seed)
+    off, tgt, test = synth.split_edges(w.n, u, v, 0.1, synth.EVAL_SEED)
+    neg = synth.negative_pairs(w.n, u, v, len(test), synth.EVAL_SEED + 1)
+    cfg = ocfg()
+    V = oracle.init_vertex(w.n, 128, 42)
+    Cm = np.zeros_like(V)
+    tables = oracle.build_alias_tables(cfg, off)
+    for ep in range(5):
+        oracle.train_epoch(cfg, off, tgt, V, Cm, ep, 0.025, tables=tables)
+    a_ref = oracle.auc(oracle.score_pairs(V, Cm, test), oracle.score_pairs(V, Cm, neg))
+    aucs = []
+    for run in range(3):
+        eng = engine(deterministic=False)
+        eng.load_graph(off, tgt)
+        for ep in range(5):
+            eng.train_epoch(ep, 0.025)
+        Vg, Cg = eng.embeddings(0), eng.embeddings(1)
+        aucs.append(oracle.auc(oracle.score_pairs(Vg, Cg, test), oracle.score_pairs(Vg, Cg, neg)))
+        eng.close()
+    assert all(abs(a - a_ref) <= 0.01 for a in aucs), (a_ref, aucs)
