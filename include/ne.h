@@ -52,8 +52,9 @@ enum {
 
 /* ne_train_epoch flags. */
 enum {
-    NE_REUSE_SAMPLES = 1u  /* train again on the pool built earlier instead of
+    NE_REUSE_SAMPLES = 1u, /* train again on the pool built earlier instead of
                               walking anew (walk reuse); needs episodes == 1 */
+    NE_CHECK_BLOCKS = 2u   /* verify every pool after it is built (ne_check_pool)   */
 };
 
 /* ne_config.writeback */
@@ -178,7 +179,7 @@ int ne_build_samples(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint64_t *n_
  * rank), then sends that sub-part to rank+1 and receives the next from
  * rank-1.  Each positive sample (u, v) gets K alias negatives (O8) and
  * 1+K sequential SGNS updates (O10).  stats may be NULL.
- * Errors: NE_ESTATE, NE_ENCCL, NE_ECUDA, NE_ESCHED (debug builds). */
+ * Errors: NE_ESTATE, NE_ENCCL, NE_ECUDA. */
 int ne_train_samples(ne_ctx *ctx, uint32_t epoch, uint32_t episode, float lr, ne_stats *stats);
 
 /* One epoch ("one epoch goes over all the sampled edges"): for every
@@ -205,6 +206,13 @@ const char *ne_last_error(const ne_ctx *ctx);
 
 /* Release the context and all its device memory. */
 void ne_destroy(ne_ctx *ctx);
+
+/* Schedule check of the current pool ("orthogonal vertex
+ * usage"): every sample of block (vsub, rank) must have its source in vertex
+ * sub-part vsub and its context node in this rank's part.  Returns NE_OK, or
+ * NE_ESCHED with the first offending position and its block in the message.
+ * ne_train_epoch runs it after each build with the NE_CHECK_BLOCKS flag. */
+int ne_check_pool(ne_ctx *ctx);
 
 /* ---- test hooks (bit-exact parity against the oracle) -------------------- */
 

@@ -103,18 +103,25 @@ cudaError_t launch_count_line(const uint32_t* tgt, const PoolParams& p, uint32_t
 
 // O5 + O6, warp per walker: the walk is staged in shared memory, the Pw window
 // slots are taken 32 at a time in generation order; a kept pair's local index
-// is base[w] + (kept pairs of earlier rounds) + (kept lanes below it), and the
-// pair lands at slots[pi(x)].
+// is base[w] + (kept pairs of earlier rounds) + (kept lanes below it).  Kept
+// (x, pair) items go to a per-warp queue in shared memory and the Feistel runs
+// on full batches of 32 queued items -- all lanes busy -- instead of on every
+// round with the holes and foreign-part slots idling most lanes.
+constexpr uint32_t kQueue = 64;  // per-warp queue capacity (>= 2 x 32)
+
 __global__ void __launch_bounds__(kThreads) pairs_walk_kernel(const uint32_t* __restrict__ walks,
                                                               const uint32_t* __restrict__ slot_tab,
                                                               PoolParams p, Feistel f,
                                                               const uint64_t* __restrict__ base,
                                                               uint64_t* __restrict__ slots) {
-    extern __shared__ uint32_t smem_path[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    uint32_t* path = smem_path + warp * (p.k + 1);
+    uint64_t* qx = reinterpret_cast<uint64_t*>(smem_raw) + (size_t)warp * 2 * kQueue;  // local index
+    uint64_t* qp = qx + kQueue;                                                        // pair
+    uint32_t* path = reinterpret_cast<uint32_t*>(smem_raw + (size_t)kWarps * 2 * kQueue * 8) + warp * (p.k + 1);
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t qn = 0;  // queued items (warp-uniform)
     for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < p.units; w += nwarps) {
         const uint32_t* src = walks + w * (uint64_t)(p.k + 1);
         for (uint32_t i = lane; i <= p.k; i += 32) path[i] = src[i];
@@ -132,18 +139,34 @@ __global__ void __launch_bounds__(kThreads) pairs_walk_kernel(const uint32_t* __
                 a = path[i];
             }
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, kept);
-            if (kept) slots[f(x + __popc(bal & lt))] = (uint64_t)a | ((uint64_t)b << 32);
+            if (kept) {
+                const uint32_t r = __popc(bal & lt);
+                qx[qn + r] = x + r;
+                qp[qn + r] = (uint64_t)a | ((uint64_t)b << 32);
+            }
             x += __popc(bal);
+            qn += __popc(bal);
+            __syncwarp();
+            if (qn >= 32) {  // one full batch: every lane permutes one item
+                slots[f(qx[lane])] = qp[lane];
+                __syncwarp();
+                if (lane < qn - 32) {
+                    qx[lane] = qx[32 + lane];
+                    qp[lane] = qp[32 + lane];
+                }
+                qn -= 32;
+                __syncwarp();
+            }
         }
-        __syncwarp();
     }
+    if (lane < qn) slots[f(qx[lane])] = qp[lane];  // the partial last batch
 }
 
 cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
                               const uint64_t* base, uint64_t* slots, const Device& dev, cudaStream_t s) {
     if (p.units == 0 || p.N == 0) return cudaSuccess;
     const Feistel f = make_feistel(p);
-    const size_t smem = (size_t)kWarps * (p.k + 1) * sizeof(uint32_t);
+    const size_t smem = (size_t)kWarps * (2 * kQueue * sizeof(uint64_t) + (p.k + 1) * sizeof(uint32_t));
     pairs_walk_kernel<<<grid_cap(ceil_div(p.units, kWarps), dev, 8), kThreads, smem, s>>>(
         walks, slot_tab, p, f, base, slots);
     return cudaGetLastError();
@@ -330,6 +353,31 @@ __global__ void __launch_bounds__(kThreads) bucket_scatter_kernel(const uint64_t
         }
         __syncthreads();
     }
+}
+
+// S:230 schedule check: every sample at position i of the pool lies in its 2D
+// block -- src in the block's vertex sub-part, dst in this rank's context part.
+// bad[0] = first offending position (or ~0).
+__global__ void check_pool_kernel(const uint64_t* __restrict__ pool, const uint64_t* __restrict__ boff,
+                                  const uint64_t* __restrict__ sub_bounds, uint32_t nb, uint64_t c_begin,
+                                  uint64_t c_end, unsigned long long* bad) {
+    const uint64_t total = boff[nb];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const uint32_t b = range_of(boff, nb, i);
+        const uint32_t src = (uint32_t)pool[i], dst = (uint32_t)(pool[i] >> 32);
+        if (src < sub_bounds[b] || src >= sub_bounds[b + 1] || dst < c_begin || dst >= c_end)
+            atomicMin(bad, (unsigned long long)i);
+    }
+}
+
+cudaError_t launch_check_pool(const uint64_t* pool, const uint64_t* boff, uint64_t total,
+                              const uint64_t* sub_bounds, uint32_t nb, uint64_t c_begin, uint64_t c_end,
+                              unsigned long long* bad, const Device& dev, cudaStream_t s) {
+    if (total == 0) return cudaSuccess;
+    check_pool_kernel<<<grid_cap(ceil_div(total, kThreads), dev, 8), kThreads, 0, s>>>(
+        pool, boff, sub_bounds, nb, c_begin, c_end, bad);
+    return cudaGetLastError();
 }
 
 size_t scan_scratch_bytes(uint64_t M) {

@@ -215,7 +215,7 @@ static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStr
         return cudaGetLastError();
     }
     const uint64_t warps = want / S;
-    const uint64_t full = (uint64_t)dev.sm_count * per_sm;
+    const uint64_t full = (uint64_t)std::max(1, dev.sm_count - p.reserve_sms) * per_sm;
     const int wpb = kSgnsThreads / 32;
     if (warps >= full * wpb) {
         kern<<<(unsigned)full, kSgnsThreads, 0, s>>>(p);

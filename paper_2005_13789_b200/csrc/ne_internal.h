@@ -58,6 +58,10 @@ cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, c
 cudaError_t launch_pairs_line(const uint64_t* off, const uint32_t* tgt, uint64_t n,
                               const PoolParams& p, const uint64_t* base, uint64_t* slots,
                               const Device& dev, cudaStream_t s);
+// first pool position outside its 2D block -> *bad (atomicMin; init ~0).
+cudaError_t launch_check_pool(const uint64_t* pool, const uint64_t* boff, uint64_t total,
+                              const uint64_t* sub_bounds, uint32_t nb, uint64_t c_begin, uint64_t c_end,
+                              unsigned long long* bad, const Device& dev, cudaStream_t s);
 // Stable partition of the slots by vertex sub-part (bounds over nb+1 entries,
 // device pointer): pool[block_offsets[b] ...] in slot order.
 size_t bucket_scratch_bytes(uint64_t N, uint32_t nb);
@@ -82,6 +86,7 @@ struct SgnsParams {
     int deterministic;          // 1: one warp, canonical order
     uint64_t max_warps;         // Hogwild concurrency cap (>= 1)
     int atomic_writeback;       // Hogwild: red.add row deltas instead of storing rows
+    int reserve_sms;            // SMs left free for the concurrent NCCL ring kernels
 };
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s);
 cudaError_t launch_sgns_tma(const SgnsParams& p, const Device& dev, cudaStream_t s);  // kernels_sgns_tma.cu

@@ -15,6 +15,7 @@
 #include <memory>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -412,6 +413,13 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
     const double cap = eps / (kk / cr + 1.0 / vr);
     p.max_warps = cap >= 1e15 ? ~0ull : std::max<uint64_t>(1, (uint64_t)cap);
     p.atomic_writeback = c->cfg.writeback == NE_WB_ATOMIC_DELTA ? 1 : 0;
+    // with a ring, leave SMs to NCCL's send/recv kernels so the transfer of the
+    // previous sub-part overlaps this block (developer knob NE_RING_RESERVE_SMS)
+    static const int reserve = [] {
+        const char* e = std::getenv("NE_RING_RESERVE_SMS");
+        return e ? std::atoi(e) : 2;
+    }();
+    p.reserve_sms = (c->world > 1 && c->comm) ? reserve : 0;
     return p;
 }
 
@@ -806,6 +814,7 @@ int ne_train_epoch(ne_ctx* c, uint32_t epoch, float lr, uint32_t flags, ne_stats
             if (c->cfg.walk_len > 0) NE_TRY(do_walk(c, epoch, e));
             NE_CUDA(c, cudaEventRecord(b, c->stream));
             NE_TRY(do_build(c, epoch, e));  // synchronises the stream
+            if (flags & NE_CHECK_BLOCKS) NE_TRY(ne_check_pool(c));
             NE_CUDA(c, cudaEventRecord(d, c->stream));
             NE_CUDA(c, cudaEventSynchronize(d));
             float mw = 0.f, mb = 0.f;
@@ -946,6 +955,27 @@ int ne_train_samples_local_ring(ne_ctx* const* ctxs, uint32_t world, uint32_t ep
     NE_CUDA(c0, cudaStreamSynchronize(c0->stream));
     if (stats) { stats->loss_sum = loss; stats->kernel_launches = stats->train_launches; }
     return NE_OK;
+}
+
+int ne_check_pool(ne_ctx* c) {
+    NE_TRY(enter(c));
+    NE_TRY(check_loaded(c));
+    if (c->built_episode < 0) return fail(c, NE_ESTATE, "no sample pool built");
+    NE_CUDA(c, cudaMemsetAsync(c->d_bad, 0xFF, sizeof(unsigned long long), c->stream));
+    NE_CUDA(c, ne::launch_check_pool(c->d_pool, c->d_boff, c->boff.back(), c->d_sub_bounds, nb_local(c),
+                                     c->c_begin, c->c_begin + c->c_count, c->d_bad, c->dev, c->stream));
+    c->launches += 1;
+    unsigned long long bad = 0;
+    NE_CUDA(c, cudaMemcpyAsync(&bad, c->d_bad, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (bad == ~0ull) return NE_OK;
+    uint64_t rec = 0;
+    NE_CUDA(c, cudaMemcpy(&rec, c->d_pool + bad, sizeof rec, cudaMemcpyDeviceToHost));
+    const uint32_t b = (uint32_t)(std::upper_bound(c->boff.begin(), c->boff.end(), (uint64_t)bad) - c->boff.begin() - 1);
+    return fail(c, NE_ESCHED, "pool[%llu] = (%u, %u) outside block (vertex sub-part %u = [%llu, %llu), context part [%llu, %llu))",
+                bad, (uint32_t)rec, (uint32_t)(rec >> 32), b, (unsigned long long)c->sub_bounds[b],
+                (unsigned long long)c->sub_bounds[b + 1], (unsigned long long)c->c_begin,
+                (unsigned long long)(c->c_begin + c->c_count));
 }
 
 const char* ne_last_error(const ne_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }

@@ -23,6 +23,7 @@ _lib = C.CDLL(LIB_PATH)
 
 NE_OK, NE_EINVAL, NE_ERANGE, NE_ENOMEM, NE_ESTATE, NE_ECUDA, NE_ENCCL, NE_ESCHED = 0, -1, -2, -3, -4, -5, -6, -7
 NE_REUSE_SAMPLES = 1
+NE_CHECK_BLOCKS = 2
 NE_VERTEX, NE_CONTEXT = 0, 1
 NE_WB_ATOMIC_DELTA, NE_WB_STORE = 0, 1
 
@@ -63,6 +64,7 @@ _sig = {
     "ne_set_embeddings": (C.c_int, [_P, C.c_int, C.c_uint32, C.c_uint32, _P]),
     "ne_last_error": (C.c_char_p, [_P]),
     "ne_destroy": (None, [_P]),
+    "ne_check_pool": (C.c_int, [_P]),
     "ne_export_samples": (C.c_int, [_P, C.c_uint32, _P, C.c_size_t, C.POINTER(C.c_uint64)]),
     "ne_export_negatives": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, _P]),
     "ne_train_samples_local_ring": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
@@ -175,6 +177,10 @@ def ne_last_error(ctx) -> str:
 
 def ne_destroy(ctx) -> None:
     _lib.ne_destroy(ctx)
+
+
+def ne_check_pool(ctx) -> None:
+    _check(ctx, _lib.ne_check_pool(ctx))
 
 
 def ne_export_samples(ctx, vsub: int, out: np.ndarray | None = None) -> int:

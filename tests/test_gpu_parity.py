@@ -397,3 +397,22 @@ def test_hogwild_auc_gate_c1():
         aucs.append(oracle.auc(oracle.score_pairs(Vg, Cg, test), oracle.score_pairs(Vg, Cg, neg)))
         eng.close()
     assert all(abs(a - a_ref) <= 0.01 for a in aucs), (a_ref, aucs)
+
+
+@pytest.mark.parametrize("P", [1, 4])
+def test_pool_schedule_check(c1, P):
+    """ne_check_pool: every pooled sample lies in its 2D block."""
+    from paper_2005_13789_b200 import ne
+    off, tgt = c1
+    for g in range(P):
+        eng = engine(rank=g, world=P, deterministic=False)
+        eng.load_graph(off, tgt)
+        eng.random_walk(0, 0)
+        eng.build_samples(0, 0)
+        ne.ne_check_pool(eng.ctx)
+        eng.close()
+    eng = engine(deterministic=False)
+    eng.load_graph(off, tgt)
+    st = ne.ne_train_epoch(eng.ctx, 0, 0.025, ne.NE_CHECK_BLOCKS)
+    assert st.samples > 0
+    eng.close()
