@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--ref-episodes", type=int, default=1536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--episodes", type=int, default=0, help="episodes per epoch (0 = workload default)")
+    ap.add_argument("--subparts", type=int, default=4, help="vertex sub-parts per GPU (the paper's k, P:152)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -201,7 +202,8 @@ def main():
         nccl_id = obj[0]
     stream = torch.cuda.current_stream()
     eng = Engine(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
-                 walks_per_node=1, episodes=episodes, subparts=4, deterministic=False, seed=42, p=w.p, q=w.q,
+                 walks_per_node=1, episodes=episodes, subparts=args.subparts, deterministic=False, seed=42,
+                 p=w.p, q=w.q,
                  device=local, rank=rank, world=world, nccl_id=nccl_id, torch_allocator=True,
                  stream=stream.cuda_stream)
     eng.load_graph(off, tgt)
@@ -295,7 +297,7 @@ def main():
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": desc, "step": "one epoch: walk + augment + order/bucket + SGNS (+ ring)",
-                       "samples_per_step": samples_all / args.steps, "episodes": episodes, "subparts": 4,
+                       "samples_per_step": samples_all / args.steps, "episodes": episodes, "subparts": args.subparts,
                        "mode": "hogwild", "parallelism": f"2D ring x{world}",
                        "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * 4 / 1e9),
                        "graph_generator": "numpy Philox (host)" if w.m <= 200_000_000 else "torch CUDA generator"},
@@ -310,7 +312,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     # CSR validation flags + offsets ends (32 B), block offsets (5 x 8 B), loss (8 B)
-                    "d2h_bytes_per_step": 32 + episodes * (8 * (4 * world + 1) + 8)},
+                    "d2h_bytes_per_step": 32 + episodes * (8 * (args.subparts * world + 1) + 8)},
             "clocks": clk.summary(),
             "gpu_launches": int(tsum[3]),
         }

@@ -84,6 +84,9 @@ struct ne_ctx {
     uint32_t launches = 0;
     std::shared_ptr<void> alias_scratch;  // host buffers reused across ne_load_graph calls
     std::vector<uint2> alias_host;
+    std::vector<uint64_t> alias_deg;      // context-part degrees the alias builder reads
+    std::thread alias_thread;             // host alias build, overlapped with walk + pool build
+    bool alias_pending = false;
 };
 
 namespace {
@@ -159,6 +162,8 @@ int dalloc_t(ne_ctx* c, T** out, size_t count) {
 }
 
 void free_all(ne_ctx* c) {
+    if (c->alias_thread.joinable()) c->alias_thread.join();
+    c->alias_pending = false;
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
     for (auto& a : c->allocs) {
@@ -171,6 +176,10 @@ void free_all(ne_ctx* c) {
     c->loaded = false;
     c->walked_epoch = c->walked_episode = c->built_epoch = c->built_episode = -1;
 }
+
+// Join the host alias build started by ne_load_graph and upload its table
+// (once).  Everything that reads the alias table calls this first.
+int wait_alias(ne_ctx* c);
 
 cudaEvent_t next_event(ne_ctx* c) {
     if (c->ev_used == c->ev_pool.size()) {
@@ -279,6 +288,16 @@ void build_alias(const uint64_t* deg, size_t n, std::vector<uint2>& out, AliasSc
             }
         });
     for (auto& x : th) x.join();
+}
+
+int wait_alias(ne_ctx* c) {
+    if (!c->alias_pending) return NE_OK;
+    if (c->alias_thread.joinable()) c->alias_thread.join();
+    c->alias_pending = false;
+    NE_CUDA(c, cudaMemcpyAsync(c->d_alias, c->alias_host.data(), c->alias_host.size() * sizeof(uint2),
+                               cudaMemcpyHostToDevice, c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));  // alias_host is reused by the next load
+    return NE_OK;
 }
 
 uint64_t pairs_per_walk(uint32_t k, uint32_t l) {
@@ -428,6 +447,7 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
 // sent to rank+1 while slot t+1 trains, and the sub-part for round r+1 arrives
 // from rank-1 into the other half of the ping-pong buffers.
 int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st) {
+    NE_TRY(wait_alias(c));
     const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank;
     const uint64_t d = c->cfg.dim;
     if (P > 1 && !c->comm)
@@ -623,6 +643,8 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     if (n < (uint32_t)c->world) return fail(c, NE_ERANGE, "n=%u < world=%d", n, c->world);
     if (nnz >= (1ull << 40)) return fail(c, NE_ERANGE, "nnz=%llu too large", (unsigned long long)nnz);
     // A graph of the same shape reuses every device buffer (repeated loads, e2e).
+    if (c->alias_thread.joinable()) c->alias_thread.join();
+    c->alias_pending = false;
     const bool reuse = c->loaded && c->n == n && c->nnz == nnz;
     if (!reuse) free_all(c);
     c->loaded = false;
@@ -701,14 +723,17 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
         NE_CUDA(c, cudaStreamSynchronize(c->stream));
         deg_src = hoff.data();
     }
-    std::vector<uint64_t> deg(c->c_count);
-    for (uint64_t i = 0; i < c->c_count; ++i) deg[i] = deg_src[i + 1] - deg_src[i];
+    c->alias_deg.resize(c->c_count);
+    for (uint64_t i = 0; i < c->c_count; ++i) c->alias_deg[i] = deg_src[i + 1] - deg_src[i];
     if (!c->alias_scratch) c->alias_scratch = std::make_shared<AliasScratch>();
-    build_alias(deg.data(), deg.size(), c->alias_host, *static_cast<AliasScratch*>(c->alias_scratch.get()));
     NE_ALLOC(c->d_alias, std::max<uint64_t>(c->c_count, 1));
-    NE_CUDA(c, cudaMemcpyAsync(c->d_alias, c->alias_host.data(), c->alias_host.size() * sizeof(uint2),
-                               cudaMemcpyHostToDevice, c->stream));
-    NE_CUDA(c, cudaStreamSynchronize(c->stream));  // alias_host is reused by the next load
+    // The table is built on host threads while the GPU initialises, walks and
+    // builds the first pool; wait_alias joins it before the first SGNS launch.
+    c->alias_thread = std::thread([c] {
+        build_alias(c->alias_deg.data(), c->alias_deg.size(), c->alias_host,
+                    *static_cast<AliasScratch*>(c->alias_scratch.get()));
+    });
+    c->alias_pending = true;
 
     // Embeddings (O9): context part = 0; home vertex sub-parts initialised.
     NE_ALLOC(c->d_C, std::max<uint64_t>(c->c_count, 1) * g.dim);
@@ -897,6 +922,7 @@ int ne_export_negatives(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vs
     if (!out && count) return fail(c, NE_EINVAL, "null output");
     const uint64_t total = count * c->cfg.negatives;
     if (total == 0) return NE_OK;
+    NE_TRY(wait_alias(c));
     if (c->tmp_u32_cap < total) {
         NE_TRY(dalloc_t(c, &c->d_tmp_u32, total));
         c->tmp_u32_cap = total;
@@ -932,6 +958,7 @@ int ne_train_samples_local_ring(ne_ctx* const* ctxs, uint32_t world, uint32_t ep
         if (c->built_episode != (int64_t)episode)
             return fail(c0, NE_ESTATE, "context %u has no pool for episode %u", g, episode);
     }
+    for (uint32_t g = 0; g < world; ++g) NE_TRY(wait_alias(ctxs[g]));
     if (stats) std::memset(stats, 0, sizeof *stats);
     NE_CUDA(c0, cudaMemsetAsync(c0->d_loss, 0, sizeof(double), c0->stream));
     // Every rank's launches go to rank 0's stream, in plan order: round r, slot t,
