@@ -60,6 +60,9 @@ enum {
 /* ne_config.writeback */
 enum { NE_WB_ATOMIC_DELTA = 0, NE_WB_STORE = 1 };
 
+/* ne_config.update_rule */
+enum { NE_UPDATE_SEQUENTIAL = 0, NE_UPDATE_ACCUMULATED = 1 };
+
 /* ne_get_embeddings / ne_set_embeddings: which matrix. */
 enum { NE_VERTEX = 0, NE_CONTEXT = 1 };
 
@@ -101,6 +104,12 @@ typedef struct {
                                 P:355; rejection sampling as in KnightKing).
                                 p = q = 1 (or 0) = first-order DeepWalk walk.  Other
                                 values need every CSR row sorted by target.         */
+    uint32_t update_rule;    /* NE_UPDATE_SEQUENTIAL (0): the 1+K Train calls of Alg. 1
+                                in order, each seeing the updated vertex row (D2);
+                                NE_UPDATE_ACCUMULATED (1): word2vec / GraphVite style --
+                                all 1+K dots use the pre-sample vertex row, whose
+                                accumulated gradient is applied once (NEXT-4)       */
+    uint32_t reserved;       /* must be 0                                             */
     uint64_t seed;           /* Philox key (contract R1)                                */
 } ne_config;
 

@@ -47,7 +47,7 @@ class _Config(C.Structure):
     _fields_ = [("dim", C.c_uint32), ("negatives", C.c_uint32), ("walk_len", C.c_uint32),
                 ("window", C.c_uint32), ("walks_per_node", C.c_uint32), ("episodes", C.c_uint32),
                 ("subparts", C.c_uint32), ("parts", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
-                ("seed", C.c_uint64)]
+                ("update_rule", C.c_uint32), ("reserved", C.c_uint32), ("seed", C.c_uint64)]
 
 
 class _Stats(C.Structure):
@@ -68,10 +68,12 @@ class Config:
     seed: int = 42
     p: float = 1.0   # node2vec return parameter (NEXT-1); p = q = 1: first order
     q: float = 1.0   # node2vec in-out parameter
+    update_rule: int = 0  # 0 sequential (Alg. 1), 1 accumulated (word2vec, NEXT-4)
 
     def c(self) -> _Config:
         return _Config(self.dim, self.negatives, self.walk_len, self.window, self.walks_per_node,
-                       self.episodes, self.subparts, self.parts, self.p, self.q, self.seed)
+                       self.episodes, self.subparts, self.parts, self.p, self.q, self.update_rule, 0,
+                       self.seed)
 
 
 _lib = None
@@ -132,6 +134,11 @@ def lib():
     L.or_train_sample.argtypes = [_f32p, _f32p, C.c_uint32, C.c_uint32, C.c_uint32, _u32p,
                                   C.c_uint32, C.c_float]
     L.or_train_sample.restype = C.c_double
+    L.or_train_sample_accumulated.argtypes = [_f32p, _f32p, C.c_uint32, C.c_uint32, C.c_uint32, _u32p,
+                                              C.c_uint32, C.c_float]
+    L.or_train_sample_accumulated.restype = C.c_double
+    L.or_sgns_total_grad.argtypes = [_f64p, C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.c_int), C.c_uint32,
+                                     C.c_uint32, _f64p, C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.c_double)]
     L.or_plan_vsub.argtypes = [C.c_uint32] * 5
     L.or_plan_vsub.restype = C.c_uint32
     L.or_build_alias_tables.argtypes = [C.POINTER(_Config), C.c_uint64, _u64p, _u32p, _u32p]
@@ -335,6 +342,29 @@ def train_sample(V, Cm, src: int, dst: int, negs, lr: float) -> float:
 
 def plan_vsub(P: int, k: int, r: int, t: int, g: int) -> int:
     return int(lib().or_plan_vsub(P, k, r, t, g))
+
+
+def train_sample_accumulated(V, Cm, src: int, dst: int, negs, lr: float) -> float:
+    negs = np.ascontiguousarray(negs, np.uint32)
+    arg = negs if len(negs) else np.zeros(1, np.uint32)
+    return float(lib().or_train_sample_accumulated(V.reshape(-1), Cm.reshape(-1), V.shape[1], src, dst, arg,
+                                                   len(negs), lr))
+
+
+def sgns_total_grad(v, cs, labels):
+    """Gradient of the per-sample loss sum_j l(v.c_j, y_j): (dL/dv, [dL/dc_j], L)."""
+    v = np.ascontiguousarray(v, np.float64)
+    cs = [np.ascontiguousarray(c, np.float64) for c in cs]
+    m, d = len(cs), len(v)
+    gv = np.zeros(d)
+    gcs = [np.zeros(d) for _ in range(m)]
+    PD = C.POINTER(C.c_double)
+    cp = (PD * m)(*[c.ctypes.data_as(PD) for c in cs])
+    gp = (PD * m)(*[g.ctypes.data_as(PD) for g in gcs])
+    lab = (C.c_int * m)(*labels)
+    loss = C.c_double()
+    lib().or_sgns_total_grad(v, cp, lab, m, d, gv, gp, C.byref(loss))
+    return gv, gcs, float(loss.value)
 
 
 def train_epoch(cfg: Config, offsets, targets, V: np.ndarray, Cm: np.ndarray, epoch: int,

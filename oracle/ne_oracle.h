@@ -34,6 +34,8 @@ typedef struct {
     uint32_t subparts;       /* vertex sub-parts per part, k=4         */
     uint32_t parts;          /* P context/vertex parts (GPUs)   */
     float    p, q;           /* node2vec return / in-out parameters; 1, 1 (or 0) = first order */
+    uint32_t update_rule;    /* 0 sequential (Alg. 1, D2); 1 accumulated (word2vec, NEXT-4) */
+    uint32_t reserved;
     uint64_t seed;           /* Philox key                                      */
 } or_config;
 
@@ -92,6 +94,10 @@ void     or_sgns_grad(const double *v, const double *c, uint32_t d, int label,
 double   or_sgns_step(float *v, float *c, uint32_t d, int label, float lr);
 double   or_train_sample(float *V, float *C, uint32_t d, uint32_t src, uint32_t dst,
                          const uint32_t *negs, uint32_t K, float lr);
+void     or_sgns_total_grad(const double *v, const double *const *c, const int *labels, uint32_t m,
+                            uint32_t d, double *gv, double *const *gc, double *loss);
+double   or_train_sample_accumulated(float *V, float *C, uint32_t d, uint32_t src, uint32_t dst,
+                                     const uint32_t *negs, uint32_t K, float lr);
 uint32_t or_plan_vsub(uint32_t P, uint32_t k, uint32_t r, uint32_t t, uint32_t g);
 int      or_build_alias_tables(const or_config *cfg, uint64_t n, const uint64_t *offsets,
                                uint32_t *thr, uint32_t *alias);

@@ -88,6 +88,57 @@ double or_train_sample(float *V, float *C, uint32_t d, uint32_t src, uint32_t ds
     return loss;
 }
 
+/* NEXT-4 (word2vec / GraphVite update, cited P:313): gradient of the
+ * per-sample negative-sampling loss L = sum_j l(v . c_j, y_j) over the 1+K
+ * context rows: dL/dv = sum_j g_j c_j, dL/dc_j = g_j v, g_j = s(v.c_j) - y_j.
+ * (For distinct c_j.)  m = 1 + K rows, c[j] / gc[j] their pointers. */
+void or_sgns_total_grad(const double *v, const double *const *c, const int *labels, uint32_t m,
+                        uint32_t d, double *gv, double *const *gc, double *loss)
+{
+    uint32_t i, j;
+    double tot = 0.0;
+    for (i = 0; i < d; ++i) gv[i] = 0.0;
+    for (j = 0; j < m; ++j) {
+        double x = 0.0, s, g;
+        for (i = 0; i < d; ++i) x += v[i] * c[j][i];
+        s = or_sigmoid(x);
+        g = s - (double)labels[j];
+        for (i = 0; i < d; ++i) { gv[i] += g * c[j][i]; gc[j][i] = g * v[i]; }
+        tot += labels[j] ? -log(s) : -log(1.0 - s);
+    }
+    if (loss) *loss = tot;
+}
+
+/* NEXT-4: the accumulated-gradient update of one sample, in word2vec's order:
+ * for (c, y) in [(dst,1), (neg_0,0), ...]: x = v0 . c (v0 = the vertex row
+ * before the sample), g = s(x) - y, e += g c, c <- c - lr g v0 (in place, so a
+ * repeated context id sees its earlier update); then v <- v0 - lr e.  Without
+ * repeats this is one SGD step on L (or_sgns_total_grad).  fp64 arithmetic,
+ * fp32 storage rounded once per row update. */
+double or_train_sample_accumulated(float *V, float *C, uint32_t d, uint32_t src, uint32_t dst,
+                                   const uint32_t *negs, uint32_t K, float lr)
+{
+    double v0[d], e[d], eta = (double)lr, loss = 0.0;
+    float *v = V + (size_t)src * d;
+    uint32_t i, j;
+    for (i = 0; i < d; ++i) { v0[i] = (double)v[i]; e[i] = 0.0; }
+    for (j = 0; j <= K; ++j) {
+        float *c = C + (size_t)(j == 0 ? dst : negs[j - 1]) * d;
+        double x = 0.0, s, g;
+        for (i = 0; i < d; ++i) x += v0[i] * (double)c[i];
+        s = or_sigmoid(x);
+        g = s - (j == 0 ? 1.0 : 0.0);
+        loss += j == 0 ? -log(s) : -log(1.0 - s);
+        for (i = 0; i < d; ++i) {
+            const double ci = (double)c[i];
+            e[i] += g * ci;
+            c[i] = (float)(ci - eta * g * v0[i]);
+        }
+    }
+    for (i = 0; i < d; ++i) v[i] = (float)(v0[i] - eta * e[i]);
+    return loss;
+}
+
 /* Alias tables of every context part (O3), part-local ids, stored at the
  * global row index of each part's first row. */
 int or_build_alias_tables(const or_config *cfg, uint64_t n, const uint64_t *offsets,
@@ -138,6 +189,7 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
         cfg->episodes == 0 || cfg->episodes > 4096 || epoch >= (1u << 24))
         return -1;
     if (cfg->walk_len > 0 && (cfg->window == 0 || cfg->walks_per_node == 0)) return -1;
+    if (cfg->update_rule > 1) return -1;
     or_partition_bounds(0, n, P, bounds);
     boff = (uint64_t *)malloc((nblocks + 1) * sizeof(uint64_t));
     if (!boff) return -1;
@@ -162,7 +214,9 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
                         const uint32_t *pr = pairs + 2 * (boff[B] + p);
                         double loss;
                         if (K > 0) or_negatives(cfg, thr + cb, alias + cb, cb, cn, epoch, e, B, p, negs);
-                        loss = or_train_sample(V, C, d, pr[0], pr[1], negs, K, lr);
+                        loss = cfg->update_rule == 1
+                                   ? or_train_sample_accumulated(V, C, d, pr[0], pr[1], negs, K, lr)
+                                   : or_train_sample(V, C, d, pr[0], pr[1], negs, K, lr);
                         if (stats) { stats->samples += 1; stats->loss_sum += loss; }
                     }
                 }

@@ -44,7 +44,10 @@ constexpr int kSgnsThreads = 256;
 // in deterministic mode too.
 // p.deterministic: only group 0 of the (single) warp works, one sample at a
 // time in canonical order -- the same arithmetic as the production mapping.
-template <int G, int R, int KT, int MINB, bool ADD, bool PF>
+// ACC: NEXT-4 accumulated-gradient rule (all 1+K dots against the pre-sample
+// vertex row, which is updated once at the end): the 1+K group reductions are
+// independent, so they overlap instead of forming one dependency chain.
+template <int G, int R, int KT, int MINB, bool ADD, bool PF, bool ACC = false>
 __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) {
     constexpr int S = 32 / G;
     constexpr int KM = KT > 0 ? KT : kMaxK;
@@ -91,13 +94,14 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
         const bool dup = __any_sync(0xFFFFFFFFu, __popc(__match_any_sync(0xFFFFFFFFu, mkey)) > 1);
 
         float4* vrow = reinterpret_cast<float4*>(p.V + (uint64_t)(prA.x - p.v_begin) * p.d);
-        float4 v[R], v0[ADD ? R : 1];
+        float4 v[R], v0[(ADD || ACC) ? R : 1], eacc[ACC ? R : 1];
         float4 c[KM + 1][R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t e = sub + G * r;
             v[r] = (act && e < q) ? vrow[e] : make_float4(0.f, 0.f, 0.f, 0.f);
-            if constexpr (ADD) v0[r] = v[r];
+            if constexpr (ADD || ACC) v0[r] = v[r];
+            if constexpr (ACC) eacc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int j = 0; j <= KM; ++j) {
@@ -149,8 +153,14 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
                         if (i <= K && ids[i] == ids[j]) last = false;
                 }
                 float4 vo[R];
-                float lt;
-                const float a = sgns_step<G, R>(v, c[j], vo, p.lr, j == 0, lt);
+                float lt, a;
+                if constexpr (ACC) {
+                    a = sgns_step_acc<G, R>(v0, c[j], eacc, p.lr, j == 0, lt);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) vo[r] = v0[r];
+                } else {
+                    a = sgns_step<G, R>(v, c[j], vo, p.lr, j == 0, lt);
+                }
                 if (sub == 0 && act) loss += (double)lt;
                 float4* crow = reinterpret_cast<float4*>(p.C + (uint64_t)(ids[j] - p.c_begin) * p.d);
 #pragma unroll
@@ -168,6 +178,8 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t e = sub + G * r;
+            if constexpr (ACC)
+                v[r] = make_float4(v0[r].x - eacc[r].x, v0[r].y - eacc[r].y, v0[r].z - eacc[r].z, v0[r].w - eacc[r].w);
             if (act && e < q) {
                 if constexpr (ADD)
                     atomicAdd(vrow + e, make_float4(v[r].x - v0[r].x, v[r].y - v0[r].y,
@@ -195,12 +207,16 @@ template <int G, int R, int KT, int MINB>
 static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStream_t s) {
     static const bool pf = env_int("NE_SGNS_PF", 0) != 0;  // developer knob: L2 row prefetch (measured: no gain)
     if (p.deterministic) {  // one warp, one sample at a time, canonical order, plain stores
-        if (pf) sgns_kernel<G, R, KT, MINB, false, true><<<1, 32, 0, s>>>(p);
+        if (p.accumulate) sgns_kernel<G, R, KT, MINB, false, false, true><<<1, 32, 0, s>>>(p);
+        else if (pf) sgns_kernel<G, R, KT, MINB, false, true><<<1, 32, 0, s>>>(p);
         else sgns_kernel<G, R, KT, MINB, false, false><<<1, 32, 0, s>>>(p);
         return cudaGetLastError();
     }
-    auto kern = p.atomic_writeback ? (pf ? sgns_kernel<G, R, KT, MINB, true, true> : sgns_kernel<G, R, KT, MINB, true, false>)
-                                   : (pf ? sgns_kernel<G, R, KT, MINB, false, true> : sgns_kernel<G, R, KT, MINB, false, false>);
+    auto kern = p.accumulate
+                    ? (p.atomic_writeback ? sgns_kernel<G, R, KT, MINB, true, false, true>
+                                          : sgns_kernel<G, R, KT, MINB, false, false, true>)
+                : p.atomic_writeback ? (pf ? sgns_kernel<G, R, KT, MINB, true, true> : sgns_kernel<G, R, KT, MINB, true, false>)
+                                     : (pf ? sgns_kernel<G, R, KT, MINB, false, true> : sgns_kernel<G, R, KT, MINB, false, false>);
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSgnsThreads, 0);
     if (e != cudaSuccess) return e;
@@ -227,7 +243,7 @@ static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStr
     return cudaGetLastError();
 }
 
-// Occupancy variant (developer knob NE_SGNS_MINB = 1..4): the register budget
+// Occupancy variant (developer knob NE_SGNS_MINB = 2..3): the register budget
 // __launch_bounds__(256, MINB) gives the compiler.  Defaults: 16-lane groups
 // carry two samples' rows per lane (MINB 2); 32-lane groups MINB 3.
 
@@ -241,12 +257,9 @@ static cudaError_t launch_sgns_k(const SgnsParams& p, const Device& dev, cudaStr
     // (d <= 256) hold 2 float4 per row: both need the 128-register budget of 2 CTAs
     int minb = knob >= 1 && knob <= 4 ? knob : (G == 16 || R == 2 ? 2 : 3);
     if (KT == 0) minb = std::min(minb, 2);  // runtime K keeps kMaxK+1 rows live: stay spill-free
-    switch (minb) {
-        case 1: return launch_sgns_v<G, R, KT, 1>(p, dev, s);
-        case 2: return launch_sgns_v<G, R, KT, 2>(p, dev, s);
-        case 4: return launch_sgns_v<G, R, KT, 4>(p, dev, s);
-        default: return launch_sgns_v<G, R, KT, 3>(p, dev, s);
-    }
+    // (the knob's other budgets were measured and dropped: 1 and 4 CTAs/SM lose)
+    if (minb <= 2) return launch_sgns_v<G, R, KT, 2>(p, dev, s);
+    return launch_sgns_v<G, R, KT, 3>(p, dev, s);
 }
 
 template <int G, int R>
@@ -262,7 +275,7 @@ cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s) 
     // copies (kernels_sgns_tma.cu); measured slower than the register kernel
     // with L2 prefetch (smem caps it at 12 warps/SM), so it is off by default
     static const int tma = env_int("NE_SGNS_TMA", 0);
-    if (tma) {
+    if (tma && !p.accumulate) {
         const cudaError_t e = launch_sgns_tma(p, dev, s);
         if (e != cudaErrorNotSupported) return e;
         cudaGetLastError();

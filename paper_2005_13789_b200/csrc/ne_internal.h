@@ -87,6 +87,7 @@ struct SgnsParams {
     uint64_t max_warps;         // Hogwild concurrency cap (>= 1)
     int atomic_writeback;       // Hogwild: red.add row deltas instead of storing rows
     int reserve_sms;            // SMs left free for the concurrent NCCL ring kernels
+    int accumulate;             // NEXT-4 accumulated-gradient update (word2vec order)
 };
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s);
 cudaError_t launch_sgns_tma(const SgnsParams& p, const Device& dev, cudaStream_t s);  // kernels_sgns_tma.cu

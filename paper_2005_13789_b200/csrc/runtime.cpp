@@ -432,6 +432,7 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
     const double cap = eps / (kk / cr + 1.0 / vr);
     p.max_warps = cap >= 1e15 ? ~0ull : std::max<uint64_t>(1, (uint64_t)cap);
     p.atomic_writeback = c->cfg.writeback == NE_WB_ATOMIC_DELTA ? 1 : 0;
+    p.accumulate = (int)c->cfg.update_rule;
     // with a ring, leave SMs to NCCL's send/recv kernels so the transfer of the
     // previous sub-part overlaps this block (developer knob NE_RING_RESERVE_SMS)
     static const int reserve = [] {
@@ -567,6 +568,9 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     if (g.episodes == 0 || g.episodes > 4095)
         return bad(fail(c, NE_EINVAL, "episodes=%u not in [1, 4095]", g.episodes));
     if (g.writeback > NE_WB_STORE) return bad(fail(c, NE_EINVAL, "writeback=%u not in {0, 1}", g.writeback));
+    if (g.update_rule > NE_UPDATE_ACCUMULATED)
+        return bad(fail(c, NE_EINVAL, "update_rule=%u not in {0, 1}", g.update_rule));
+    if (g.reserved != 0) return bad(fail(c, NE_EINVAL, "reserved field must be 0"));
     if (!(g.p >= 0.f) || !(g.q >= 0.f))
         return bad(fail(c, NE_EINVAL, "node2vec p=%g q=%g must be > 0 (0 = 1)", g.p, g.q));
     {

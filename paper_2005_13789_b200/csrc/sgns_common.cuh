@@ -80,6 +80,35 @@ __device__ __forceinline__ float sgns_step(float4 (&v)[R], float4 (&c)[R], float
     return a;
 }
 
+// NEXT-4 accumulated update of one pair (word2vec order): x = v0 . c with the
+// pre-sample vertex row v0, a = lr (s - y); e += a c (the vertex row's
+// accumulated step, applied once by the caller: v = v0 - e); c <- c - a v0.
+template <int G, int R>
+__device__ __forceinline__ float sgns_step_acc(const float4 (&v0)[R], float4 (&c)[R], float4 (&e)[R], float lr,
+                                               bool positive, float& loss) {
+    float part = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        part = fmaf(v0[r].x, c[r].x, part);
+        part = fmaf(v0[r].y, c[r].y, part);
+        part = fmaf(v0[r].z, c[r].z, part);
+        part = fmaf(v0[r].w, c[r].w, part);
+    }
+    const float x = fminf(fmaxf(group_sum<G>(part), -30.f), 30.f);
+    const float ex = __expf(-x);
+    const float s = __fdividef(1.f, 1.f + ex);
+    const float a = lr * (s - (positive ? 1.f : 0.f));
+    loss = __logf(1.f + ex) + (positive ? 0.f : x);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const float4 co = c[r];
+        e[r] = make_float4(fmaf(a, co.x, e[r].x), fmaf(a, co.y, e[r].y), fmaf(a, co.z, e[r].z), fmaf(a, co.w, e[r].w));
+        c[r] = make_float4(fmaf(-a, v0[r].x, co.x), fmaf(-a, v0[r].y, co.y),
+                           fmaf(-a, v0[r].z, co.z), fmaf(-a, v0[r].w, co.w));
+    }
+    return a;
+}
+
 __device__ __forceinline__ float4 scaled(float a, const float4& x) {
     return make_float4(a * x.x, a * x.y, a * x.z, a * x.w);
 }

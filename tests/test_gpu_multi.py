@@ -16,14 +16,16 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("mode", ["det", "hogwild"])
-def test_nccl_ring(world, mode):
+@pytest.mark.parametrize("world,mode,kind", [
+    (2, "det", "deepwalk"), (2, "hogwild", "deepwalk"), (4, "det", "deepwalk"), (4, "hogwild", "deepwalk"),
+    (2, "det", "node2vec"), (2, "det", "line"), (4, "det", "line"),
+])
+def test_nccl_ring(world, mode, kind):
     if _ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={29600 + world}",
-           os.path.join(ROOT, "tools", "multi_parity.py"), mode]
+           os.path.join(ROOT, "tools", "multi_parity.py"), mode, kind]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MULTI" in r.stdout

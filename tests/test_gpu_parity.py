@@ -416,3 +416,32 @@ def test_pool_schedule_check(c1, P):
     st = ne.ne_train_epoch(eng.ctx, 0, 0.025, ne.NE_CHECK_BLOCKS)
     assert st.samples > 0
     eng.close()
+
+
+# ---------------------------------------------------------------- NEXT-4 accumulated update
+def test_accumulated_rule_deterministic_epoch_c1():
+    off, tgt = synth.workload_graph("c1")
+    dv, dc = _det_epoch(off, tgt, update_rule=1)
+    assert dv <= TOL and dc <= TOL, (dv, dc)
+
+
+def test_accumulated_rule_hogwild_auc():
+    n = 2000
+    u, v = synth.planted_partition_edges(n, 20, 12.0, 1.0, 17)
+    off, tgt, test = synth.split_edges(n, u, v, 0.1, 7)
+    neg = synth.negative_pairs(n, u, v, len(test), 8)
+    kw = dict(dim=32, walk_len=20, window=3, walks_per_node=4, subparts=1, update_rule=1)
+    cfg = ocfg(**kw)
+    V = oracle.init_vertex(n, 32, 42)
+    Cm = np.zeros_like(V)
+    for ep in range(2):
+        oracle.train_epoch(cfg, off, tgt, V, Cm, ep, 0.05)
+    a_ref = oracle.auc(oracle.score_pairs(V, Cm, test), oracle.score_pairs(V, Cm, neg))
+    eng = engine(deterministic=False, **kw)
+    eng.load_graph(off, tgt)
+    for ep in range(2):
+        eng.train_epoch(ep, 0.05)
+    Vg, Cg = eng.embeddings(0), eng.embeddings(1)
+    a = oracle.auc(oracle.score_pairs(Vg, Cg, test), oracle.score_pairs(Vg, Cg, neg))
+    eng.close()
+    assert abs(a - a_ref) <= 0.01, (a_ref, a)

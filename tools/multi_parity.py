@@ -18,6 +18,8 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     mode = sys.argv[1] if len(sys.argv) > 1 else "det"
+    kind = sys.argv[2] if len(sys.argv) > 2 else "deepwalk"
+    extra = {"deepwalk": {}, "node2vec": dict(p=0.5, q=2.0), "line": dict(walk_len=0, window=0)}[kind]
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     obj = [ne.ne_get_nccl_id() if rank == 0 else None]
@@ -25,7 +27,7 @@ def main():
     off, tgt = synth.workload_graph("c1")
     n = len(off) - 1
     eng = Engine(dim=128, deterministic=(mode == "det"), device=local, rank=rank, world=world,
-                 nccl_id=obj[0], episodes=2)
+                 nccl_id=obj[0], episodes=2, **extra)
     eng.load_graph(off, tgt)
     stats = [eng.train_epoch(ep, 0.025) for ep in range(2)]
     a, b = eng.part
@@ -33,8 +35,10 @@ def main():
     parts = [None] * world
     dist.all_gather_object(parts, (a, b, V, Cm, stats))
     if rank == 0:
-        cfg = oracle.Config(dim=128, negatives=5, walk_len=40, window=5, walks_per_node=1, episodes=2,
-                            subparts=4, parts=world, seed=42)
+        base = dict(dim=128, negatives=5, walk_len=40, window=5, walks_per_node=1, episodes=2,
+                    subparts=4, parts=world, seed=42)
+        base.update(extra)
+        cfg = oracle.Config(**base)
         Vr = oracle.init_vertex(n, 128, 42)
         Cr = np.zeros_like(Vr)
         ns = 0
@@ -44,7 +48,7 @@ def main():
         assert got_ns == ns, (got_ns, ns)
         dv = max(np.abs(p[2] - Vr[p[0]:p[1]]).max() for p in parts)
         dc = max(np.abs(p[3] - Cr[p[0]:p[1]]).max() for p in parts)
-        print(f"MULTI {mode} world={world} samples={ns} max|dV|={dv:.3e} max|dC|={dc:.3e}", flush=True)
+        print(f"MULTI {mode} {kind} world={world} samples={ns} max|dV|={dv:.3e} max|dC|={dc:.3e}", flush=True)
         if mode == "det":
             assert dv <= 1e-4 and dc <= 1e-4, (dv, dc)
         else:
