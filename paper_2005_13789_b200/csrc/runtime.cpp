@@ -81,6 +81,11 @@ struct ne_ctx {
 
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
+    // recorded on the comm stream after the last ring transfers of a call (the
+    // "return home" sends, still in flight when ne_train_samples returns); the
+    // next call's first training of every slot waits on it
+    cudaEvent_t ring_done = nullptr;
+    bool ring_pending = false;
     uint32_t launches = 0;
     std::shared_ptr<void> alias_scratch;  // host buffers reused across ne_load_graph calls
     std::vector<uint2> alias_host;
@@ -435,9 +440,9 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
     p.accumulate = (int)c->cfg.update_rule;
     // with a ring, leave SMs to NCCL's send/recv kernels so the transfer of the
     // previous sub-part overlaps this block (developer knob NE_RING_RESERVE_SMS)
-    static const int reserve = [] {
+    static const int reserve = [] {  // measured: 0, 2, 4 SMs perform alike (C4, 4 GPUs)
         const char* e = std::getenv("NE_RING_RESERVE_SMS");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 0;
     }();
     p.reserve_sms = (c->world > 1 && c->comm) ? reserve : 0;
     return p;
@@ -455,6 +460,7 @@ int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st
         return fail(c, NE_ESTATE, "world=%u context has no NCCL communicator (layout-only)", P);
     NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
     std::vector<cudaEvent_t> recv(k, nullptr);
+    if (c->ring_pending) recv.assign(k, c->ring_done);  // home-coming sub-parts of the last call
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, waits;
     uint64_t samples = 0;
     for (uint32_t r = 0; r < P; ++r) {
@@ -493,14 +499,15 @@ int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st
         }
         if (P > 1) c->cur = 1 - c->cur;
     }
-    if (P > 1) {  // the sub-parts are home again; the compute stream waits for them
-        for (uint32_t t = 0; t < k; ++t) {
-            cudaEvent_t w0 = next_event(c), w1 = next_event(c);
-            NE_CUDA(c, cudaEventRecord(w0, c->stream));
-            NE_CUDA(c, cudaStreamWaitEvent(c->stream, recv[t], 0));
-            NE_CUDA(c, cudaEventRecord(w1, c->stream));
-            waits.push_back({w0, w1});
-        }
+    // The sub-parts are on their way home.  The receives are not awaited here:
+    // the next call's first training of each slot waits for them (the next
+    // episode's walk and pool build overlap the transfers); every reader of the
+    // vertex slots (get/set embeddings, reload, destroy) drains the comm stream.
+    c->ring_pending = false;
+    if (P > 1) {
+        if (!c->ring_done) NE_CUDA(c, cudaEventCreateWithFlags(&c->ring_done, cudaEventDisableTiming));
+        NE_CUDA(c, cudaEventRecord(c->ring_done, c->comm_stream));
+        c->ring_pending = true;
     }
     double loss = 0.0;
     NE_CUDA(c, cudaMemcpyAsync(&loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -647,6 +654,8 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     if (n < (uint32_t)c->world) return fail(c, NE_ERANGE, "n=%u < world=%d", n, c->world);
     if (nnz >= (1ull << 40)) return fail(c, NE_ERANGE, "nnz=%llu too large", (unsigned long long)nnz);
     // A graph of the same shape reuses every device buffer (repeated loads, e2e).
+    NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));  // ring transfers into the vertex slots
+    c->ring_pending = false;
     if (c->alias_thread.joinable()) c->alias_thread.join();
     c->alias_pending = false;
     const bool reuse = c->loaded && c->n == n && c->nnz == nnz;
@@ -1016,6 +1025,7 @@ void ne_destroy(ne_ctx* c) {
     cudaSetDevice(c->device);
     free_all(c);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->ring_done) cudaEventDestroy(c->ring_done);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->d_loss) cudaFree(c->d_loss);
     if (c->d_bad) cudaFree(c->d_bad);
