@@ -63,6 +63,9 @@ enum { NE_WB_ATOMIC_DELTA = 0, NE_WB_STORE = 1 };
 /* ne_config.update_rule */
 enum { NE_UPDATE_SEQUENTIAL = 0, NE_UPDATE_ACCUMULATED = 1 };
 
+/* ne_config.staging */
+enum { NE_STAGE_DEVICE = 0, NE_STAGE_HOST = 1 };
+
 /* ne_get_embeddings / ne_set_embeddings: which matrix. */
 enum { NE_VERTEX = 0, NE_CONTEXT = 1 };
 
@@ -109,7 +112,12 @@ typedef struct {
                                 NE_UPDATE_ACCUMULATED (1): word2vec / GraphVite style --
                                 all 1+K dots use the pre-sample vertex row, whose
                                 accumulated gradient is applied once (NEXT-4)       */
-    uint32_t reserved;       /* must be 0                                             */
+    uint32_t staging;        /* NE_STAGE_DEVICE (0): the vertex matrix lives in HBM;
+                                NE_STAGE_HOST (1): in pinned host memory, streamed
+                                through 3 device sub-part slots -- H2D of sub-part t+1
+                                and D2H of t-1 overlap the training of t (the paper's
+                                pipeline stages 5 and 2; NEXT-2).
+                                Single rank only (world == 1).                         */
     uint64_t seed;           /* Philox key (contract R1)                                */
 } ne_config;
 

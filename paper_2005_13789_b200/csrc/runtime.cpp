@@ -51,7 +51,12 @@ struct ne_ctx {
     uint2* d_alias = nullptr;
     float* d_C = nullptr;
     uint64_t c_begin = 0, c_count = 0;
-    std::vector<float*> vslot;  // 2k buffers
+    std::vector<float*> vslot;  // ring: 2k buffers (ping-pong); one GPU: k; host staging: 3
+    float* h_V = nullptr;       // host staging: this rank's vertex rows, pinned
+    size_t h_V_bytes = 0;
+    cudaStream_t copy_stream = nullptr;  // host staging H2D (D2H uses comm_stream)
+    cudaEvent_t stage_done = nullptr;    // last D2H of a call (deferred like ring_done)
+    bool stage_pending = false;
     int cur = 0;                // half [cur*k, cur*k+k) holds the current sub-parts
     uint64_t max_sub_rows = 0;
 
@@ -171,6 +176,8 @@ void free_all(ne_ctx* c) {
     c->alias_pending = false;
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    c->stage_pending = false;
     for (auto& a : c->allocs) {
         if (c->free_fn) c->free_fn(a.p, a.bytes, c->device, (void*)c->stream, c->user);
         else cudaFree(a.p);
@@ -452,8 +459,69 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
 // (vsub = ((rank - r) mod P)*k + t, context part rank); the trained sub-part is
 // sent to rank+1 while slot t+1 trains, and the sub-part for round r+1 arrives
 // from rank-1 into the other half of the ping-pong buffers.
+// NEXT-2 host staging (P:142 stages 2 and 5), one GPU: sub-part t trains in
+// slot t mod 3 while sub-part t+1 is copied in (copy stream) and t-1 copied
+// back (comm stream); a slot is refilled only after its previous D2H.
+int do_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st) {
+    const uint32_t k = c->cfg.subparts, S = (uint32_t)c->vslot.size();
+    const uint64_t d = c->cfg.dim, pb = c->part_bounds[c->rank];
+    NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
+    std::vector<cudaEvent_t> loaded(k), stored(k);
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
+    auto h2d = [&](uint32_t t) -> int {
+        if (t >= S) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, stored[t - S], 0));
+        else if (c->stage_pending) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->stage_done, 0));
+        const uint64_t sb = c->sub_bounds[t], rows = c->sub_bounds[t + 1] - sb;
+        NE_CUDA(c, cudaMemcpyAsync(c->vslot[t % S], c->h_V + (sb - pb) * d, rows * d * sizeof(float),
+                                   cudaMemcpyHostToDevice, c->copy_stream));
+        loaded[t] = next_event(c);
+        NE_CUDA(c, cudaEventRecord(loaded[t], c->copy_stream));
+        return NE_OK;
+    };
+    uint64_t samples = 0;
+    if (k) NE_TRY(h2d(0));
+    for (uint32_t t = 0; t < k; ++t) {
+        if (t + 1 < k) NE_TRY(h2d(t + 1));
+        NE_CUDA(c, cudaStreamWaitEvent(c->stream, loaded[t], 0));
+        const ne::SgnsParams sp = sgns_params(c, t, c->vslot[t % S], epoch, episode, lr);
+        cudaEvent_t e0 = next_event(c), e1 = next_event(c);
+        NE_CUDA(c, cudaEventRecord(e0, c->stream));
+        NE_CUDA(c, ne::launch_sgns(sp, c->dev, c->stream));
+        NE_CUDA(c, cudaEventRecord(e1, c->stream));
+        if (sp.count) { c->launches += 1; if (st) st->train_launches += 1; }
+        timed.push_back({e0, e1});
+        samples += sp.count;
+        const uint64_t sb = c->sub_bounds[t], rows = c->sub_bounds[t + 1] - sb;
+        NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, e1, 0));
+        NE_CUDA(c, cudaMemcpyAsync(c->h_V + (sb - pb) * d, c->vslot[t % S], rows * d * sizeof(float),
+                                   cudaMemcpyDeviceToHost, c->comm_stream));
+        stored[t] = next_event(c);
+        NE_CUDA(c, cudaEventRecord(stored[t], c->comm_stream));
+    }
+    // the last copies back stay in flight; the next call's first H2D and every
+    // host-side reader wait for them
+    if (!c->stage_done) NE_CUDA(c, cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
+    NE_CUDA(c, cudaEventRecord(c->stage_done, c->comm_stream));
+    c->stage_pending = true;
+    double loss = 0.0;
+    NE_CUDA(c, cudaMemcpyAsync(&loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (st) {
+        st->samples += samples;
+        st->loss_sum += loss;
+        for (auto& pr : timed) {
+            float ms = 0.f;
+            NE_CUDA(c, cudaEventElapsedTime(&ms, pr.first, pr.second));
+            st->ms_train += ms;
+        }
+    }
+    c->ev_used = 0;
+    return NE_OK;
+}
+
 int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st) {
     NE_TRY(wait_alias(c));
+    if (c->cfg.staging == NE_STAGE_HOST) return do_train_staged(c, epoch, episode, lr, st);
     const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank;
     const uint64_t d = c->cfg.dim;
     if (P > 1 && !c->comm)
@@ -577,7 +645,7 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     if (g.writeback > NE_WB_STORE) return bad(fail(c, NE_EINVAL, "writeback=%u not in {0, 1}", g.writeback));
     if (g.update_rule > NE_UPDATE_ACCUMULATED)
         return bad(fail(c, NE_EINVAL, "update_rule=%u not in {0, 1}", g.update_rule));
-    if (g.reserved != 0) return bad(fail(c, NE_EINVAL, "reserved field must be 0"));
+    if (g.staging > NE_STAGE_HOST) return bad(fail(c, NE_EINVAL, "staging=%u not in {0, 1}", g.staging));
     if (!(g.p >= 0.f) || !(g.q >= 0.f))
         return bad(fail(c, NE_EINVAL, "node2vec p=%g q=%g must be > 0 (0 = 1)", g.p, g.q));
     {
@@ -607,6 +675,7 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&c->d_loss, sizeof(double)) != cudaSuccess ||
         cudaMalloc(&c->d_bad, 3 * sizeof(unsigned long long)) != cudaSuccess)
         return bad(fail(c, NE_ECUDA, "stream/scratch setup failed on device %d", device));
@@ -633,6 +702,8 @@ int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
     NE_TRY(enter(c));
     if (c->loaded) return fail(c, NE_ESTATE, "ne_init_dist must precede ne_load_graph");
     if (world < 1 || rank < 0 || rank >= world) return fail(c, NE_EINVAL, "rank=%d world=%d", rank, world);
+    if (world > 1 && c->cfg.staging == NE_STAGE_HOST)
+        return fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", world);
     if ((uint64_t)world * c->cfg.subparts > 256 || (uint64_t)world * world * c->cfg.subparts > 4096)
         return fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
     if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
@@ -655,7 +726,9 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     if (nnz >= (1ull << 40)) return fail(c, NE_ERANGE, "nnz=%llu too large", (unsigned long long)nnz);
     // A graph of the same shape reuses every device buffer (repeated loads, e2e).
     NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));  // ring transfers into the vertex slots
+    NE_CUDA(c, cudaStreamSynchronize(c->copy_stream));
     c->ring_pending = false;
+    c->stage_pending = false;
     if (c->alias_thread.joinable()) c->alias_thread.join();
     c->alias_pending = false;
     const bool reuse = c->loaded && c->n == n && c->nnz == nnz;
@@ -751,14 +824,38 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     // Embeddings (O9): context part = 0; home vertex sub-parts initialised.
     NE_ALLOC(c->d_C, std::max<uint64_t>(c->c_count, 1) * g.dim);
     NE_CUDA(c, cudaMemsetAsync(c->d_C, 0, c->c_count * g.dim * sizeof(float), c->stream));
-    if (!reuse) c->vslot.assign(2 * (size_t)k, nullptr);
+    // vertex sub-part slots: the ring needs 2k (ping-pong), one GPU k, host staging 3
+    const bool staged = g.staging == NE_STAGE_HOST;
+    if (staged && c->world > 1)
+        return fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", c->world);
+    const size_t nslots = staged ? std::min<size_t>(3, k) : (c->world > 1 ? 2 * (size_t)k : k);
+    if (!reuse) c->vslot.assign(nslots, nullptr);
     for (size_t i = 0; i < c->vslot.size(); ++i) NE_ALLOC(c->vslot[i], std::max<uint64_t>(c->max_sub_rows, 1) * g.dim);
     c->cur = 0;
+    if (staged) {
+        const size_t bytes = (c->part_bounds[c->rank + 1] - c->part_bounds[c->rank]) * g.dim * sizeof(float);
+        if (c->h_V_bytes != bytes) {
+            if (c->h_V) cudaFreeHost(c->h_V);
+            c->h_V = nullptr;
+            c->h_V_bytes = 0;
+            cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_V), std::max<size_t>(bytes, 16), cudaHostAllocDefault);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return fail(c, NE_ENOMEM, "cudaHostAlloc(%zu) for the host-staged vertex matrix: %s", bytes,
+                            cudaGetErrorString(e));
+            }
+            c->h_V_bytes = bytes;
+        }
+    }
     for (uint32_t t = 0; t < k; ++t) {
         const size_t vs = (size_t)c->rank * k + t;
-        NE_CUDA(c, ne::launch_init_vertex(c->vslot[t], c->sub_bounds[vs], c->sub_bounds[vs + 1] - c->sub_bounds[vs],
-                                          g.dim, g.seed, c->dev, c->stream));
+        const uint64_t rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
+        float* slot = staged ? c->vslot[t % c->vslot.size()] : c->vslot[t];
+        NE_CUDA(c, ne::launch_init_vertex(slot, c->sub_bounds[vs], rows, g.dim, g.seed, c->dev, c->stream));
         c->launches += 1;
+        if (staged)  // stream order: the slot is reused only after its copy to the host
+            NE_CUDA(c, cudaMemcpyAsync(c->h_V + (c->sub_bounds[vs] - c->part_bounds[c->rank]) * g.dim, slot,
+                                       rows * g.dim * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     }
 
     // Episode buffers: walks, pi-indexed slots, pool, bucketing scratch.
@@ -893,6 +990,11 @@ static int rows_op(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, f
         return NE_OK;
     };
     if (which == NE_CONTEXT) return copy(c->d_C, c->c_begin, row_begin, row_end);
+    if (c->cfg.staging == NE_STAGE_HOST) {
+        NE_CUDA(c, cudaStreamSynchronize(c->copy_stream));
+        c->stage_pending = false;
+        return copy(c->h_V + (uint64_t)(row_begin - pb) * d, row_begin, row_begin, row_end);
+    }
     const uint32_t k = c->cfg.subparts;
     for (uint32_t t = 0; t < k; ++t) {
         const size_t vs = (size_t)c->rank * k + t;
@@ -1026,6 +1128,9 @@ void ne_destroy(ne_ctx* c) {
     free_all(c);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->ring_done) cudaEventDestroy(c->ring_done);
+    if (c->stage_done) cudaEventDestroy(c->stage_done);
+    if (c->h_V) cudaFreeHost(c->h_V);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->d_loss) cudaFree(c->d_loss);
     if (c->d_bad) cudaFree(c->d_bad);

@@ -12,10 +12,11 @@ class Engine:
     def __init__(self, dim=128, negatives=5, walk_len=40, window=5, walks_per_node=1, episodes=1,
                  subparts=4, deterministic=False, seed=42, device=0, rank=0, world=1,
                  nccl_id=None, torch_allocator=False, stream=None, conflict_permille=0,
-                 writeback=ne.NE_WB_ATOMIC_DELTA, p=1.0, q=1.0, update_rule=ne.NE_UPDATE_SEQUENTIAL):
+                 writeback=ne.NE_WB_ATOMIC_DELTA, p=1.0, q=1.0, update_rule=ne.NE_UPDATE_SEQUENTIAL,
+                 staging=ne.NE_STAGE_DEVICE):
         self.cfg = ne.ne_config(dim, negatives, walk_len, window, walks_per_node, episodes, subparts,
-                                int(bool(deterministic)), conflict_permille, writeback, p, q, update_rule, 0,
-                                seed)
+                                int(bool(deterministic)), conflict_permille, writeback, p, q, update_rule,
+                                staging, seed)
         self._alloc = ne.torch_allocator() if torch_allocator else (None, None)
         self.ctx = ne.ne_create(self.cfg, device, *self._alloc)
         self.rank, self.world = rank, world

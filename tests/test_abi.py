@@ -69,3 +69,5 @@ def test_create_validates_update_rule():
     from paper_2005_13789_b200 import ne
     with pytest.raises(ne.NEError, match="NE_EINVAL: update_rule=2"):
         ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 2, 0, 42), 0)
+    with pytest.raises(ne.NEError, match="NE_EINVAL: staging=3"):
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 3, 42), 0)

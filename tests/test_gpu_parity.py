@@ -125,7 +125,7 @@ def test_negatives_bit_exact(c1, P):
 # ---------------------------------------------------------------- O10/O11 training
 def _det_epoch(off, tgt, epochs=1, lr=0.025, **kw):
     n = len(off) - 1
-    cfg = ocfg(**{k: v for k, v in kw.items() if k not in ("deterministic", "conflict_permille", "writeback")})
+    cfg = ocfg(**{k: v for k, v in kw.items() if k not in ("deterministic", "conflict_permille", "writeback", "staging")})
     eng = engine(**kw)
     eng.load_graph(off, tgt)
     V = oracle.init_vertex(n, cfg.dim, 42)
@@ -445,3 +445,30 @@ def test_accumulated_rule_hogwild_auc():
     a = oracle.auc(oracle.score_pairs(Vg, Cg, test), oracle.score_pairs(Vg, Cg, neg))
     eng.close()
     assert abs(a - a_ref) <= 0.01, (a_ref, a)
+
+
+# ---------------------------------------------------------------- NEXT-2 host staging
+@pytest.mark.parametrize("subparts", [2, 7])
+def test_host_staged_vertex_matrix_matches_oracle(subparts):
+    """NE_STAGE_HOST: the vertex matrix lives in pinned host memory and streams
+    through 3 device slots (P:142 stages 2, 5); results equal the in-HBM path."""
+    off, tgt = synth.rmat_graph(3000, 20000, 41)
+    dv, dc = _det_epoch(off, tgt, epochs=2, dim=64, walk_len=12, window=3, subparts=subparts,
+                        episodes=2, staging=1)
+    assert dv <= TOL and dc <= TOL, (dv, dc)
+
+
+def test_host_staged_set_get_and_hogwild():
+    off, tgt = synth.rmat_graph(3000, 20000, 42)
+    eng = engine(dim=32, walk_len=10, window=2, subparts=8, staging=1, deterministic=False)
+    eng.load_graph(off, tgt)
+    V = eng.embeddings(0)
+    assert np.array_equal(V, oracle.init_vertex(3000, 32, 42))
+    mark = np.full((5, 32), 0.25, np.float32)
+    eng.set_embeddings(0, 100, mark)
+    assert np.array_equal(eng.embeddings(0, rows=(100, 105)), mark)
+    st = eng.train_epoch(0, 0.025)
+    assert st["samples"] > 0 and np.isfinite(st["loss_sum"])
+    V2 = eng.embeddings(0)
+    assert np.isfinite(V2).all() and not np.array_equal(V2, V)
+    eng.close()
