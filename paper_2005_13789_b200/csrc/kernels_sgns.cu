@@ -249,15 +249,21 @@ static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStr
 
 template <int G, int R, int KT>
 static cudaError_t launch_sgns_k(const SgnsParams& p, const Device& dev, cudaStream_t s) {
-    if constexpr (R > 2) {  // wide rows (d > 256): the register file holds 2+K rows of up to 2 KB
+    if constexpr (R > 2 && G == 32) {  // wide rows (d > 256): the register file holds 2+K rows of up to 2 KB
         return launch_sgns_v<G, R, KT, 1>(p, dev, s);
     }
     static const int knob = env_int("NE_SGNS_MINB", 0);
     // 16-lane groups hold two samples' rows per lane, 32-lane groups with R = 2
     // (d <= 256) hold 2 float4 per row: both need the 128-register budget of 2 CTAs
-    int minb = knob >= 1 && knob <= 4 ? knob : (G == 16 || R == 2 ? 2 : 3);
+    // defaults (measured): 8-lane groups 1 CTA/SM (974 vs 841 M/s at 2 with spills,
+    // C4); 16-lane groups and 32-lane R = 2 need 128 registers (2 CTAs); else 3
+    int minb = knob >= 1 && knob <= 4 ? knob : (G == 8 ? 1 : (G == 16 || R == 2 ? 2 : 3));
     if (KT == 0) minb = std::min(minb, 2);  // runtime K keeps kMaxK+1 rows live: stay spill-free
-    // (the knob's other budgets were measured and dropped: 1 and 4 CTAs/SM lose)
+    // (the knob's other budgets were measured and dropped: 1 and 4 CTAs/SM lose,
+    // except for 8-lane groups, whose 3 float4 per row fit 1 CTA/SM spill-free)
+    if constexpr (G == 8) {
+        if (minb <= 1) return launch_sgns_v<G, R, KT, 1>(p, dev, s);
+    }
     if (minb <= 2) return launch_sgns_v<G, R, KT, 2>(p, dev, s);
     return launch_sgns_v<G, R, KT, 3>(p, dev, s);
 }
@@ -284,6 +290,10 @@ cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s) 
     // d <= 128: 16 lanes x 2 float4 (two samples per warp; developer knob
     // NE_SGNS_LANES=32 selects one sample per warp); d > 128: 32 lanes x R.
     static const int lanes = env_int("NE_SGNS_LANES", 16);
+    // 64 < d <= 96 at K = 5: 8-lane groups x 3 float4, four samples per warp, so
+    // a 384-byte row uses every lane (16-lane groups leave a quarter idle)
+    if (q > 16 && q <= 24 && p.K == 5 && lanes != 32 && env_int("NE_SGNS_G8", 1))
+        return launch_sgns_k<8, 3, 5>(p, dev, s);
     if (q <= 32 && lanes == 16) {
         if (q <= 16) return launch_sgns_r<16, 1>(p, dev, s);
         return launch_sgns_r<16, 2>(p, dev, s);

@@ -162,6 +162,8 @@ def test_hogwild_code_path_single_warp_c1(writeback):
     dict(dim=96, negatives=8, walk_len=12, window=4, subparts=3, episodes=2),
     dict(dim=256, negatives=2, walk_len=8, window=8, walks_per_node=3),
     dict(dim=100, negatives=5, walk_len=0, window=0, episodes=2),
+    dict(dim=96, negatives=5, walk_len=10, window=3),              # 8-lane groups (C4's d)
+    dict(dim=80, negatives=5, walk_len=10, window=3, subparts=2),  # 8 lanes, ragged last float4
 ])
 def test_deterministic_shapes(kw):
     off, tgt = synth.rmat_graph(700, 4000, 3)
