@@ -455,10 +455,6 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
     return p;
 }
 
-// O7 ring (P:152, P:190-191): round r, slot t trains block
-// (vsub = ((rank - r) mod P)*k + t, context part rank); the trained sub-part is
-// sent to rank+1 while slot t+1 trains, and the sub-part for round r+1 arrives
-// from rank-1 into the other half of the ping-pong buffers.
 // NEXT-2 host staging (P:142 stages 2 and 5), one GPU: sub-part t trains in
 // slot t mod 3 while sub-part t+1 is copied in (copy stream) and t-1 copied
 // back (comm stream); a slot is refilled only after its previous D2H.
@@ -519,6 +515,10 @@ int do_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_st
     return NE_OK;
 }
 
+// O7 ring (P:152, P:190-191): round r, slot t trains block
+// (vsub = ((rank - r) mod P)*k + t, context part rank); the trained sub-part is
+// sent to rank+1 while slot t+1 trains, and the sub-part for round r+1 arrives
+// from rank-1 into the other half of the ping-pong buffers.
 int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st) {
     NE_TRY(wait_alias(c));
     if (c->cfg.staging == NE_STAGE_HOST) return do_train_staged(c, epoch, episode, lr, st);
