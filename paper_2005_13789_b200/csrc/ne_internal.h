@@ -51,21 +51,42 @@ size_t scan_scratch_bytes(uint64_t M);
 cudaError_t launch_scan(const uint32_t* in, uint64_t M, uint64_t* out, uint64_t* total, void* scratch,
                         cudaStream_t s, uint32_t* launches);
 // O5 + O6: the kept pairs of unit u get part-local indices base[u] + rank
-// (generation order) and land at slots[pi(x)], pi the Feistel bijection over
-// [0, p.N): a dense array, no holes.
+// (generation order); pair x belongs at position y = pi(x) of [0, p.N), pi the
+// Feistel bijection.  Where it is stored is the sink's choice:
+//  * direct (key == nullptr): out[y] = pair -- a dense pi-indexed array, one
+//    random 8-byte store per pair.  Measured on C3 (522 M pairs): ~24 ms, a
+//    random store over a multi-GB target per pair (TLB reach is 256 MB);
+//  * keyed (default): out[x] = pair, key[x] = y in generation order (coalesced);
+//    launch_order then moves the pairs to their positions with radix passes.
+struct PoolSink {
+    uint64_t* out;
+    uint32_t* key;       // keyed mode (needs N <= 2^32)
+};
 cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
-                              const uint64_t* base, uint64_t* slots, const Device& dev, cudaStream_t s);
+                              const uint64_t* base, const PoolSink& sink, const Device& dev, cudaStream_t s);
 cudaError_t launch_pairs_line(const uint64_t* off, const uint32_t* tgt, uint64_t n,
-                              const PoolParams& p, const uint64_t* base, uint64_t* slots,
+                              const PoolParams& p, const uint64_t* base, const PoolSink& sink,
                               const Device& dev, cudaStream_t s);
 // first pool position outside its 2D block -> *bad (atomicMin; init ~0).
 cudaError_t launch_check_pool(const uint64_t* pool, const uint64_t* boff, uint64_t total,
                               const uint64_t* sub_bounds, uint32_t nb, uint64_t c_begin, uint64_t c_end,
                               unsigned long long* bad, const Device& dev, cudaStream_t s);
-// Stable partition of the slots by vertex sub-part (bounds over nb+1 entries,
-// device pointer): pool[block_offsets[b] ...] in slot order.
+// Keyed sink -> window layout: 1-2 radix passes over the 32-bit keys above
+// the low kPoolWinBits (pi is a bijection, so the region of every key prefix
+// is known: prefix << shift).  Buffers ping-pong: (pairs0, keys0) hold the
+// sink's output, (pairs1, keys1) are the same size; on return *win_pairs /
+// *win_pos (u16 = y mod 2^kPoolWinBits, aliasing a key buffer) are the window
+// layout and *spare the pair buffer launch_bucket may write the pool to.
+constexpr uint32_t kPoolWinBits = 13;
+cudaError_t launch_order(uint64_t N, uint64_t* pairs0, uint32_t* keys0, uint64_t* pairs1, uint32_t* keys1,
+                         uint32_t* cursors, const uint64_t** win_pairs, const uint16_t** win_pos, uint64_t** spare,
+                         const Device& dev, cudaStream_t s, uint32_t* launches);
+// Stable partition of the pairs by vertex sub-part (bounds over nb+1 entries,
+// device pointer): pool[block_offsets[b] ...] in pi order.  pos == nullptr:
+// `slots` is the dense pi-indexed array; else the window layout.
+// scratch >= bucket_scratch_bytes(N, nb); its head doubles as radix cursors.
 size_t bucket_scratch_bytes(uint64_t N, uint32_t nb);
-cudaError_t launch_bucket(const uint64_t* slots, uint64_t N, const uint64_t* sub_bounds,
+cudaError_t launch_bucket(const uint64_t* slots, const uint16_t* pos, uint64_t N, const uint64_t* sub_bounds,
                           uint32_t nb, void* scratch, uint64_t* pool, uint64_t* block_offsets,
                           const Device& dev, cudaStream_t s, uint32_t* launches);
 

@@ -65,7 +65,9 @@ struct ne_ctx {
     uint32_t* d_walks = nullptr;
     uint32_t* d_slot_tab = nullptr;
     uint64_t* d_slots = nullptr;
+    uint32_t* d_keys[2] = {nullptr, nullptr};  // keyed pool sink + radix ping-pong (nullptr: direct sink)
     uint64_t* d_pool = nullptr;
+    uint64_t* pool_at = nullptr;  // the buffer (d_pool or d_slots) holding the built pool
     void* d_scratch = nullptr;
     uint32_t* d_counts = nullptr;   // per-unit kept-pair counts (O5)
     uint64_t* d_base = nullptr;     // their exclusive scan: part-local index bases
@@ -185,6 +187,8 @@ void free_all(ne_ctx* c) {
     c->allocs.clear();
     c->d_tmp_u32 = nullptr;
     c->tmp_u32_cap = 0;
+    c->d_keys[0] = c->d_keys[1] = nullptr;
+    c->pool_at = nullptr;
     c->loaded = false;
     c->walked_epoch = c->walked_episode = c->built_epoch = c->built_episode = -1;
 }
@@ -397,17 +401,32 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     }
     if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > capacity %llu", (unsigned long long)N,
                                   (unsigned long long)c->N_max);
-    // O6: every kept pair to slots[pi(x)] (dense [0, N)), then stable bucketing
+    // O6: every kept pair to its position pi(x), then stable bucketing by sub-part
     p.N = N;
+    const bool keyed = c->d_keys[0] && N > 0 && N <= (1ull << 32);
     if (N) {
+        ne::PoolSink sink{c->d_slots, keyed ? c->d_keys[0] : nullptr};
         if (c->cfg.walk_len > 0)
-            NE_CUDA(c, ne::launch_pairs_walk(c->d_walks, c->d_slot_tab, p, c->d_base, c->d_slots, c->dev, c->stream));
+            NE_CUDA(c, ne::launch_pairs_walk(c->d_walks, c->d_slot_tab, p, c->d_base, sink, c->dev, c->stream));
         else
-            NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_base, c->d_slots, c->dev, c->stream));
+            NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_base, sink, c->dev, c->stream));
         c->launches += 1;
     }
-    NE_CUDA(c, ne::launch_bucket(c->d_slots, N, c->d_sub_bounds, nb_local(c), c->d_scratch,
-                                 c->d_pool, c->d_boff, c->dev, c->stream, &c->launches));
+    c->pool_at = c->d_pool;
+    if (keyed) {  // radix passes to the window layout (cursors: head of the bucketing scratch)
+        const uint64_t* win_pairs = nullptr;
+        const uint16_t* win_pos = nullptr;
+        uint64_t* spare = nullptr;
+        NE_CUDA(c, ne::launch_order(N, c->d_slots, c->d_keys[0], c->d_pool, c->d_keys[1],
+                                    static_cast<uint32_t*>(c->d_scratch), &win_pairs, &win_pos, &spare, c->dev,
+                                    c->stream, &c->launches));
+        c->pool_at = spare;
+        NE_CUDA(c, ne::launch_bucket(win_pairs, win_pos, N, c->d_sub_bounds, nb_local(c), c->d_scratch,
+                                     c->pool_at, c->d_boff, c->dev, c->stream, &c->launches));
+    } else {
+        NE_CUDA(c, ne::launch_bucket(c->d_slots, nullptr, N, c->d_sub_bounds, nb_local(c), c->d_scratch,
+                                     c->pool_at, c->d_boff, c->dev, c->stream, &c->launches));
+    }
     c->boff.assign(nb_local(c) + 1, 0);
     NE_CUDA(c, cudaMemcpyAsync(c->boff.data(), c->d_boff, c->boff.size() * sizeof(uint64_t),
                                cudaMemcpyDeviceToHost, c->stream));
@@ -420,7 +439,7 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
 ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t epoch,
                            uint32_t episode, float lr) {
     ne::SgnsParams p{};
-    p.pool = reinterpret_cast<const uint2*>(c->d_pool + c->boff[vsub]);
+    p.pool = reinterpret_cast<const uint2*>(c->pool_at + c->boff[vsub]);
     p.count = c->boff[vsub + 1] - c->boff[vsub];
     p.V = V;
     p.v_begin = c->sub_bounds[vsub];
@@ -882,6 +901,29 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     NE_ALLOC(c->d_pool, std::max<uint64_t>(c->N_max, 1));
     if (!reuse) NE_TRY(dalloc(c, &c->d_scratch, ne::bucket_scratch_bytes(c->N_max, nb_local(c))));
     NE_ALLOC(c->d_boff, (size_t)nb_local(c) + 1);
+    // Keyed pool sink: two u32 key buffers (8 bytes per slot), allocated last
+    // and only if they fit (HBM left after everything above); otherwise the
+    // direct sink builds the same pool.  NE_POOL_DIRECT=1 forces the direct
+    // sink (tests, A/B).
+    if (!reuse) {
+        const char* e = std::getenv("NE_POOL_DIRECT");
+        c->d_keys[0] = c->d_keys[1] = nullptr;
+        const size_t bytes = std::max<uint64_t>(c->N_max, 1) * sizeof(uint32_t);
+        size_t free_b = 0, total_b = 0;
+        const bool room = c->alloc || (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+                                       free_b >= 2 * bytes + (1ull << 30));  // keep 1 GiB for the caller
+        if (room && !(e && std::atoi(e) != 0)) {
+            void* k0 = nullptr;
+            void* k1 = nullptr;
+            const std::string saved = c->err;
+            if (dalloc(c, &k0, bytes) == NE_OK && dalloc(c, &k1, bytes) == NE_OK) {
+                c->d_keys[0] = static_cast<uint32_t*>(k0);
+                c->d_keys[1] = static_cast<uint32_t*>(k1);
+            } else {
+                c->err = saved;  // not an error: the direct sink (k0, if any, stays unused until free_all)
+            }
+        }
+    }
 #undef NE_ALLOC
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
     c->loaded = true;
@@ -1025,7 +1067,7 @@ int ne_export_samples(ne_ctx* c, uint32_t vsub, uint32_t* pairs_out, size_t cap_
     if (count) *count = cnt;
     if (!pairs_out) return NE_OK;
     if (cap_pairs < cnt) return fail(c, NE_ERANGE, "capacity %zu < %llu pairs", cap_pairs, (unsigned long long)cnt);
-    if (cnt) NE_CUDA(c, cudaMemcpy(pairs_out, c->d_pool + c->boff[vsub], cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (cnt) NE_CUDA(c, cudaMemcpy(pairs_out, c->pool_at + c->boff[vsub], cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     return NE_OK;
 }
 
@@ -1104,7 +1146,7 @@ int ne_check_pool(ne_ctx* c) {
     NE_TRY(check_loaded(c));
     if (c->built_episode < 0) return fail(c, NE_ESTATE, "no sample pool built");
     NE_CUDA(c, cudaMemsetAsync(c->d_bad, 0xFF, sizeof(unsigned long long), c->stream));
-    NE_CUDA(c, ne::launch_check_pool(c->d_pool, c->d_boff, c->boff.back(), c->d_sub_bounds, nb_local(c),
+    NE_CUDA(c, ne::launch_check_pool(c->pool_at, c->d_boff, c->boff.back(), c->d_sub_bounds, nb_local(c),
                                      c->c_begin, c->c_begin + c->c_count, c->d_bad, c->dev, c->stream));
     c->launches += 1;
     unsigned long long bad = 0;
@@ -1112,7 +1154,7 @@ int ne_check_pool(ne_ctx* c) {
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
     if (bad == ~0ull) return NE_OK;
     uint64_t rec = 0;
-    NE_CUDA(c, cudaMemcpy(&rec, c->d_pool + bad, sizeof rec, cudaMemcpyDeviceToHost));
+    NE_CUDA(c, cudaMemcpy(&rec, c->pool_at + bad, sizeof rec, cudaMemcpyDeviceToHost));
     const uint32_t b = (uint32_t)(std::upper_bound(c->boff.begin(), c->boff.end(), (uint64_t)bad) - c->boff.begin() - 1);
     return fail(c, NE_ESCHED, "pool[%llu] = (%u, %u) outside block (vertex sub-part %u = [%llu, %llu), context part [%llu, %llu))",
                 bad, (uint32_t)rec, (uint32_t)(rec >> 32), b, (unsigned long long)c->sub_bounds[b],

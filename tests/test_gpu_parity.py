@@ -85,6 +85,38 @@ def test_pool_bit_exact_c1(c1, P):
         eng.close()
 
 
+@pytest.mark.parametrize("sink", ["keyed", "direct"])
+@pytest.mark.parametrize("kind", ["walk", "line"])
+def test_pool_sinks_bit_exact(c1, sink, kind, monkeypatch):
+    """Both pool paths (keyed + radix passes, the default; direct pi-indexed
+    scatter, used when HBM is short) against the oracle: C1 at P = 1 and 4 (one
+    radix pass, hundreds of 8192-position windows, a ragged last one), C1 with
+    4 walks per node (N ~ 5.6 M > 2^22: two radix passes) and a small graph whose
+    pool is a single partial window."""
+    if sink == "direct":
+        monkeypatch.setenv("NE_POOL_DIRECT", "1")
+    else:
+        monkeypatch.delenv("NE_POOL_DIRECT", raising=False)
+    small = synth.csr_from_undirected(60, *synth.planted_partition_edges(60, 3, 4.0, 1.0, 3))
+    kw = dict(walk_len=0, window=0) if kind == "line" else {}
+    cases = [(c1, 1, 1), (c1, 4, 1), (small, 1, 1)] + ([(c1, 1, 4)] if kind == "walk" else [])
+    for (off, tgt), P, wpn in cases:
+        k = 3
+        ref, boff = oracle.build_episode(ocfg(parts=P, subparts=k, walks_per_node=wpn, **kw), off, tgt, 4, 0)
+        for g in range(P):
+            eng = engine(rank=g, world=P, subparts=k, walks_per_node=wpn, **kw)
+            eng.load_graph(off, tgt)
+            if not kw:
+                eng.random_walk(4, 0)
+            total = eng.build_samples(4, 0)
+            if P == 1:
+                assert total == int(boff[-1])
+            for vs in range(P * k):
+                B = vs * P + g
+                assert np.array_equal(eng.export_samples(vs), ref[int(boff[B]):int(boff[B + 1])]), (P, g, vs, wpn)
+            eng.close()
+
+
 def test_pool_bit_exact_multi_episode_line(c1):
     off, tgt = c1
     for kw in (dict(episodes=3, walks_per_node=2, subparts=2), dict(walk_len=0, window=0, episodes=2)):
@@ -283,6 +315,25 @@ def test_c2_full_size_sampled():
     V = eng.embeddings(0)
     assert np.isfinite(V).all()
     eng.close()
+
+
+def test_pool_keyed_equals_direct_c2(monkeypatch):
+    """Full-size C2 pool (N ~ 10^8 > 2^22: two radix passes, ~13 000 windows):
+    the keyed path equals the direct pi-indexed scatter block by block (both
+    are pinned to the oracle on C1 by test_pool_sinks_bit_exact)."""
+    off, tgt = synth.workload_graph("c2")
+    pools = []
+    for direct in ("0", "1"):
+        monkeypatch.setenv("NE_POOL_DIRECT", direct)
+        eng = engine(deterministic=False)
+        eng.load_graph(off, tgt)
+        eng.random_walk(3, 0)
+        total = eng.build_samples(3, 0)
+        assert total > (1 << 22)
+        pools.append([eng.export_samples(vs) for vs in range(4)])
+        eng.close()
+    for a, b in zip(*pools):
+        assert np.array_equal(a, b)
 
 
 # ---------------------------------------------------------------- P-rank ring on one GPU
