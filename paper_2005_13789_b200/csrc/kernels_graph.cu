@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) walk_kernel(const uint64_t* __restrict__ 
                                                    const uint32_t* __restrict__ tgt, uint64_t n,
                                                    uint64_t omega0, uint64_t count, uint32_t k,
                                                    uint64_t seed, uint32_t epoch, ulonglong4 thr,
-                                                   uint32_t* __restrict__ walks) {
+                                                   uint32_t* __restrict__ walks, WalkCount wc) {
     const uint2 key = key_of(seed);
     const uint32_t tw = tag_word(kTagWalk, epoch);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256) walk_kernel(const uint64_t* __restrict__ 
         uint64_t cur = omega % n, prev = 0;
         uint32_t* out = walks + w * (uint64_t)(k + 1);
         out[0] = (uint32_t)cur;
-        uint32_t t = 1;
+        uint32_t t = 1, kept = 0;
         for (; t <= k; ++t) {
             const uint64_t b = __ldg(off + cur), e = __ldg(off + cur + 1);
             if (e == b) break;
@@ -117,22 +117,26 @@ __global__ void __launch_bounds__(256) walk_kernel(const uint64_t* __restrict__ 
             prev = cur;
             cur = cand;
             out[t] = (uint32_t)cur;
+            // O5: node t is the context of the min(t, l) window slots (t - delta, t)
+            if (cur >= wc.c_begin && cur < wc.c_end) kept += min(t, wc.l);
         }
         for (; t <= k; ++t) out[t] = kSentinel;
+        if (wc.counts) wc.counts[w] = kept;
     }
 }
 
 cudaError_t launch_walk(const uint64_t* off, const uint32_t* tgt, uint64_t n, uint64_t omega0,
                         uint64_t count, uint32_t k, uint64_t seed, uint32_t epoch,
-                        const uint64_t* n2v_thr, uint32_t* walks, const Device& dev, cudaStream_t s) {
+                        const uint64_t* n2v_thr, uint32_t* walks, const WalkCount& wc, const Device& dev,
+                        cudaStream_t s) {
     if (count == 0) return cudaSuccess;
     if (n2v_thr) {
         const ulonglong4 thr = make_ulonglong4(n2v_thr[0], n2v_thr[1], n2v_thr[2], 0);
         walk_kernel<true><<<grid_for(count, 256, dev), 256, 0, s>>>(off, tgt, n, omega0, count, k, seed,
-                                                                     epoch, thr, walks);
+                                                                     epoch, thr, walks, wc);
     } else {
         walk_kernel<false><<<grid_for(count, 256, dev), 256, 0, s>>>(off, tgt, n, omega0, count, k, seed,
-                                                                      epoch, make_ulonglong4(0, 0, 0, 0), walks);
+                                                                      epoch, make_ulonglong4(0, 0, 0, 0), walks, wc);
     }
     return cudaGetLastError();
 }

@@ -25,10 +25,18 @@ cudaError_t launch_init_vertex(float* V, uint64_t row_begin, uint64_t rows, uint
                                uint64_t seed, const Device& dev, cudaStream_t s);
 // O4: walkers [omega0, omega0 + count) -> walks[count][k+1].  node2vec
 // (NEXT-1) when n2v_thr != nullptr: thresholds (return, neighbour, farther),
-// each <= 2^32, of the rejection step.
+// each <= 2^32, of the rejection step.  With wc.counts != nullptr the kernel
+// also writes the O5 count of every walker (its window pairs whose context
+// node lies in [c_begin, c_end)) -- what count_walk would compute from the walk.
+struct WalkCount {
+    uint32_t* counts;
+    uint32_t l;
+    uint64_t c_begin, c_end;
+};
 cudaError_t launch_walk(const uint64_t* off, const uint32_t* tgt, uint64_t n, uint64_t omega0,
                         uint64_t count, uint32_t k, uint64_t seed, uint32_t epoch,
-                        const uint64_t* n2v_thr, uint32_t* walks, const Device& dev, cudaStream_t s);
+                        const uint64_t* n2v_thr, uint32_t* walks, const WalkCount& wc, const Device& dev,
+                        cudaStream_t s);
 
 // ---- sample pool (kernels_samples.cu) ---------------------------------------
 struct PoolParams {

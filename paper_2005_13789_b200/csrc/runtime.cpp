@@ -68,6 +68,7 @@ struct ne_ctx {
     uint32_t* d_keys[2] = {nullptr, nullptr};  // keyed pool sink + radix ping-pong (nullptr: direct sink)
     uint64_t* d_pool = nullptr;
     uint64_t* pool_at = nullptr;  // the buffer (d_pool or d_slots) holding the built pool
+    bool walk_counts = false;     // d_counts holds the O5 counts of the current walk (unsharded walk)
     void* d_scratch = nullptr;
     uint32_t* d_counts = nullptr;   // per-unit kept-pair counts (O5)
     uint64_t* d_base = nullptr;     // their exclusive scan: part-local index bases
@@ -355,15 +356,18 @@ int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         const uint64_t mine = std::min<uint64_t>(units, mine_b + chunk) - mine_b;
         NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0 + mine_b, mine, c->cfg.walk_len,
                                    c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr,
-                                   c->d_walks + mine_b * row, c->dev, c->stream));
+                                   c->d_walks + mine_b * row, ne::WalkCount{}, c->dev, c->stream));
         if (mine) c->launches += 1;
+        c->walk_counts = false;  // other ranks' walkers: counted by the pool build
         NE_NCCL(c, ncclAllGather(c->d_walks + (uint64_t)c->rank * chunk * row, c->d_walks, chunk * row,
                                  ncclUint32, c->comm, c->stream));
     } else {
         NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0, units, c->cfg.walk_len,
-                                   c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr, c->d_walks, c->dev,
-                                   c->stream));
+                                   c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr, c->d_walks,
+                                   ne::WalkCount{c->d_counts, c->cfg.window, c->c_begin, c->c_begin + c->c_count},
+                                   c->dev, c->stream));
         if (units) c->launches += 1;
+        c->walk_counts = true;  // O5 counts of this walk are in d_counts
     }
     c->walked_epoch = epoch;
     c->walked_episode = episode;
@@ -389,11 +393,13 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     // O5: kept pairs per unit, exclusive scan -> part-local index bases, N_g
     uint64_t N = 0;
     if (units) {
-        if (c->cfg.walk_len > 0)
-            NE_CUDA(c, ne::launch_count_walk(c->d_walks, c->d_slot_tab, p, c->d_counts, c->dev, c->stream));
-        else
+        if (c->cfg.walk_len == 0) {
             NE_CUDA(c, ne::launch_count_line(c->d_tgt, p, c->d_counts, c->dev, c->stream));
-        c->launches += 1;
+            c->launches += 1;
+        } else if (!c->walk_counts) {
+            NE_CUDA(c, ne::launch_count_walk(c->d_walks, c->d_slot_tab, p, c->d_counts, c->dev, c->stream));
+            c->launches += 1;
+        }
         NE_CUDA(c, ne::launch_scan(c->d_counts, units, c->d_base, c->d_total, c->d_scan_scratch, c->stream,
                                    &c->launches));
         NE_CUDA(c, cudaMemcpyAsync(&N, c->d_total, sizeof N, cudaMemcpyDeviceToHost, c->stream));
