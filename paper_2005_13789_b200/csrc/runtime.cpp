@@ -69,6 +69,7 @@ struct ne_ctx {
     uint64_t* d_pool = nullptr;
     uint64_t* pool_at = nullptr;  // the buffer (d_pool or d_slots) holding the built pool
     bool walk_counts = false;     // d_counts holds the O5 counts of the current walk (unsharded walk)
+    uint64_t pool_cap = 0;        // pairs d_slots / d_pool (and d_keys) hold; grown by ensure_pool
     void* d_scratch = nullptr;
     uint32_t* d_counts = nullptr;   // per-unit kept-pair counts (O5)
     uint64_t* d_base = nullptr;     // their exclusive scan: part-local index bases
@@ -174,6 +175,16 @@ int dalloc_t(ne_ctx* c, T** out, size_t count) {
     return NE_OK;
 }
 
+void dfree(ne_ctx* c, void* p) {
+    for (size_t i = 0; i < c->allocs.size(); ++i)
+        if (c->allocs[i].p == p) {
+            if (c->free_fn) c->free_fn(p, c->allocs[i].bytes, c->device, (void*)c->stream, c->user);
+            else cudaFree(p);
+            c->allocs.erase(c->allocs.begin() + (long)i);
+            return;
+        }
+}
+
 void free_all(ne_ctx* c) {
     if (c->alias_thread.joinable()) c->alias_thread.join();
     c->alias_pending = false;
@@ -189,7 +200,8 @@ void free_all(ne_ctx* c) {
     c->d_tmp_u32 = nullptr;
     c->tmp_u32_cap = 0;
     c->d_keys[0] = c->d_keys[1] = nullptr;
-    c->pool_at = nullptr;
+    c->d_slots = c->d_pool = c->pool_at = nullptr;
+    c->pool_cap = 0;
     c->loaded = false;
     c->walked_epoch = c->walked_episode = c->built_epoch = c->built_episode = -1;
 }
@@ -376,6 +388,40 @@ int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     return NE_OK;
 }
 
+// Episode pool buffers, sized by the episode's actual pool N (grow-only, 1/8
+// headroom; the bound N_max -- every walk full length, every pair kept -- is
+// 3-4x the real pool on power-law graphs).  The key buffers of the keyed path
+// are optional: if they do not fit, the direct path builds the same pool.
+int ensure_pool(ne_ctx* c, uint64_t N) {
+    if (N <= c->pool_cap && c->d_slots) return NE_OK;
+    for (void* p : {(void*)c->d_slots, (void*)c->d_pool, (void*)c->d_keys[0], (void*)c->d_keys[1]})
+        if (p) dfree(c, p);
+    c->d_slots = c->d_pool = c->pool_at = nullptr;
+    c->d_keys[0] = c->d_keys[1] = nullptr;
+    c->pool_cap = 0;
+    c->built_epoch = c->built_episode = -1;
+    const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(std::max<uint64_t>(c->N_max, 1), N + N / 8));
+    NE_TRY(dalloc_t(c, &c->d_slots, cap));
+    NE_TRY(dalloc_t(c, &c->d_pool, cap));
+    c->pool_cap = cap;
+    const char* e = std::getenv("NE_POOL_DIRECT");  // 1: force the direct path (tests, A/B)
+    if (e && std::atoi(e) != 0) return NE_OK;
+    const size_t bytes = cap * sizeof(uint32_t);
+    size_t free_b = 0, total_b = 0;
+    if (!c->alloc && !(cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b >= 2 * bytes + (1ull << 30)))
+        return NE_OK;  // keep 1 GiB for the caller
+    const std::string saved = c->err;
+    uint32_t *k0 = nullptr, *k1 = nullptr;
+    if (dalloc_t(c, &k0, cap) == NE_OK && dalloc_t(c, &k1, cap) == NE_OK) {
+        c->d_keys[0] = k0;
+        c->d_keys[1] = k1;
+    } else {
+        if (k0) dfree(c, k0);
+        c->err = saved;  // not an error: the direct path
+    }
+    return NE_OK;
+}
+
 int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     uint64_t u0, units;
     episode_range(c, episode, &u0, &units);
@@ -405,8 +451,9 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         NE_CUDA(c, cudaMemcpyAsync(&N, c->d_total, sizeof N, cudaMemcpyDeviceToHost, c->stream));
         NE_CUDA(c, cudaStreamSynchronize(c->stream));
     }
-    if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > capacity %llu", (unsigned long long)N,
+    if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
                                   (unsigned long long)c->N_max);
+    NE_TRY(ensure_pool(c, N));
     // O6: every kept pair to its position pi(x), then stable bucketing by sub-part
     p.N = N;
     const bool keyed = c->d_keys[0] && N > 0 && N <= (1ull << 32);
@@ -903,33 +950,9 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     NE_ALLOC(c->d_base, std::max<uint64_t>(c->units_max, 1));
     if (!reuse) NE_TRY(dalloc(c, &c->d_scan_scratch, ne::scan_scratch_bytes(c->units_max)));
     NE_ALLOC(c->d_total, 1);
-    NE_ALLOC(c->d_slots, std::max<uint64_t>(c->N_max, 1));
-    NE_ALLOC(c->d_pool, std::max<uint64_t>(c->N_max, 1));
+    // d_slots / d_pool / d_keys: sized by the first episode's pool (ensure_pool)
     if (!reuse) NE_TRY(dalloc(c, &c->d_scratch, ne::bucket_scratch_bytes(c->N_max, nb_local(c))));
     NE_ALLOC(c->d_boff, (size_t)nb_local(c) + 1);
-    // Keyed pool sink: two u32 key buffers (8 bytes per slot), allocated last
-    // and only if they fit (HBM left after everything above); otherwise the
-    // direct sink builds the same pool.  NE_POOL_DIRECT=1 forces the direct
-    // sink (tests, A/B).
-    if (!reuse) {
-        const char* e = std::getenv("NE_POOL_DIRECT");
-        c->d_keys[0] = c->d_keys[1] = nullptr;
-        const size_t bytes = std::max<uint64_t>(c->N_max, 1) * sizeof(uint32_t);
-        size_t free_b = 0, total_b = 0;
-        const bool room = c->alloc || (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
-                                       free_b >= 2 * bytes + (1ull << 30));  // keep 1 GiB for the caller
-        if (room && !(e && std::atoi(e) != 0)) {
-            void* k0 = nullptr;
-            void* k1 = nullptr;
-            const std::string saved = c->err;
-            if (dalloc(c, &k0, bytes) == NE_OK && dalloc(c, &k1, bytes) == NE_OK) {
-                c->d_keys[0] = static_cast<uint32_t*>(k0);
-                c->d_keys[1] = static_cast<uint32_t*>(k1);
-            } else {
-                c->err = saved;  // not an error: the direct sink (k0, if any, stays unused until free_all)
-            }
-        }
-    }
 #undef NE_ALLOC
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
     c->loaded = true;

@@ -117,6 +117,29 @@ def test_pool_sinks_bit_exact(c1, sink, kind, monkeypatch):
             eng.close()
 
 
+@pytest.mark.parametrize("direct", ["0", "1"])
+def test_pool_buffers_grow(direct, monkeypatch):
+    """Pool buffers are sized by the first pool built (plus 1/8) and kept
+    across same-shape reloads; a larger pool grows them.  R-MAT (84 550 pairs)
+    -> uniform graph of the same n, nnz (114 000: growth) -> R-MAT again, two
+    episodes each: every pool equals the oracle's."""
+    monkeypatch.setenv("NE_POOL_DIRECT", direct)
+    A = synth.rmat_graph(600, 3000, 21)
+    B = synth.uniform_graph(600, 3000, 22)
+    kw = dict(dim=32, episodes=2, subparts=2)
+    cfg = ocfg(**kw)
+    eng = engine(**kw)
+    for off, tgt in (A, B, A):
+        eng.load_graph(off, tgt)
+        for e in (1, 0):
+            ref, boff = oracle.build_episode(cfg, off, tgt, 6, e)
+            eng.random_walk(6, e)
+            assert eng.build_samples(6, e) == int(boff[-1])
+            for vs in range(2):
+                assert np.array_equal(eng.export_samples(vs), ref[int(boff[vs]):int(boff[vs + 1])]), (e, vs)
+    eng.close()
+
+
 def test_pool_bit_exact_multi_episode_line(c1):
     off, tgt = c1
     for kw in (dict(episodes=3, walks_per_node=2, subparts=2), dict(walk_len=0, window=0, episodes=2)):
