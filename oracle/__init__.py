@@ -47,7 +47,7 @@ class _Config(C.Structure):
     _fields_ = [("dim", C.c_uint32), ("negatives", C.c_uint32), ("walk_len", C.c_uint32),
                 ("window", C.c_uint32), ("walks_per_node", C.c_uint32), ("episodes", C.c_uint32),
                 ("subparts", C.c_uint32), ("parts", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
-                ("update_rule", C.c_uint32), ("reserved", C.c_uint32), ("seed", C.c_uint64)]
+                ("update_rule", C.c_uint32), ("storage", C.c_uint32), ("seed", C.c_uint64)]
 
 
 class _Stats(C.Structure):
@@ -69,11 +69,12 @@ class Config:
     p: float = 1.0   # node2vec return parameter (NEXT-1); p = q = 1: first order
     q: float = 1.0   # node2vec in-out parameter
     update_rule: int = 0  # 0 sequential (Alg. 1), 1 accumulated (word2vec, NEXT-4)
+    storage: int = 0      # 0 fp32 rows, 1 bf16 rows (NEXT-4, reading D16)
 
     def c(self) -> _Config:
         return _Config(self.dim, self.negatives, self.walk_len, self.window, self.walks_per_node,
-                       self.episodes, self.subparts, self.parts, self.p, self.q, self.update_rule, 0,
-                       self.seed)
+                       self.episodes, self.subparts, self.parts, self.p, self.q, self.update_rule,
+                       self.storage, self.seed)
 
 
 _lib = None
@@ -95,6 +96,7 @@ def lib():
     L.or_partition_bounds.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, _u64p]
     L.or_part_of.argtypes = [C.c_uint64, _u64p, C.c_uint32]
     L.or_part_of.restype = C.c_uint32
+    L.or_round_bf16_array.argtypes = [_f32p, C.c_uint64]
     L.or_weight075.argtypes = [C.c_uint64]
     L.or_weight075.restype = C.c_double
     L.or_alias_build.argtypes = [_u64p, C.c_uint64, _u32p, _u32p]
@@ -308,6 +310,15 @@ def init_vertex(n: int, d: int, seed: int, row_begin: int = 0) -> np.ndarray:
     if n:
         lib().or_init_vertex(V.reshape(-1), row_begin, row_begin + n, d, seed)
     return V
+
+
+def round_bf16(x) -> np.ndarray:
+    """NEXT-4 bf16 storage: every element rounded to the nearest bfloat16 (ties
+    to even), as float32 (a copy)."""
+    a = np.array(x, np.float32, copy=True, order="C")
+    if a.size:
+        lib().or_round_bf16_array(a.reshape(-1), a.size)
+    return a
 
 
 def sigmoid(x: float) -> float:

@@ -35,7 +35,7 @@ typedef struct {
     uint32_t parts;          /* P context/vertex parts (GPUs)   */
     float    p, q;           /* node2vec return / in-out parameters; 1, 1 (or 0) = first order */
     uint32_t update_rule;    /* 0 sequential (Alg. 1, D2); 1 accumulated (word2vec, NEXT-4) */
-    uint32_t reserved;
+    uint32_t storage;        /* 0 fp32 rows; 1 bf16 rows (NEXT-4, reading D16)  */
     uint64_t seed;           /* Philox key                                      */
 } or_config;
 
@@ -89,6 +89,10 @@ void     or_negatives(const or_config *cfg, const uint32_t *thr, const uint32_t 
 /* ---- O9 / O10 / O11 ----------------------------------------------------- */
 void     or_init_vertex(float *V, uint64_t row_begin, uint64_t row_end, uint32_t d, uint64_t seed);
 double   or_sigmoid(double x);
+/* NEXT-4 bf16 row storage (DESIGN reading D16): the bfloat16 nearest to x,
+ * ties to even (NaN stays NaN), returned as the float it represents. */
+float    or_round_bf16(float x);
+void     or_round_bf16_array(float *x, uint64_t count);
 void     or_sgns_grad(const double *v, const double *c, uint32_t d, int label,
                       double *gv, double *gc, double *loss);
 double   or_sgns_step(float *v, float *c, uint32_t d, int label, float lr);

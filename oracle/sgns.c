@@ -176,6 +176,40 @@ uint32_t or_plan_vsub(uint32_t P, uint32_t k, uint32_t r, uint32_t t, uint32_t g
  * usage"), so the order over g is immaterial; reverse_within_step = 1 replays
  * it backwards to let a test check exactly that.  thr/alias come from
  * or_build_alias_tables.  Returns 0, or -1 on a bad configuration. */
+/* NEXT-4 bf16 row storage (reading D16).  bfloat16 keeps the upper 16 bits of
+ * the IEEE binary32 pattern; round to nearest, ties to even, on the dropped
+ * lower half: add 0x7FFF plus the lowest kept bit, then truncate. */
+float or_round_bf16(float x)
+{
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu)) {  /* NaN: keep it a (quiet) NaN */
+        u |= 0x00400000u;
+    } else {
+        u += 0x7FFFu + ((u >> 16) & 1u);
+    }
+    u &= 0xFFFF0000u;
+    memcpy(&x, &u, 4);
+    return x;
+}
+
+void or_round_bf16_array(float *x, uint64_t count)
+{
+    uint64_t i;
+    for (i = 0; i < count; ++i) x[i] = or_round_bf16(x[i]);
+}
+
+/* bf16 storage: the sample ran on full-precision working rows (the in-place
+ * updates of or_train_sample); its rows are stored once, rounded, at the end. */
+static void round_sample_rows(float *V, float *C, uint32_t d, uint32_t src, uint32_t dst,
+                              const uint32_t *negs, uint32_t K)
+{
+    uint32_t j;
+    or_round_bf16_array(V + (uint64_t)src * d, d);
+    or_round_bf16_array(C + (uint64_t)dst * d, d);
+    for (j = 0; j < K; ++j) or_round_bf16_array(C + (uint64_t)negs[j] * d, d);
+}
+
 int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offsets,
                           const uint32_t *targets, const uint32_t *thr, const uint32_t *alias,
                           uint32_t epoch, float lr, uint32_t episode_begin, uint32_t episode_end,
@@ -189,7 +223,7 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
         cfg->episodes == 0 || cfg->episodes > 4096 || epoch >= (1u << 24))
         return -1;
     if (cfg->walk_len > 0 && (cfg->window == 0 || cfg->walks_per_node == 0)) return -1;
-    if (cfg->update_rule > 1) return -1;
+    if (cfg->update_rule > 1 || cfg->storage > 1) return -1;
     or_partition_bounds(0, n, P, bounds);
     boff = (uint64_t *)malloc((nblocks + 1) * sizeof(uint64_t));
     if (!boff) return -1;
@@ -217,6 +251,7 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
                         loss = cfg->update_rule == 1
                                    ? or_train_sample_accumulated(V, C, d, pr[0], pr[1], negs, K, lr)
                                    : or_train_sample(V, C, d, pr[0], pr[1], negs, K, lr);
+                        if (cfg->storage == 1) round_sample_rows(V, C, d, pr[0], pr[1], negs, K);
                         if (stats) { stats->samples += 1; stats->loss_sum += loss; }
                     }
                 }
