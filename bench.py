@@ -37,10 +37,11 @@ SGNS_KERNEL = ("ne::sgns_tma_kernel (rows staged by TMA bulk copies, 16 lanes/sa
                "ne::sgns_kernel<16,2,5,2,ADD> (16 lanes/sample, 2 samples/warp, red.v4 write-back)")
 
 
-def alg_bytes_per_sample(d: int, K: int) -> int:
+def alg_bytes_per_sample(d: int, K: int, esz: int = 4) -> int:
     """pair (8 B) + K alias entries (8 B) + read and write of the
-    vertex row, the positive context row and K negative rows (8 d (2 + K))."""
-    return 8 + 8 * K + 8 * d * (2 + K)
+    vertex row, the positive context row and K negative rows (2 esz d (2 + K);
+    esz = 4 for fp32 rows: 7216 B at d = 128, K = 5; 2 for bf16 rows: 3632 B)."""
+    return 8 + 8 * K + 2 * esz * d * (2 + K)
 
 
 def hbm_peak():
@@ -172,6 +173,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--episodes", type=int, default=0, help="episodes per epoch (0 = workload default)")
     ap.add_argument("--subparts", type=int, default=4, help="vertex sub-parts per GPU (the paper's k, P:152)")
+    ap.add_argument("--storage", default="f32", choices=["f32", "bf16"],
+                    help="row storage: f32 (the paper's, the headline) or bf16 (NEXT-4 option, reading D16)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -203,7 +206,7 @@ def main():
     stream = torch.cuda.current_stream()
     eng = Engine(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
                  walks_per_node=1, episodes=episodes, subparts=args.subparts, deterministic=False, seed=42,
-                 p=w.p, q=w.q,
+                 p=w.p, q=w.q, storage=ne.NE_STORE_BF16 if args.storage == "bf16" else ne.NE_STORE_F32,
                  device=local, rank=rank, world=world, nccl_id=nccl_id, torch_allocator=True,
                  stream=stream.cuda_stream)
     eng.load_graph(off, tgt)
@@ -245,7 +248,8 @@ def main():
     value = samples_all / (ms_max / 1e3)
 
     # roofline of the dominant kernel (SGNS), this rank's launches
-    B = alg_bytes_per_sample(w.dim, w.negatives)
+    esz = 2 if args.storage == "bf16" else 4
+    B = alg_bytes_per_sample(w.dim, w.negatives, esz)
     achieved = samples * B / (ms_train / 1e3) / 1e9 if ms_train > 0 else 0.0
     peak, peak_src = hbm_peak()
     traffic = None
@@ -254,7 +258,7 @@ def main():
         with open(prof) as f:
             tr = json.load(f).get(args.workload)
         if tr:
-            traffic = tr.get("dram_bytes_per_launch")
+            traffic = tr.get("dram_bytes_per_launch") if esz == 4 else tr.get("bf16_dram_bytes_per_launch")
 
     # end-to-end through the public API with host buffers (pinned)
     if isinstance(off, np.ndarray):
@@ -294,12 +298,13 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f32" if esz == 4 else "bf16 rows, f32 arithmetic (NEXT-4 option; not the headline)",
             "data": "synthetic",
             "config": {"workload": desc, "step": "one epoch: walk + augment + order/bucket + SGNS (+ ring)",
                        "samples_per_step": samples_all / args.steps, "episodes": episodes, "subparts": args.subparts,
                        "mode": "hogwild", "parallelism": f"2D ring x{world}",
-                       "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * 4 / 1e9),
+                       "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * esz / 1e9),
                        "graph_generator": "numpy Philox (host)" if w.m <= 200_000_000 else "torch CUDA generator"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": SGNS_KERNEL,

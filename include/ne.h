@@ -66,6 +66,9 @@ enum { NE_UPDATE_SEQUENTIAL = 0, NE_UPDATE_ACCUMULATED = 1 };
 /* ne_config.staging */
 enum { NE_STAGE_DEVICE = 0, NE_STAGE_HOST = 1 };
 
+/* ne_config.storage */
+enum { NE_STORE_F32 = 0, NE_STORE_BF16 = 1 };
+
 /* ne_get_embeddings / ne_set_embeddings: which matrix. */
 enum { NE_VERTEX = 0, NE_CONTEXT = 1 };
 
@@ -118,6 +121,14 @@ typedef struct {
                                 and D2H of t-1 overlap the training of t (the paper's
                                 pipeline stages 5 and 2; NEXT-2).
                                 Single rank only (world == 1).                         */
+    uint32_t storage;        /* NE_STORE_F32 (0): fp32 rows, the paper's precision;
+                                NE_STORE_BF16 (1): rows stored as bfloat16 (NEXT-4,
+                                DESIGN reading D16) -- half the bytes per sample;
+                                compute stays fp32, each touched row is rounded to the
+                                nearest bf16 (ties to even) when the sample stores it.
+                                ne_get/set_embeddings still take fp32 host arrays.
+                                This round: world == 1 and staging == NE_STAGE_DEVICE. */
+    uint32_t reserved;       /* must be 0                                               */
     uint64_t seed;           /* Philox key (contract R1)                                */
 } ne_config;
 

@@ -13,6 +13,7 @@ import os
 import subprocess
 import sys
 import sysconfig
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -49,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     common = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
-    objs = []
+    objs, jobs = [], []
     for src in sources():
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         objs.append(obj)
@@ -57,7 +58,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd = [NVCC] + ARCH + common + ["-c", src, "-o", obj]
             if verbose and src.endswith(".cu"):
                 cmd += ["-Xptxas", "-v"]
-            subprocess.run(cmd, check=True)
+            jobs.append(cmd)
+    # translation units compile in parallel (the SGNS instantiations dominate)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(subprocess.run, cmd, check=True) for cmd in jobs]:
+            f.result()
     if force or _stale(OUT, objs):
         tmp = OUT + f".tmp{os.getpid()}"
         cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + \

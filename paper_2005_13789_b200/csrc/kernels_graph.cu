@@ -2,6 +2,8 @@
 // engine (sm_100a).
 #include <algorithm>
 
+#include <cuda_bf16.h>
+
 #include "ne_device.cuh"
 #include "ne_internal.h"
 
@@ -42,7 +44,7 @@ cudaError_t launch_validate_csr(const uint64_t* off, const uint32_t* tgt, uint64
 // x = Philox((i_lo, i_hi, c/4, INIT<<24)).  IEEE division (no fast-math), so the
 // result is bit-identical to any correctly rounded implementation.
 __global__ void init_vertex_kernel(float* __restrict__ V, uint64_t row_begin, uint64_t rows,
-                                   uint32_t d, uint64_t seed) {
+                                   uint32_t d, uint64_t seed, bool bf16) {
     const uint32_t q = d / 4;
     const uint64_t total = rows * q;
     const uint2 key = key_of(seed);
@@ -58,14 +60,41 @@ __global__ void init_vertex_kernel(float* __restrict__ V, uint64_t row_begin, ui
         o.y = __fdiv_rn(__fsub_rn(__fmul_rn((float)(x.y >> 8), 0x1p-24f), 0.5f), fd);
         o.z = __fdiv_rn(__fsub_rn(__fmul_rn((float)(x.z >> 8), 0x1p-24f), 0.5f), fd);
         o.w = __fdiv_rn(__fsub_rn(__fmul_rn((float)(x.w >> 8), 0x1p-24f), 0.5f), fd);
-        reinterpret_cast<float4*>(V)[w] = o;
+        if (bf16) {  // NEXT-4 (D16): the O9 value rounded to the nearest bf16
+            const __nv_bfloat162 a = __floats2bfloat162_rn(o.x, o.y), b = __floats2bfloat162_rn(o.z, o.w);
+            reinterpret_cast<uint2*>(V)[w] = make_uint2(*reinterpret_cast<const uint32_t*>(&a),
+                                                        *reinterpret_cast<const uint32_t*>(&b));
+        } else {
+            reinterpret_cast<float4*>(V)[w] = o;
+        }
     }
 }
 
+// bf16 rows (NEXT-4) <-> fp32 host arrays: exact widening; rounding to nearest even.
+__global__ void convert_rows_kernel(const void* __restrict__ in, void* __restrict__ out, uint64_t n,
+                                    bool to_bf16) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        if (to_bf16) {
+            reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(reinterpret_cast<const float*>(in)[i]);
+        } else {
+            const uint32_t h = reinterpret_cast<const uint16_t*>(in)[i];
+            reinterpret_cast<float*>(out)[i] = __uint_as_float(h << 16);
+        }
+    }
+}
+
+cudaError_t launch_convert_rows(const void* in, void* out, uint64_t n, bool to_bf16, const Device& dev,
+                                cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    convert_rows_kernel<<<grid_for(n, 256, dev), 256, 0, s>>>(in, out, n, to_bf16);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_init_vertex(float* V, uint64_t row_begin, uint64_t rows, uint32_t d,
-                               uint64_t seed, const Device& dev, cudaStream_t s) {
+                               uint64_t seed, bool bf16, const Device& dev, cudaStream_t s) {
     if (rows == 0) return cudaSuccess;
-    init_vertex_kernel<<<grid_for(rows * (d / 4), 256, dev), 256, 0, s>>>(V, row_begin, rows, d, seed);
+    init_vertex_kernel<<<grid_for(rows * (d / 4), 256, dev), 256, 0, s>>>(V, row_begin, rows, d, seed, bf16);
     return cudaGetLastError();
 }
 

@@ -22,7 +22,10 @@ cudaError_t launch_validate_csr(const uint64_t* off, const uint32_t* tgt, uint64
                                 const Device& dev, cudaStream_t s);
 // O9: rows [row_begin, row_begin + rows) of the vertex matrix into V (row-major).
 cudaError_t launch_init_vertex(float* V, uint64_t row_begin, uint64_t rows, uint32_t d,
-                               uint64_t seed, const Device& dev, cudaStream_t s);
+                               uint64_t seed, bool bf16, const Device& dev, cudaStream_t s);
+// NEXT-4 bf16 rows: n elements bf16 -> fp32 (exact) or fp32 -> bf16 (nearest even).
+cudaError_t launch_convert_rows(const void* in, void* out, uint64_t n, bool to_bf16, const Device& dev,
+                                cudaStream_t s);
 // O4: walkers [omega0, omega0 + count) -> walks[count][k+1].  node2vec
 // (NEXT-1) when n2v_thr != nullptr: thresholds (return, neighbour, farther),
 // each <= 2^32, of the rejection step.  With wc.counts != nullptr the kernel
@@ -116,9 +119,12 @@ struct SgnsParams {
     uint64_t max_warps;         // Hogwild concurrency cap (>= 1)
     int atomic_writeback;       // Hogwild: red.add row deltas instead of storing rows
     int reserve_sms;            // SMs left free for the concurrent NCCL ring kernels
+    int bf16;                   // rows stored as bfloat16 (NEXT-4, reading D16); V, C point at them
     int accumulate;             // NEXT-4 accumulated-gradient update (word2vec order)
 };
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s);
+// bf16-row instantiations (kernels_sgns_bf16.cu); launch_sgns dispatches on p.bf16.
+cudaError_t launch_sgns_bf16(const SgnsParams& p, const Device& dev, cudaStream_t s);
 cudaError_t launch_sgns_tma(const SgnsParams& p, const Device& dev, cudaStream_t s);  // kernels_sgns_tma.cu
 cudaError_t launch_export_negatives(const SgnsParams& p, uint64_t pos_begin, uint64_t count,
                                     uint32_t* out, const Device& dev, cudaStream_t s);

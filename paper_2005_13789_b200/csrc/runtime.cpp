@@ -70,6 +70,8 @@ struct ne_ctx {
     uint64_t* pool_at = nullptr;  // the buffer (d_pool or d_slots) holding the built pool
     bool walk_counts = false;     // d_counts holds the O5 counts of the current walk (unsharded walk)
     uint64_t pool_cap = 0;        // pairs d_slots / d_pool (and d_keys) hold; grown by ensure_pool
+    float* d_tmp_f32 = nullptr;   // bf16 rows: fp32 staging of ne_get/set_embeddings
+    uint64_t tmp_f32_cap = 0;
     void* d_scratch = nullptr;
     uint32_t* d_counts = nullptr;   // per-unit kept-pair counts (O5)
     uint64_t* d_base = nullptr;     // their exclusive scan: part-local index bases
@@ -199,6 +201,8 @@ void free_all(ne_ctx* c) {
     c->allocs.clear();
     c->d_tmp_u32 = nullptr;
     c->tmp_u32_cap = 0;
+    c->d_tmp_f32 = nullptr;
+    c->tmp_f32_cap = 0;
     c->d_keys[0] = c->d_keys[1] = nullptr;
     c->d_slots = c->d_pool = c->pool_at = nullptr;
     c->pool_cap = 0;
@@ -517,6 +521,7 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
     p.max_warps = cap >= 1e15 ? ~0ull : std::max<uint64_t>(1, (uint64_t)cap);
     p.atomic_writeback = c->cfg.writeback == NE_WB_ATOMIC_DELTA ? 1 : 0;
     p.accumulate = (int)c->cfg.update_rule;
+    p.bf16 = c->cfg.storage == NE_STORE_BF16 ? 1 : 0;
     // with a ring, leave SMs to NCCL's send/recv kernels so the transfer of the
     // previous sub-part overlaps this block (developer knob NE_RING_RESERVE_SMS)
     static const int reserve = [] {  // measured: 0, 2, 4 SMs perform alike (C4, 4 GPUs)
@@ -718,6 +723,10 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     if (g.update_rule > NE_UPDATE_ACCUMULATED)
         return bad(fail(c, NE_EINVAL, "update_rule=%u not in {0, 1}", g.update_rule));
     if (g.staging > NE_STAGE_HOST) return bad(fail(c, NE_EINVAL, "staging=%u not in {0, 1}", g.staging));
+    if (g.storage > NE_STORE_BF16) return bad(fail(c, NE_EINVAL, "storage=%u not in {0, 1}", g.storage));
+    if (g.reserved != 0) return bad(fail(c, NE_EINVAL, "reserved=%u must be 0", g.reserved));
+    if (g.storage == NE_STORE_BF16 && g.staging != NE_STAGE_DEVICE)
+        return bad(fail(c, NE_EINVAL, "storage=NE_STORE_BF16 needs staging=NE_STAGE_DEVICE (this round)"));
     if (!(g.p >= 0.f) || !(g.q >= 0.f))
         return bad(fail(c, NE_EINVAL, "node2vec p=%g q=%g must be > 0 (0 = 1)", g.p, g.q));
     {
@@ -776,6 +785,8 @@ int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
     if (world < 1 || rank < 0 || rank >= world) return fail(c, NE_EINVAL, "rank=%d world=%d", rank, world);
     if (world > 1 && c->cfg.staging == NE_STAGE_HOST)
         return fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", world);
+    if (world > 1 && c->cfg.storage == NE_STORE_BF16)
+        return fail(c, NE_EINVAL, "storage=NE_STORE_BF16 needs world == 1 this round (world=%d)", world);
     if ((uint64_t)world * c->cfg.subparts > 256 || (uint64_t)world * world * c->cfg.subparts > 4096)
         return fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
     if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
@@ -894,15 +905,16 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     c->alias_pending = true;
 
     // Embeddings (O9): context part = 0; home vertex sub-parts initialised.
-    NE_ALLOC(c->d_C, std::max<uint64_t>(c->c_count, 1) * g.dim);
-    NE_CUDA(c, cudaMemsetAsync(c->d_C, 0, c->c_count * g.dim * sizeof(float), c->stream));
+    const uint64_t esz = g.storage == NE_STORE_BF16 ? 2 : 4;  // bytes per stored element
+    NE_ALLOC(c->d_C, std::max<uint64_t>(c->c_count, 1) * g.dim * esz / 4);
+    NE_CUDA(c, cudaMemsetAsync(c->d_C, 0, c->c_count * g.dim * esz, c->stream));
     // vertex sub-part slots: the ring needs 2k (ping-pong), one GPU k, host staging 3
     const bool staged = g.staging == NE_STAGE_HOST;
     if (staged && c->world > 1)
         return fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", c->world);
     const size_t nslots = staged ? std::min<size_t>(3, k) : (c->world > 1 ? 2 * (size_t)k : k);
     if (!reuse) c->vslot.assign(nslots, nullptr);
-    for (size_t i = 0; i < c->vslot.size(); ++i) NE_ALLOC(c->vslot[i], std::max<uint64_t>(c->max_sub_rows, 1) * g.dim);
+    for (size_t i = 0; i < c->vslot.size(); ++i) NE_ALLOC(c->vslot[i], std::max<uint64_t>(c->max_sub_rows, 1) * g.dim * esz / 4);
     c->cur = 0;
     if (staged) {
         const size_t bytes = (c->part_bounds[c->rank + 1] - c->part_bounds[c->rank]) * g.dim * sizeof(float);
@@ -923,7 +935,8 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
         const size_t vs = (size_t)c->rank * k + t;
         const uint64_t rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
         float* slot = staged ? c->vslot[t % c->vslot.size()] : c->vslot[t];
-        NE_CUDA(c, ne::launch_init_vertex(slot, c->sub_bounds[vs], rows, g.dim, g.seed, c->dev, c->stream));
+        NE_CUDA(c, ne::launch_init_vertex(slot, c->sub_bounds[vs], rows, g.dim, g.seed,
+                                          g.storage == NE_STORE_BF16, c->dev, c->stream));
         c->launches += 1;
         if (staged)  // stream order: the slot is reused only after its copy to the host
             NE_CUDA(c, cudaMemcpyAsync(c->h_V + (c->sub_bounds[vs] - c->part_bounds[c->rank]) * g.dim, slot,
@@ -1052,12 +1065,36 @@ static int rows_op(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, f
                     (unsigned long long)((row_end - row_begin) * d));
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
     NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));
+    const bool bf = c->cfg.storage == NE_STORE_BF16;
     auto copy = [&](float* dev_base, uint64_t base_row, uint64_t a, uint64_t b) -> int {
         if (a >= b) return NE_OK;
-        float* dptr = dev_base + (a - base_row) * d;
-        const size_t off = (a - row_begin) * d, bytes = (b - a) * d * sizeof(float);
-        if (host) NE_CUDA(c, cudaMemcpy(host + off, dptr, bytes, cudaMemcpyDefault));
-        else NE_CUDA(c, cudaMemcpy(dptr, in + off, bytes, cudaMemcpyDefault));
+        const size_t off = (a - row_begin) * d, count = (b - a) * d;
+        if (!bf) {
+            float* dptr = dev_base + (a - base_row) * d;
+            if (host) NE_CUDA(c, cudaMemcpy(host + off, dptr, count * sizeof(float), cudaMemcpyDefault));
+            else NE_CUDA(c, cudaMemcpy(dptr, in + off, count * sizeof(float), cudaMemcpyDefault));
+            return NE_OK;
+        }
+        // bf16 rows: convert through an fp32 device buffer (exact widening / nearest-even rounding)
+        uint16_t* dptr = reinterpret_cast<uint16_t*>(dev_base) + (a - base_row) * d;
+        if (c->tmp_f32_cap < count) {
+            if (c->d_tmp_f32) dfree(c, c->d_tmp_f32);
+            c->d_tmp_f32 = nullptr;
+            c->tmp_f32_cap = 0;
+            NE_TRY(dalloc_t(c, &c->d_tmp_f32, count));
+            c->tmp_f32_cap = count;
+        }
+        if (host) {
+            NE_CUDA(c, ne::launch_convert_rows(dptr, c->d_tmp_f32, count, false, c->dev, c->stream));
+            NE_CUDA(c, cudaMemcpyAsync(host + off, c->d_tmp_f32, count * sizeof(float), cudaMemcpyDefault,
+                                       c->stream));
+        } else {
+            NE_CUDA(c, cudaMemcpyAsync(c->d_tmp_f32, in + off, count * sizeof(float), cudaMemcpyDefault,
+                                       c->stream));
+            NE_CUDA(c, ne::launch_convert_rows(c->d_tmp_f32, dptr, count, true, c->dev, c->stream));
+        }
+        c->launches += 1;
+        NE_CUDA(c, cudaStreamSynchronize(c->stream));
         return NE_OK;
     };
     if (which == NE_CONTEXT) return copy(c->d_C, c->c_begin, row_begin, row_end);

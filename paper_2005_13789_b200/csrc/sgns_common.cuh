@@ -3,6 +3,7 @@
 // Every kernel variant calls sgns_step, so they share one arithmetic.
 #pragma once
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "ne_device.cuh"
@@ -108,6 +109,51 @@ __device__ __forceinline__ float sgns_step_acc(const float4 (&v0)[R], float4 (&c
     }
     return a;
 }
+
+// Row access by element group e (4 consecutive elements) of row `row` of a
+// d-wide matrix: fp32 rows are float4 accesses; bf16 rows (NEXT-4, reading
+// D16) are 8-byte accesses widened exactly to fp32 on load, rounded to nearest
+// even on store, and Hogwild deltas are added with one bf16x4 vector reduction
+// (red.global.add.noftz.v2.bf16x2 = REDG.E.ADD.BF16x4.RN).
+template <bool BF>
+struct RowIO;
+
+template <>
+struct RowIO<false> {
+    static __device__ __forceinline__ float4 load(const float* m, uint64_t row, uint32_t d, uint32_t e) {
+        return reinterpret_cast<const float4*>(m + row * d)[e];
+    }
+    static __device__ __forceinline__ void store(float* m, uint64_t row, uint32_t d, uint32_t e, float4 v) {
+        reinterpret_cast<float4*>(m + row * d)[e] = v;
+    }
+    static __device__ __forceinline__ void add(float* m, uint64_t row, uint32_t d, uint32_t e, float4 dv) {
+        atomicAdd(reinterpret_cast<float4*>(m + row * d) + e, dv);
+    }
+};
+
+template <>
+struct RowIO<true> {
+    static __device__ __forceinline__ uint2* at(const float* m, uint64_t row, uint32_t d, uint32_t e) {
+        return reinterpret_cast<uint2*>(const_cast<float*>(m)) + row * (d >> 2) + e;
+    }
+    static __device__ __forceinline__ uint32_t pack(float a, float b) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // .x = a in the low half
+        return *reinterpret_cast<const uint32_t*>(&h);
+    }
+    static __device__ __forceinline__ float4 load(const float* m, uint64_t row, uint32_t d, uint32_t e) {
+        const uint2 u = *at(m, row, d, e);
+        return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                           __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+    }
+    static __device__ __forceinline__ void store(float* m, uint64_t row, uint32_t d, uint32_t e, float4 v) {
+        *at(m, row, d, e) = make_uint2(pack(v.x, v.y), pack(v.z, v.w));
+    }
+    static __device__ __forceinline__ void add(float* m, uint64_t row, uint32_t d, uint32_t e, float4 dv) {
+        asm volatile("red.global.add.noftz.v2.bf16x2 [%0], {%1, %2};" ::"l"(at(m, row, d, e)),
+                     "r"(pack(dv.x, dv.y)), "r"(pack(dv.z, dv.w))
+                     : "memory");
+    }
+};
 
 __device__ __forceinline__ float4 scaled(float a, const float4& x) {
     return make_float4(a * x.x, a * x.y, a * x.z, a * x.w);

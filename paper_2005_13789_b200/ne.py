@@ -28,6 +28,7 @@ NE_VERTEX, NE_CONTEXT = 0, 1
 NE_WB_ATOMIC_DELTA, NE_WB_STORE = 0, 1
 NE_UPDATE_SEQUENTIAL, NE_UPDATE_ACCUMULATED = 0, 1
 NE_STAGE_DEVICE, NE_STAGE_HOST = 0, 1
+NE_STORE_F32, NE_STORE_BF16 = 0, 1
 
 
 class ne_config(C.Structure):
@@ -35,7 +36,8 @@ class ne_config(C.Structure):
                 ("window", C.c_uint32), ("walks_per_node", C.c_uint32), ("episodes", C.c_uint32),
                 ("subparts", C.c_uint32), ("deterministic", C.c_uint32), ("conflict_permille", C.c_uint32),
                 ("writeback", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
-                ("update_rule", C.c_uint32), ("staging", C.c_uint32), ("seed", C.c_uint64)]
+                ("update_rule", C.c_uint32), ("staging", C.c_uint32), ("storage", C.c_uint32),
+                ("reserved", C.c_uint32), ("seed", C.c_uint64)]
 
 
 class ne_stats(C.Structure):

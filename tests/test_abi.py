@@ -48,26 +48,37 @@ def test_host_partitions_match_oracle(orc):
 def test_create_validates_config_without_gpu():
     from paper_2005_13789_b200 import ne
     with pytest.raises(ne.NEError, match="NE_EINVAL: dim=130"):
-        ne.ne_create(ne.ne_config(130, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 42), 0)
+        ne.ne_create(ne.ne_config(130, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 0, 0, 42), 0)
     with pytest.raises(ne.NEError, match="NE_EINVAL: negatives=9"):
-        ne.ne_create(ne.ne_config(128, 9, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 42), 0)
+        ne.ne_create(ne.ne_config(128, 9, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 0, 0, 42), 0)
     with pytest.raises(ne.NEError, match="NE_EINVAL: window=6"):
-        ne.ne_create(ne.ne_config(128, 5, 5, 6, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 42), 0)
+        ne.ne_create(ne.ne_config(128, 5, 5, 6, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 0, 0, 42), 0)
 
 
 def test_create_validates_node2vec_and_writeback():
     from paper_2005_13789_b200 import ne
     with pytest.raises(ne.NEError, match="NE_EINVAL: node2vec p=-1"):
-        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, -1.0, 1.0, 0, 0, 42), 0)
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, -1.0, 1.0, 0, 0, 0, 0, 42), 0)
     with pytest.raises(ne.NEError, match="NE_EINVAL: writeback=7"):
-        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 7, 1.0, 1.0, 0, 0, 42), 0)
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 7, 1.0, 1.0, 0, 0, 0, 0, 42), 0)
     with pytest.raises(ne.NEError, match="NE_EINVAL: episodes=0"):
-        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 0, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 42), 0)
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 0, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 0, 0, 42), 0)
 
 
 def test_create_validates_update_rule():
     from paper_2005_13789_b200 import ne
     with pytest.raises(ne.NEError, match="NE_EINVAL: update_rule=2"):
-        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 2, 0, 42), 0)
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 2, 0, 0, 0, 42), 0)
     with pytest.raises(ne.NEError, match="NE_EINVAL: staging=3"):
-        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 3, 42), 0)
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 3, 0, 0, 42), 0)
+
+
+def test_create_validates_storage():
+    from paper_2005_13789_b200 import ne
+    with pytest.raises(ne.NEError, match="NE_EINVAL: storage=2"):
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 2, 0, 42), 0)
+    with pytest.raises(ne.NEError, match="NE_EINVAL: reserved=1"):
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 0, 1, 42), 0)
+    with pytest.raises(ne.NEError, match="NE_EINVAL: storage=NE_STORE_BF16 needs staging"):
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, ne.NE_STAGE_HOST,
+                                  ne.NE_STORE_BF16, 0, 42), 0)
