@@ -257,8 +257,10 @@ def main():
     if os.path.exists(prof):
         with open(prof) as f:
             tr = json.load(f).get(args.workload)
-        if tr:
-            traffic = tr.get("dram_bytes_per_launch") if esz == 4 else tr.get("bf16_dram_bytes_per_launch")
+        per_sample = (tr or {}).get("dram_bytes_per_sample" if esz == 4 else "bf16_dram_bytes_per_sample")
+        if per_sample and train_launches:
+            # captured DRAM bytes per sample x this run's samples per SGNS launch (this rank)
+            traffic = per_sample * samples / train_launches
 
     # end-to-end through the public API with host buffers (pinned)
     if isinstance(off, np.ndarray):
