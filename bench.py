@@ -32,9 +32,25 @@ import numpy as np  # noqa: E402
 METRIC = "positive edge samples/sec at d=128, K=5 (1/2/4/8 B200); HBM GB/s vs peak"
 UNIT = "positive samples/s"
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
-SGNS_KERNEL = ("ne::sgns_tma_kernel (rows staged by TMA bulk copies, 16 lanes/sample)"
-               if os.environ.get("NE_SGNS_TMA", "0") != "0" else
-               "ne::sgns_kernel<16,2,5,2,ADD> (16 lanes/sample, 2 samples/warp, red.v4 write-back)")
+def sgns_kernel_name(d: int, K: int, bf16: bool) -> str:
+    """The SGNS instantiation launch_sgns selects for (d, K, storage) -- the
+    default knobs of kernels_sgns.cu / sgns_kernel.cuh."""
+    if os.environ.get("NE_SGNS_TMA", "0") != "0" and not bf16:
+        return "ne::sgns_tma_kernel (rows staged by TMA bulk copies, 16 lanes/sample)"
+    q = d // 4
+    red = "bf16x4 red" if bf16 else "red.v4.f32"
+    kt = 5 if K == 5 else 0
+    if 16 < q <= 24 and K == 5:
+        g, r, minb = 8, 3, 1
+    elif q <= 32:
+        g, r, minb = 16, (1 if q <= 16 else 2), 2
+    else:
+        g, r = 32, (q + 31) // 32
+        minb = 1 if r > 2 else (2 if r == 2 else 3)
+    if kt == 0:
+        minb = min(minb, 2)
+    return (f"ne::sgns_kernel<{g},{r},{kt},{minb},ADD,BF={int(bf16)}> ({g} lanes/sample, "
+            f"{32 // g} samples/warp, {red} write-back)")
 
 
 def alg_bytes_per_sample(d: int, K: int, esz: int = 4) -> int:
@@ -309,7 +325,8 @@ def main():
                        "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * esz / 1e9),
                        "graph_generator": "numpy Philox (host)" if w.m <= 200_000_000 else "torch CUDA generator"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": SGNS_KERNEL,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": sgns_kernel_name(w.dim, w.negatives, esz == 2),
                          "bytes_per_sample": B, "launches": train_launches,
                          "avg_launch_ms": ms_train / max(train_launches, 1), "peak_source": peak_src},
             "phases_ms_per_step": {"walk": float(tsum[4]) / world / args.steps,
