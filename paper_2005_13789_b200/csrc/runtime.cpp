@@ -37,6 +37,9 @@ struct ne_ctx {
     void* user = nullptr;
     int rank = 0, world = 1;
     ncclComm_t comm = nullptr;
+    ncclComm_t comm_walk = nullptr;  // split of comm for the walk all-gather: NCCL serialises the
+                                     // operations of one communicator, and the ring's last
+                                     // return-home transfers would otherwise delay the next walk
     std::string err;
 
     struct Alloc { void* p; size_t bytes; };
@@ -376,7 +379,7 @@ int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         if (mine) c->launches += 1;
         c->walk_counts = false;  // other ranks' walkers: counted by the pool build
         NE_NCCL(c, ncclAllGather(c->d_walks + (uint64_t)c->rank * chunk * row, c->d_walks, chunk * row,
-                                 ncclUint32, c->comm, c->stream));
+                                 ncclUint32, c->comm_walk, c->stream));
     } else {
         NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0, units, c->cfg.walk_len,
                                    c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr, c->d_walks,
@@ -789,6 +792,7 @@ int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
         return fail(c, NE_EINVAL, "storage=NE_STORE_BF16 needs world == 1 this round (world=%d)", world);
     if ((uint64_t)world * c->cfg.subparts > 256 || (uint64_t)world * world * c->cfg.subparts > 4096)
         return fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
+    if (c->comm_walk) { ncclCommDestroy(c->comm_walk); c->comm_walk = nullptr; }
     if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
     c->rank = rank;
     c->world = world;
@@ -796,6 +800,7 @@ int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
         ncclUniqueId u;
         std::memcpy(&u, id, 128);
         NE_NCCL(c, ncclCommInitRank(&c->comm, world, u, rank));
+        NE_NCCL(c, ncclCommSplit(c->comm, 0, rank, &c->comm_walk, nullptr));
     }
     return NE_OK;
 }
@@ -1239,6 +1244,7 @@ void ne_destroy(ne_ctx* c) {
     if (c->stage_done) cudaEventDestroy(c->stage_done);
     if (c->h_V) cudaFreeHost(c->h_V);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->comm_walk) ncclCommDestroy(c->comm_walk);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->d_loss) cudaFree(c->d_loss);
     if (c->d_bad) cudaFree(c->d_bad);
