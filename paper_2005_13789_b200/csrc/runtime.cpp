@@ -637,8 +637,9 @@ int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st
                 float* Vn = c->vslot[(1 - c->cur) * k + t];
                 NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, e1, 0));
                 NE_NCCL(c, ncclGroupStart());
-                NE_NCCL(c, ncclSend(V, send_rows * d, ncclFloat, (int)((g + 1) % P), c->comm, c->comm_stream));
-                NE_NCCL(c, ncclRecv(Vn, recv_rows * d, ncclFloat, (int)((g + P - 1) % P), c->comm, c->comm_stream));
+                const ncclDataType_t dt = c->cfg.storage == NE_STORE_BF16 ? ncclBfloat16 : ncclFloat;
+                NE_NCCL(c, ncclSend(V, send_rows * d, dt, (int)((g + 1) % P), c->comm, c->comm_stream));
+                NE_NCCL(c, ncclRecv(Vn, recv_rows * d, dt, (int)((g + P - 1) % P), c->comm, c->comm_stream));
                 NE_NCCL(c, ncclGroupEnd());
                 cudaEvent_t rv = next_event(c);
                 NE_CUDA(c, cudaEventRecord(rv, c->comm_stream));
@@ -788,8 +789,6 @@ int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
     if (world < 1 || rank < 0 || rank >= world) return fail(c, NE_EINVAL, "rank=%d world=%d", rank, world);
     if (world > 1 && c->cfg.staging == NE_STAGE_HOST)
         return fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", world);
-    if (world > 1 && c->cfg.storage == NE_STORE_BF16)
-        return fail(c, NE_EINVAL, "storage=NE_STORE_BF16 needs world == 1 this round (world=%d)", world);
     if ((uint64_t)world * c->cfg.subparts > 256 || (uint64_t)world * world * c->cfg.subparts > 4096)
         return fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
     if (c->comm_walk) { ncclCommDestroy(c->comm_walk); c->comm_walk = nullptr; }

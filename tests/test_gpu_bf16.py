@@ -181,7 +181,35 @@ def test_bf16_hogwild_auc_matches_oracle():
     assert all(abs(a - a_ref) <= 0.01 for a in aucs), (a_ref, aucs)
 
 
-def test_bf16_rejects_ring_and_staging():
+@pytest.mark.parametrize("P", [2, 4])
+def test_bf16_ring_emulation_matching(P):
+    """P layout-only ranks on one device (pointer hand-over in place of the
+    NCCL ring, which moves bf16 sub-parts): the element-wise bar against the
+    oracle's P-part bf16 epoch on the perfect matching."""
     from paper_2005_13789_b200 import ne
-    with pytest.raises(ne.NEError, match="NE_STORE_BF16 needs world == 1"):
-        engine(rank=0, world=2)
+    off, tgt = _matching()
+    n = len(off) - 1
+    kw = dict(walk_len=1, window=1)
+    engs = [engine(rank=g, world=P, **kw) for g in range(P)]
+    for e in engs:
+        e.load_graph(off, tgt)
+        e.random_walk(0, 0)
+        e.build_samples(0, 0)
+    st = ne.ne_train_samples_local_ring([e.ctx for e in engs], 0, 0, 0.025)
+    cfg = ocfg(parts=P, **kw)
+    V = oracle.round_bf16(oracle.init_vertex(n, 128, 42))
+    Cm = np.zeros_like(V)
+    ns, loss = oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025)
+    assert st.samples == ns
+    for e in engs:
+        a, b = e.part
+        for got, ref in ((e.embeddings(0), V[a:b]), (e.embeddings(1), Cm[a:b])):
+            same, err = close_bf16(got, ref)
+            assert same >= 0.99 and err <= 2.0 + 5, (P, same, err)
+        e.close()
+
+
+def test_bf16_rejects_host_staging():
+    from paper_2005_13789_b200 import ne
+    with pytest.raises(ne.NEError, match="NE_STORE_BF16 needs staging"):
+        engine(staging=ne.NE_STAGE_HOST)
