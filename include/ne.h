@@ -127,8 +127,8 @@ typedef struct {
                                 compute stays fp32, each touched row is rounded to the
                                 nearest bf16 (ties to even) when the sample stores it.
                                 ne_get/set_embeddings still take fp32 host arrays; the
-                                ring moves bf16 sub-parts (half the bytes).
-                                Needs staging == NE_STAGE_DEVICE this round.           */
+                                ring and host staging move bf16 sub-parts (half the
+                                bytes).                                                 */
     uint32_t reserved;       /* must be 0                                               */
     uint64_t seed;           /* Philox key (contract R1)                                */
 } ne_config;

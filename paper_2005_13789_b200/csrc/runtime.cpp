@@ -180,6 +180,14 @@ int dalloc_t(ne_ctx* c, T** out, size_t count) {
     return NE_OK;
 }
 
+// Bytes per stored embedding element (NE_STORE_F32: 4, NE_STORE_BF16: 2).
+uint64_t elem_bytes(const ne_ctx* c) { return c->cfg.storage == NE_STORE_BF16 ? 2 : 4; }
+
+// Host-staged vertex matrix: address of this rank's row `row` (global id).
+void* host_row(const ne_ctx* c, uint64_t row) {
+    return reinterpret_cast<char*>(c->h_V) + (row - c->part_bounds[c->rank]) * c->cfg.dim * elem_bytes(c);
+}
+
 void dfree(ne_ctx* c, void* p) {
     for (size_t i = 0; i < c->allocs.size(); ++i)
         if (c->allocs[i].p == p) {
@@ -540,7 +548,7 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
 // back (comm stream); a slot is refilled only after its previous D2H.
 int do_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st) {
     const uint32_t k = c->cfg.subparts, S = (uint32_t)c->vslot.size();
-    const uint64_t d = c->cfg.dim, pb = c->part_bounds[c->rank];
+    const uint64_t d = c->cfg.dim;
     NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
     std::vector<cudaEvent_t> loaded(k), stored(k);
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
@@ -548,7 +556,7 @@ int do_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_st
         if (t >= S) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, stored[t - S], 0));
         else if (c->stage_pending) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->stage_done, 0));
         const uint64_t sb = c->sub_bounds[t], rows = c->sub_bounds[t + 1] - sb;
-        NE_CUDA(c, cudaMemcpyAsync(c->vslot[t % S], c->h_V + (sb - pb) * d, rows * d * sizeof(float),
+        NE_CUDA(c, cudaMemcpyAsync(c->vslot[t % S], host_row(c, sb), rows * d * elem_bytes(c),
                                    cudaMemcpyHostToDevice, c->copy_stream));
         loaded[t] = next_event(c);
         NE_CUDA(c, cudaEventRecord(loaded[t], c->copy_stream));
@@ -569,7 +577,7 @@ int do_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_st
         samples += sp.count;
         const uint64_t sb = c->sub_bounds[t], rows = c->sub_bounds[t + 1] - sb;
         NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, e1, 0));
-        NE_CUDA(c, cudaMemcpyAsync(c->h_V + (sb - pb) * d, c->vslot[t % S], rows * d * sizeof(float),
+        NE_CUDA(c, cudaMemcpyAsync(host_row(c, sb), c->vslot[t % S], rows * d * elem_bytes(c),
                                    cudaMemcpyDeviceToHost, c->comm_stream));
         stored[t] = next_event(c);
         NE_CUDA(c, cudaEventRecord(stored[t], c->comm_stream));
@@ -729,8 +737,6 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     if (g.staging > NE_STAGE_HOST) return bad(fail(c, NE_EINVAL, "staging=%u not in {0, 1}", g.staging));
     if (g.storage > NE_STORE_BF16) return bad(fail(c, NE_EINVAL, "storage=%u not in {0, 1}", g.storage));
     if (g.reserved != 0) return bad(fail(c, NE_EINVAL, "reserved=%u must be 0", g.reserved));
-    if (g.storage == NE_STORE_BF16 && g.staging != NE_STAGE_DEVICE)
-        return bad(fail(c, NE_EINVAL, "storage=NE_STORE_BF16 needs staging=NE_STAGE_DEVICE (this round)"));
     if (!(g.p >= 0.f) || !(g.q >= 0.f))
         return bad(fail(c, NE_EINVAL, "node2vec p=%g q=%g must be > 0 (0 = 1)", g.p, g.q));
     {
@@ -921,7 +927,7 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     for (size_t i = 0; i < c->vslot.size(); ++i) NE_ALLOC(c->vslot[i], std::max<uint64_t>(c->max_sub_rows, 1) * g.dim * esz / 4);
     c->cur = 0;
     if (staged) {
-        const size_t bytes = (c->part_bounds[c->rank + 1] - c->part_bounds[c->rank]) * g.dim * sizeof(float);
+        const size_t bytes = (c->part_bounds[c->rank + 1] - c->part_bounds[c->rank]) * g.dim * esz;
         if (c->h_V_bytes != bytes) {
             if (c->h_V) cudaFreeHost(c->h_V);
             c->h_V = nullptr;
@@ -943,8 +949,8 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
                                           g.storage == NE_STORE_BF16, c->dev, c->stream));
         c->launches += 1;
         if (staged)  // stream order: the slot is reused only after its copy to the host
-            NE_CUDA(c, cudaMemcpyAsync(c->h_V + (c->sub_bounds[vs] - c->part_bounds[c->rank]) * g.dim, slot,
-                                       rows * g.dim * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+            NE_CUDA(c, cudaMemcpyAsync(host_row(c, c->sub_bounds[vs]), slot, rows * g.dim * esz,
+                                       cudaMemcpyDeviceToHost, c->stream));
     }
 
     // Episode buffers: walks, pi-indexed slots, pool, bucketing scratch.
@@ -1105,7 +1111,8 @@ static int rows_op(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, f
     if (c->cfg.staging == NE_STAGE_HOST) {
         NE_CUDA(c, cudaStreamSynchronize(c->copy_stream));
         c->stage_pending = false;
-        return copy(c->h_V + (uint64_t)(row_begin - pb) * d, row_begin, row_begin, row_end);
+        // pinned host rows (device-accessible under UVA: the bf16 conversion kernel reads them in place)
+        return copy(static_cast<float*>(host_row(c, row_begin)), row_begin, row_begin, row_end);
     }
     const uint32_t k = c->cfg.subparts;
     for (uint32_t t = 0; t < k; ++t) {

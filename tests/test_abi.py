@@ -79,6 +79,4 @@ def test_create_validates_storage():
         ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 2, 0, 42), 0)
     with pytest.raises(ne.NEError, match="NE_EINVAL: reserved=1"):
         ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 0, 1, 42), 0)
-    with pytest.raises(ne.NEError, match="NE_EINVAL: storage=NE_STORE_BF16 needs staging"):
-        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, ne.NE_STAGE_HOST,
-                                  ne.NE_STORE_BF16, 0, 42), 0)
+

@@ -81,7 +81,7 @@ def test_bf16_set_get_round_trip():
 def _det_run(kw, graph=None, lr=0.025):
     off, tgt = graph if graph is not None else synth.workload_graph("c1")
     n = len(off) - 1
-    cfg = ocfg(**kw)
+    cfg = ocfg(**{k: v for k, v in kw.items() if k != "staging"})  # staging: where rows live, not what
     eng = engine(**kw)
     eng.load_graph(off, tgt)
     V = oracle.round_bf16(oracle.init_vertex(n, cfg.dim, 42))
@@ -209,7 +209,18 @@ def test_bf16_ring_emulation_matching(P):
         e.close()
 
 
-def test_bf16_rejects_host_staging():
+def test_bf16_host_staged_matching():
+    """bf16 rows with the vertex matrix in pinned host memory (NEXT-2 staging
+    moves bf16 sub-parts): the element-wise bar on the perfect matching, and
+    the host round trip through the staged matrix."""
     from paper_2005_13789_b200 import ne
-    with pytest.raises(ne.NEError, match="NE_STORE_BF16 needs staging"):
-        engine(staging=ne.NE_STAGE_HOST)
+    for got, ref in _det_run(dict(walk_len=1, window=1, staging=ne.NE_STAGE_HOST), graph=_matching()):
+        same, err = close_bf16(got, ref)
+        assert same >= 0.99 and err <= 2.0 + 5, (same, err)
+    off, tgt = _matching()
+    eng = engine(dim=64, staging=ne.NE_STAGE_HOST)
+    eng.load_graph(off, tgt)
+    x = np.random.default_rng(5).normal(0, 0.3, (len(off) - 1, 64)).astype(np.float32)
+    eng.set_embeddings(0, 0, x)
+    assert np.array_equal(eng.embeddings(0), oracle.round_bf16(x))
+    eng.close()
