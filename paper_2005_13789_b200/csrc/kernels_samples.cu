@@ -17,6 +17,7 @@
 // stores over a multi-GB target cost ~24 ms whether they miss L2 or not (TLB
 // reach is 256 MB); all-sequential passes avoid that.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ne_device.cuh"
 #include "ne_internal.h"
@@ -521,7 +522,11 @@ cudaError_t launch_order(uint64_t N, uint64_t* pairs0, uint32_t* keys0, uint64_t
     uint32_t bits = 0;
     while ((1ull << bits) < N) ++bits;
     const uint32_t total = bits > kPoolWinBits ? bits - kPoolWinBits : 0;  // key bits above the window
-    const uint32_t passes = std::max<uint32_t>(1, (total + 8) / 9);        // <= 9 bits per pass
+    // <= 9 bits per pass (2^10 bins per tile); NE_RADIX_MAXBITS (developer / test knob, 1..9)
+    // lowers the cap so small pools exercise the multi-pass path
+    const char* mb_env = std::getenv("NE_RADIX_MAXBITS");
+    const uint32_t mb = mb_env ? std::min(9u, std::max(1u, (uint32_t)std::atoi(mb_env))) : 9u;
+    const uint32_t passes = std::max<uint32_t>(1, (total + mb - 1) / mb);
     const uint32_t step = (total + passes - 1) / passes;
     cudaError_t e = cudaFuncSetAttribute(radix_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kRadSmem);

@@ -140,6 +140,28 @@ def test_pool_buffers_grow(direct, monkeypatch):
     eng.close()
 
 
+@pytest.mark.parametrize("maxbits", ["3", "2", "1"])
+def test_pool_many_radix_passes(c1, maxbits, monkeypatch):
+    """The radix passes with a lowered bits-per-pass cap (C1's ~1.4 M-pair pool
+    has 8 key bits above the window: 3 / 4 / 8 passes at P = 1, 2 / 3 / 6 at
+    P = 4): the multi-pass region arithmetic that pools above 2^31 pairs use
+    (3 passes at the default cap), bit-exact against the oracle."""
+    monkeypatch.setenv("NE_RADIX_MAXBITS", maxbits)
+    monkeypatch.delenv("NE_POOL_DIRECT", raising=False)
+    off, tgt = c1
+    for P in (1, 4):
+        ref, boff = oracle.build_episode(ocfg(parts=P, subparts=3), off, tgt, 5, 0)
+        for g in range(P):
+            eng = engine(rank=g, world=P, subparts=3)
+            eng.load_graph(off, tgt)
+            eng.random_walk(5, 0)
+            eng.build_samples(5, 0)
+            for vs in range(P * 3):
+                B = vs * P + g
+                assert np.array_equal(eng.export_samples(vs), ref[int(boff[B]):int(boff[B + 1])]), (maxbits, P, g, vs)
+            eng.close()
+
+
 def test_pool_bit_exact_multi_episode_line(c1):
     off, tgt = c1
     for kw in (dict(episodes=3, walks_per_node=2, subparts=2), dict(walk_len=0, window=0, episodes=2)):
