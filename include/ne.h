@@ -171,7 +171,9 @@ int ne_init_dist(ne_ctx *ctx, int rank, int world, const uint8_t id[128]);
 /* Load the graph G = (V, E) as CSR: offsets[n+1] (u64),
  * targets[nnz] (u32), validated on the device against S:24 (offsets
  * monotone, offsets[0] == 0, offsets[n] == nnz, every target < n); the copy is
- * resident in HBM on every rank.  Also builds this rank's alias table
+ * resident in HBM on every rank.  With world > 1 and NCCL each rank copies
+ * only its 1/world slice of the arrays it is given and an all-gather over
+ * NVLink completes the rest, so every rank must pass the same graph.  Also builds this rank's alias table
  * (deg^0.75 over its context part, O3/D9) and initialises the embeddings
  * (O9: vertex U(-0.5/d, 0.5/d), context 0).  May be called again to replace
  * the graph (re-initialises).  Errors: NE_EINVAL (+ first offending index),

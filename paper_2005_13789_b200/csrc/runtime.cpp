@@ -835,11 +835,33 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
 #define NE_ALLOC(ptr, count) \
     do { if (!reuse) NE_TRY(dalloc_t(c, &(ptr), (count))); } while (0)
 
-    // CSR into HBM, validated on the device.
-    NE_ALLOC(c->d_off, (size_t)n + 1);
-    NE_ALLOC(c->d_tgt, std::max<uint64_t>(nnz, 1));
-    NE_CUDA(c, cudaMemcpyAsync(c->d_off, offsets, ((size_t)n + 1) * sizeof(uint64_t), cudaMemcpyDefault, c->stream));
-    if (nnz) NE_CUDA(c, cudaMemcpyAsync(c->d_tgt, targets, nnz * sizeof(uint32_t), cudaMemcpyDefault, c->stream));
+    // CSR into HBM, validated on the device.  With a communicator every
+    // rank copies only its 1/P slice of the (identical) arrays over its own link
+    // and an all-gather over NVLink completes them: P x less host-link traffic
+    // per rank.  Buffers are padded to P equal chunks.
+    const bool sliced = P > 1 && c->comm_walk;
+    const uint64_t on = (uint64_t)n + 1;
+    const uint64_t oc = sliced ? (on + P - 1) / P : on, tc = sliced ? (nnz + P - 1) / P : nnz;
+    NE_ALLOC(c->d_off, sliced ? oc * P : on);
+    NE_ALLOC(c->d_tgt, std::max<uint64_t>(sliced ? tc * P : nnz, 1));
+    if (sliced) {
+        const uint64_t r = (uint64_t)c->rank;
+        const uint64_t ob = std::min(on, r * oc), oe = std::min(on, ob + oc);
+        const uint64_t tb = std::min(nnz, r * tc), te = std::min(nnz, tb + tc);
+        if (oe > ob)
+            NE_CUDA(c, cudaMemcpyAsync(c->d_off + ob, offsets + ob, (oe - ob) * sizeof(uint64_t), cudaMemcpyDefault,
+                                       c->stream));
+        if (te > tb)
+            NE_CUDA(c, cudaMemcpyAsync(c->d_tgt + tb, targets + tb, (te - tb) * sizeof(uint32_t), cudaMemcpyDefault,
+                                       c->stream));
+        NE_NCCL(c, ncclGroupStart());
+        NE_NCCL(c, ncclAllGather(c->d_off + r * oc, c->d_off, oc, ncclUint64, c->comm_walk, c->stream));
+        if (tc) NE_NCCL(c, ncclAllGather(c->d_tgt + r * tc, c->d_tgt, tc, ncclUint32, c->comm_walk, c->stream));
+        NE_NCCL(c, ncclGroupEnd());
+    } else {
+        NE_CUDA(c, cudaMemcpyAsync(c->d_off, offsets, on * sizeof(uint64_t), cudaMemcpyDefault, c->stream));
+        if (nnz) NE_CUDA(c, cudaMemcpyAsync(c->d_tgt, targets, nnz * sizeof(uint32_t), cudaMemcpyDefault, c->stream));
+    }
     NE_CUDA(c, cudaMemsetAsync(c->d_bad, 0xFF, 3 * sizeof(unsigned long long), c->stream));
     NE_CUDA(c, ne::launch_validate_csr(c->d_off, c->d_tgt, n, nnz, c->d_bad, c->n2v, c->dev, c->stream));
     c->launches += 1;
