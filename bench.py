@@ -34,22 +34,18 @@ UNIT = "positive samples/s"
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 def sgns_kernel_name(d: int, K: int, bf16: bool) -> str:
     """The SGNS instantiation launch_sgns selects for (d, K, storage) -- the
-    default knobs of kernels_sgns.cu / sgns_kernel.cuh."""
-    if os.environ.get("NE_SGNS_TMA", "0") != "0" and not bf16:
-        return "ne::sgns_tma_kernel (rows staged by TMA bulk copies, 16 lanes/sample)"
+    selection in sgns_kernel.cuh (launch_sgns_rows / launch_sgns_k)."""
     q = d // 4
     red = "bf16x4 red" if bf16 else "red.v4.f32"
     kt = 5 if K == 5 else 0
     if 16 < q <= 24 and K == 5:
-        g, r, minb = 8, 3, 1
+        g, r, shape = 8, 3, "64x5"
     elif q <= 32:
-        g, r, minb = 16, (1 if q <= 16 else 2), 2
+        g, r, shape = 16, (1 if q <= 16 else 2), "256x2"
     else:
         g, r = 32, (q + 31) // 32
-        minb = 1 if r > 2 else (2 if r == 2 else 3)
-    if kt == 0:
-        minb = min(minb, 2)
-    return (f"ne::sgns_kernel<{g},{r},{kt},{minb},ADD,BF={int(bf16)}> ({g} lanes/sample, "
+        shape = "256x2" if r == 2 else "64x1"
+    return (f"ne::sgns_kernel<{g},{r},{kt},{shape},ADD,BF={int(bf16)}> ({g} lanes/sample, "
             f"{32 // g} samples/warp, {red} write-back)")
 
 
@@ -121,59 +117,103 @@ def workload_desc(name):
                f"k={w.walk_len} l={w.window} w=1, d={w.dim}, K={w.negatives}"))
 
 
-def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle as it stands, rank 0 only."""
-    if rank != 0:
-        return
+def host_info() -> dict:
+    """Host cores (nproc: the CPUs this process may run on) and CPU model."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": len(os.sched_getaffinity(0)), "cpu_model": model}
+
+
+def oracle_hogwild(off, tgt, w, episodes: int, episode_ids, threads: int) -> dict:
+    """The oracle's Hogwild timing mode (oracle/batch.c) on episodes
+    `episode_ids` of an `episodes`-way split of epoch 0 of the workload, on
+    full-size host matrices: pool built by one thread, SGNS by `threads`
+    unsynchronised threads."""
     import oracle
-    import synth
-    w, desc = workload_desc(args.workload)
-    off, tgt = synth.workload_graph(args.workload)
     n = len(off) - 1
-    E = args.ref_episodes
     cfg = oracle.Config(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
-                        walks_per_node=1, episodes=E, subparts=4, parts=1, seed=42)
+                        walks_per_node=1, episodes=episodes, subparts=4, parts=1, seed=42, p=w.p, q=w.q)
     V = oracle.init_vertex(n, w.dim, 42)
     Cm = np.zeros_like(V)
     tables = oracle.build_alias_tables(cfg, off)
-    for s in range(args.warmup):
-        oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025, s, s + 1, tables=tables)
-    samples = 0
-    t0 = time.perf_counter()
-    for s in range(args.steps):
-        e = args.warmup + s
-        ns, _ = oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025, e, e + 1, tables=tables)
-        samples += ns
-    dt = time.perf_counter() - t0
-    value = samples / dt
-    sample = (f"episodes {args.warmup}..{args.warmup + args.steps - 1} of {E} of epoch 0 "
-              f"(~{n // E:,} walkers each, {samples:,} positive samples timed), full-size matrices")
+    tot = {"samples": 0, "sec_build": 0.0, "sec_train": 0.0, "per_step_s": []}
+    for e in episode_ids:
+        r = oracle.train_episode_hogwild(cfg, off, tgt, tables, V, Cm, 0, e, 0.025, threads)
+        tot["samples"] += r["samples"]
+        tot["sec_build"] += r["sec_build"]
+        tot["sec_train"] += r["sec_train"]
+        tot["per_step_s"].append(r["sec_build"] + r["sec_train"])
+    return tot
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands (its Hogwild timing mode,
+    one thread per host core), rank 0 only; each step is one episode of a
+    --ref-episodes split of the workload's epoch 0."""
+    if rank != 0:
+        return
+    import synth
+    w, desc = workload_desc(args.workload)
+    off, tgt = synth.workload_graph(args.workload)
+    if not isinstance(off, np.ndarray):
+        off, tgt = off.cpu().numpy().view(np.uint64), tgt.cpu().numpy().view(np.uint32)
+    hi = host_info()
+    T = hi["nproc"]
+    E = args.ref_episodes
+    oracle_hogwild(off, tgt, w, E, range(args.warmup), T)
+    r = oracle_hogwild(off, tgt, w, E, range(args.warmup, args.warmup + args.steps), T)
+    dt = r["sec_build"] + r["sec_train"]
+    value = r["samples"] / dt
+    sample = (f"episodes {args.warmup}..{args.warmup + args.steps - 1} of a {E}-episode split of epoch 0 "
+              f"(~{(len(off) - 1) // E:,} walkers each, {r['samples']:,} positive samples timed), full-size "
+              f"matrices; pool built by 1 thread ({r['sec_build']:.1f} s), SGNS by {T} Hogwild threads "
+              f"({r['sec_train']:.1f} s)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
             "dtype": "f64 arithmetic, f32 storage", "data": "synthetic",
-            "config": {"workload": desc, "impl": "oracle/ (plain C, single thread)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "config": {"workload": desc, "impl": "oracle/ (plain C), Hogwild timing mode (oracle/batch.c)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "threads": T, "kind": "oracle",
+                             "sample": sample, **hi},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline(args, off, tgt, w):
-    """The oracle timed on this host on a bounded sample of the same workload."""
+    """The oracle timed on this host on a bounded sample of the same workload:
+    its Hogwild timing mode with one thread per host core over >= 10 M samples
+    (one episode of a --cpu-episodes split), and beside it the deterministic
+    single-thread path (the parity reference) on a smaller episode."""
     import oracle
+    hi = host_info()
+    T = hi["nproc"]
     n = len(off) - 1
     E = args.cpu_episodes
+    r = oracle_hogwild(off, tgt, w, E, [0], T)
+    dt = r["sec_build"] + r["sec_train"]
+    # deterministic single thread (the parity reference), one episode of a 384-way split
     cfg = oracle.Config(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
-                        walks_per_node=1, episodes=E, subparts=4, parts=1, seed=42)
+                        walks_per_node=1, episodes=384, subparts=4, parts=1, seed=42, p=w.p, q=w.q)
     V = oracle.init_vertex(n, w.dim, 42)
     Cm = np.zeros_like(V)
     tables = oracle.build_alias_tables(cfg, off)
     t0 = time.perf_counter()
-    ns, _ = oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025, 0, 1, tables=tables)
-    dt = time.perf_counter() - t0
-    return {"value": ns / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"episode 0 of {E} (~{n // E:,} walkers, {ns:,} positive samples: walk + pool + "
-                      f"SGNS) of epoch 0 on the full-size graph and matrices, {dt:.1f} s, single thread"}
+    ns1, _ = oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025, 0, 1, tables=tables)
+    dt1 = time.perf_counter() - t0
+    return {"value": r["samples"] / dt, "unit": UNIT, "cores": T, "threads": T, "kind": "oracle", **hi,
+            "sample": (f"episode 0 of a {E}-episode split of epoch 0 (~{n // E:,} walkers, {r['samples']:,} "
+                       f"positive samples) on the full-size graph and matrices: pool built by 1 thread "
+                       f"({r['sec_build']:.1f} s), SGNS by {T} Hogwild threads ({r['sec_train']:.1f} s)"),
+            "sgns_only_value": r["samples"] / r["sec_train"],
+            "deterministic_single_thread": {"value": ns1 / dt1, "unit": UNIT, "cores": 1,
+                                            "sample": f"episode 0 of 384 ({ns1:,} samples: walk + pool + "
+                                                      f"SGNS), {dt1:.1f} s"}}
 
 
 def main():
@@ -184,8 +224,9 @@ def main():
     ap.add_argument("--workload", default="c3")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-episodes", type=int, default=384)
-    ap.add_argument("--ref-episodes", type=int, default=1536)
+    ap.add_argument("--cpu-episodes", type=int, default=48, help="cpu_baseline: one episode of this split "
+                    "(48: ~10.9 M samples on C3)")
+    ap.add_argument("--ref-episodes", type=int, default=192, help="--impl reference: one episode per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--episodes", type=int, default=0, help="episodes per epoch (0 = workload default)")
     ap.add_argument("--subparts", type=int, default=4, help="vertex sub-parts per GPU (the paper's k, P:152)")
@@ -219,7 +260,11 @@ def main():
         obj = [ne.ne_get_nccl_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    stream = torch.cuda.current_stream()
+    # the library computes on a dedicated torch stream; the timing events are
+    # recorded on that same stream (ne_join first folds the ring's trailing
+    # transfers, left on the library's comm stream, into it)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     eng = Engine(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
                  walks_per_node=1, episodes=episodes, subparts=args.subparts, deterministic=False, seed=42,
                  p=w.p, q=w.q, storage=ne.NE_STORE_BF16 if args.storage == "bf16" else ne.NE_STORE_F32,
@@ -242,6 +287,7 @@ def main():
         ev0.record(stream)
         for s in range(args.steps):
             stats.append(eng.train_epoch(args.warmup + s, 0.025))
+        eng.join()
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
@@ -268,7 +314,7 @@ def main():
     B = alg_bytes_per_sample(w.dim, w.negatives, esz)
     achieved = samples * B / (ms_train / 1e3) / 1e9 if ms_train > 0 else 0.0
     peak, peak_src = hbm_peak()
-    traffic = None
+    traffic = dram_achieved = None
     prof = os.path.join(ROOT, "profiles", "sgns_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:
@@ -277,8 +323,11 @@ def main():
         if per_sample and train_launches:
             # captured DRAM bytes per sample x this run's samples per SGNS launch (this rank)
             traffic = per_sample * samples / train_launches
+            dram_achieved = per_sample * samples / (ms_train / 1e3) / 1e9
 
-    # end-to-end through the public API with host buffers (pinned)
+    # end-to-end through the public API with host buffers (pinned): every step
+    # loads the CSR from the host (H2D), trains one epoch, reads the loss and
+    # copies this rank's trained vertex and context rows back to the host (D2H)
     if isinstance(off, np.ndarray):
         off_h = torch.from_numpy(off.view(np.int64)).pin_memory()
         tgt_h = torch.from_numpy(tgt.view(np.int32)).pin_memory()
@@ -288,6 +337,8 @@ def main():
         torch.cuda.empty_cache()
         off, tgt = off_h.numpy().view(np.uint64), tgt_h.numpy().view(np.uint32)
     h2d = off_h.numel() * 8 + tgt_h.numel() * 4
+    a, b = eng.part
+    emb_h = [torch.empty((b - a, w.dim), dtype=torch.float32).pin_memory() for _ in range(2)]
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_samples = 0
@@ -295,9 +346,12 @@ def main():
     for s in range(args.e2e_steps):
         ne.ne_load_graph(eng.ctx, off_h, tgt_h)
         st = eng.train_epoch(s, 0.025)  # loss_sum / samples read back (D2H) by the call
+        for which in (ne.NE_VERTEX, ne.NE_CONTEXT):
+            ne.ne_get_embeddings(eng.ctx, which, a, b, emb_h[which])
         e_samples += st["samples"]
     e1.record(stream)
     barrier()
+    d2h = 2 * (b - a) * w.dim * 4
     e_ms = torch.tensor([e0.elapsed_time(e1), e_samples], dtype=torch.float64, device="cuda")
     if world > 1:
         em = e_ms.clone()
@@ -326,6 +380,10 @@ def main():
                        "graph_generator": "numpy Philox (host)" if w.m <= 200_000_000 else "torch CUDA generator"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         # HBM-honest companion of frac: captured DRAM bytes per sample (ncu, committed
+                         # profile) x this run's samples / SGNS time -- frac counts L2 hits as HBM bytes
+                         "dram_achieved": dram_achieved,
+                         "dram_frac": dram_achieved / peak if dram_achieved else None,
                          "kernel": sgns_kernel_name(w.dim, w.negatives, esz == 2),
                          "bytes_per_sample": B, "launches": train_launches,
                          "avg_launch_ms": ms_train / max(train_launches, 1), "peak_source": peak_src},
@@ -335,8 +393,11 @@ def main():
                                    "comm_wait": float(tsum[6]) / world / args.steps},
             "cpu_baseline": cpu,
             "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    # CSR validation flags + offsets ends (32 B), block offsets (5 x 8 B), loss (8 B)
-                    "d2h_bytes_per_step": 32 + episodes * (8 * (args.subparts * world + 1) + 8)},
+                    # trained vertex + context rows of rank 0, CSR validation flags + offsets ends (32 B),
+                    # block offsets, pool size and loss per episode
+                    "d2h_bytes_per_step": d2h + 32 + episodes * (8 * (args.subparts * world + 1) + 16),
+                    "step": "ne_load_graph (pinned host CSR) + ne_train_epoch + ne_get_embeddings of both "
+                            "matrices (this rank's rows, to pinned host memory)"},
             "clocks": clk.summary(),
             "gpu_launches": int(tsum[3]),
         }

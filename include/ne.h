@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define NE_ABI_VERSION 1
+#define NE_ABI_VERSION 2
 
 typedef struct ne_ctx ne_ctx;
 
@@ -155,8 +155,19 @@ int ne_create(ne_ctx **out, const ne_config *cfg, int device,
               ne_alloc_fn alloc, ne_free_fn free_fn, void *user);
 
 /* Use `stream` (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream)
- * as the compute stream; NULL restores the context's own stream. */
+ * as the compute stream.  NULL (0) is the CUDA legacy default stream -- the
+ * handle torch reports for its default stream -- so work the caller queued
+ * there is ordered before the library's.  NE_STREAM_OWN selects the context's
+ * own non-blocking stream (the state after ne_create). */
+#define NE_STREAM_OWN ((void *)~(uintptr_t)0)
 int ne_set_stream(ne_ctx *ctx, void *stream);
+
+/* Make the compute stream wait (device-side, the host does not block) for
+ * every transfer the library left in flight on its side streams: the
+ * return-home ring transfers of the last ne_train_samples / ne_train_epoch
+ * and host-staging copies.  Call it before recording a timing event
+ * on the compute stream that must cover them. */
+int ne_join(ne_ctx *ctx);
 
 /* NCCL bootstrap for the multi-GPU ring: rank 0 calls
  * ne_get_nccl_id, the harness broadcasts the 128 bytes (torch.distributed),
@@ -259,6 +270,17 @@ int ne_export_samples(ne_ctx *ctx, uint32_t vsub, uint32_t *pairs_out, size_t ca
  * SGNS kernel uses (O8); out = count*K u32 (global node ids). */
 int ne_export_negatives(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint32_t vsub,
                         uint64_t pos_begin, uint64_t count, uint32_t *out);
+
+/* Train block (vsub, this rank's context part) of the built pool of
+ * (epoch, episode) once with the PRODUCTION kernel at its full grid (the
+ * deterministic flag of the context is ignored), recording the ids every
+ * sample position p trained: out[p*(2+K) + 0] = src, + 1 = dst,
+ * + 2 + j = negative j (O8).  vsub must be one of this rank's home sub-parts
+ * (rank*subparts <= vsub < (rank+1)*subparts); cap_u32 >= count*(2+K).
+ * count (nullable) receives the block size.  Updates the embeddings like
+ * training.  Errors: NE_ESTATE (no pool; host staging), NE_ERANGE. */
+int ne_capture_block(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint32_t vsub, float lr,
+                     uint32_t *out, size_t cap_u32, uint64_t *count);
 
 /* Single-GPU emulation of the P-rank ring for parity tests: ctxs[g] are
  * layout-only contexts (ne_init_dist(ctx, g, world, NULL)) on ONE device, each

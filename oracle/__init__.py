@@ -22,7 +22,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRCS = ["rng.c", "graph.c", "walk.c", "sgns.c", "eval.c"]
+_SRCS = ["rng.c", "graph.c", "walk.c", "sgns.c", "eval.c", "batch.c"]
 LIB_PATH = os.path.join(_HERE, "libne_oracle.so")
 TAG_WALK, TAG_NEG, TAG_SHUF, TAG_INIT = 1, 2, 3, 4
 
@@ -37,7 +37,7 @@ def build(force: bool = False) -> str:
     tmp = LIB_PATH + f".tmp{os.getpid()}"
     cmd = ["gcc", "-std=c11", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC",
            "-shared", "-Wall", "-Wno-maybe-uninitialized", "-o", tmp] + \
-          [os.path.join(_HERE, s) for s in _SRCS] + ["-lm"]
+          [os.path.join(_HERE, s) for s in _SRCS] + ["-lm", "-lpthread"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
@@ -155,6 +155,14 @@ def lib():
     L.or_auc_bruteforce.argtypes = [_f64p, C.c_uint64, _f64p, C.c_uint64]
     L.or_auc_bruteforce.restype = C.c_double
     L.or_score_pairs.argtypes = [_f32p, _f32p, C.c_uint32, _u32p, C.c_uint64, _f64p]
+    L.or_random_walks.argtypes = [C.c_uint64, _u64p, _u32p, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64,
+                                  C.c_uint32, C.c_float, C.c_float, _u32p]
+    L.or_negatives_range.argtypes = [C.POINTER(_Config), _u32p, _u32p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                     C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, _u32p]
+    L.or_train_episode_hogwild.argtypes = [C.POINTER(_Config), C.c_uint64, _u64p, _u32p, _u32p, _u32p,
+                                           C.c_uint32, C.c_uint32, C.c_float, C.c_uint32, _f32p, _f32p,
+                                           C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.or_train_episode_hogwild.restype = C.c_int64
     _lib = L
     return L
 
@@ -233,6 +241,20 @@ def random_walk(offsets, targets, seed: int, epoch: int, omega: int, k: int) -> 
     return path[:ln].copy()
 
 
+def random_walks(offsets, targets, seed: int, epoch: int, omega0: int, count: int, k: int,
+                 p: float = 1.0, q: float = 1.0) -> np.ndarray:
+    """O4 (or NEXT-1) walks of walkers [omega0, omega0 + count): [count, k+1] u32,
+    sentinel-padded (the layout ne_random_walk exports)."""
+    offsets = np.ascontiguousarray(offsets, np.uint64)
+    targets = np.ascontiguousarray(targets, np.uint32)
+    if len(targets) == 0:
+        targets = np.zeros(1, np.uint32)
+    out = np.zeros((max(count, 1), k + 1), np.uint32)
+    lib().or_random_walks(len(offsets) - 1, offsets, targets, seed, epoch, omega0, count, k, p, q,
+                          out.reshape(-1))
+    return out[:count]
+
+
 def node2vec_thresholds(p: float, q: float) -> np.ndarray:
     thr = np.zeros(3, np.uint64)
     lib().or_node2vec_thresholds(p, q, thr)
@@ -302,6 +324,37 @@ def negatives(cfg: Config, thr, al, c_begin: int, c_count: int, epoch: int, epis
                        np.ascontiguousarray(al[c_begin:c_begin + c_count]), c_begin, c_count,
                        epoch, episode, block, pos, out)
     return out[: cfg.negatives]
+
+
+def negatives_range(cfg: Config, thr, al, c_begin: int, c_count: int, epoch: int, episode: int,
+                    block: int, pos0: int, count: int) -> np.ndarray:
+    """O8 for positions [pos0, pos0 + count) of a block: [count, K] u32."""
+    K = cfg.negatives
+    out = np.zeros(max(count * K, 1), np.uint32)
+    c = cfg.c()
+    lib().or_negatives_range(C.byref(c), np.ascontiguousarray(thr[c_begin:c_begin + c_count]),
+                             np.ascontiguousarray(al[c_begin:c_begin + c_count]), c_begin, c_count,
+                             epoch, episode, block, pos0, count, out)
+    return out[:count * K].reshape(count, K)
+
+
+def train_episode_hogwild(cfg: Config, offsets, targets, tables, V, Cm, epoch: int, episode: int,
+                          lr: float, threads: int) -> dict:
+    """TIMING MODE ONLY (not a parity reference): one episode at P = 1, pool
+    built by one thread, each block trained by `threads` unsynchronised
+    (Hogwild) threads.  Returns samples, loss and the two phase times."""
+    offsets = np.ascontiguousarray(offsets, np.uint64)
+    targets = np.ascontiguousarray(targets, np.uint32)
+    thr, al = tables
+    c = cfg.c()
+    loss, sb, st = C.c_double(), C.c_double(), C.c_double()
+    cnt = lib().or_train_episode_hogwild(C.byref(c), len(offsets) - 1, offsets, targets, thr, al, epoch,
+                                         episode, lr, threads, V.reshape(-1), Cm.reshape(-1), C.byref(loss),
+                                         C.byref(sb), C.byref(st))
+    if cnt < 0:
+        raise RuntimeError("or_train_episode_hogwild failed")
+    return {"samples": int(cnt), "loss_sum": float(loss.value), "sec_build": float(sb.value),
+            "sec_train": float(st.value), "threads": threads}
 
 
 # --------------------------------------------------------------------------- O9-O11

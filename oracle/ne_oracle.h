@@ -114,6 +114,19 @@ int      or_train_epoch(const or_config *cfg, uint64_t n, const uint64_t *offset
                         uint32_t episode_begin, uint32_t episode_end,
                         int reverse_within_step, float *V, float *C, or_stats *stats);
 
+/* ---- batch.c: loops over the functions above; Hogwild timing mode ------- */
+void     or_random_walks(uint64_t n, const uint64_t *offsets, const uint32_t *targets, uint64_t seed,
+                         uint32_t epoch, uint64_t omega0, uint64_t count, uint32_t k, float p, float q,
+                         uint32_t *out);
+void     or_negatives_range(const or_config *cfg, const uint32_t *thr, const uint32_t *alias,
+                            uint64_t c_begin, uint64_t c_count, uint32_t epoch, uint32_t episode,
+                            uint32_t block, uint64_t pos0, uint64_t count, uint32_t *out);
+int64_t  or_train_episode_hogwild(const or_config *cfg, uint64_t n, const uint64_t *offsets,
+                                  const uint32_t *targets, const uint32_t *thr, const uint32_t *alias,
+                                  uint32_t epoch, uint32_t episode, float lr, uint32_t threads,
+                                  float *V, float *C, double *loss_sum, double *sec_build,
+                                  double *sec_train);
+
 /* ---- O12 evaluation ----------------------------------------------------- */
 double   or_auc(const double *pos, uint64_t npos, const double *neg, uint64_t nneg);
 double   or_auc_bruteforce(const double *pos, uint64_t npos, const double *neg, uint64_t nneg);

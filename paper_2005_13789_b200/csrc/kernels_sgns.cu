@@ -30,15 +30,6 @@ namespace ne {
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s) {
     if (p.count == 0) return cudaSuccess;
     if (p.K > (uint32_t)kMaxK || p.d % 4 != 0 || p.d == 0 || p.d > 512) return cudaErrorInvalidValue;
-    // NE_SGNS_TMA=1 (developer knob) stages rows in shared memory by TMA bulk
-    // copies (kernels_sgns_tma.cu); measured slower than the register kernel
-    // with L2 prefetch (smem caps it at 12 warps/SM), so it is off by default
-    static const int tma = env_int("NE_SGNS_TMA", 0);
-    if (tma && !p.accumulate && !p.bf16) {
-        const cudaError_t e = launch_sgns_tma(p, dev, s);
-        if (e != cudaErrorNotSupported) return e;
-        cudaGetLastError();
-    }
     if (p.bf16) return launch_sgns_bf16(p, dev, s);
     return launch_sgns_rows<false>(p, dev, s);
 }

@@ -121,11 +121,11 @@ struct SgnsParams {
     int reserve_sms;            // SMs left free for the concurrent NCCL ring kernels
     int bf16;                   // rows stored as bfloat16 (NEXT-4, reading D16); V, C point at them
     int accumulate;             // NEXT-4 accumulated-gradient update (word2vec order)
+    uint32_t* capture;          // test hook: (src, dst, negs) per position, [count][2+K] (nullptr: off)
 };
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s);
 // bf16-row instantiations (kernels_sgns_bf16.cu); launch_sgns dispatches on p.bf16.
 cudaError_t launch_sgns_bf16(const SgnsParams& p, const Device& dev, cudaStream_t s);
-cudaError_t launch_sgns_tma(const SgnsParams& p, const Device& dev, cudaStream_t s);  // kernels_sgns_tma.cu
 cudaError_t launch_export_negatives(const SgnsParams& p, uint64_t pos_begin, uint64_t count,
                                     uint32_t* out, const Device& dev, cudaStream_t s);
 

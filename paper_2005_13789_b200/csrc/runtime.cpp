@@ -777,7 +777,14 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
 
 int ne_set_stream(ne_ctx* c, void* stream) {
     NE_TRY(enter(c));
-    c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+    c->stream = stream == NE_STREAM_OWN ? c->own_stream : stream ? (cudaStream_t)stream : cudaStreamLegacy;
+    return NE_OK;
+}
+
+int ne_join(ne_ctx* c) {
+    NE_TRY(enter(c));
+    if (c->ring_pending) NE_CUDA(c, cudaStreamWaitEvent(c->stream, c->ring_done, 0));
+    if (c->stage_pending) NE_CUDA(c, cudaStreamWaitEvent(c->stream, c->stage_done, 0));
     return NE_OK;
 }
 
@@ -1101,10 +1108,11 @@ static int rows_op(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, f
     auto copy = [&](float* dev_base, uint64_t base_row, uint64_t a, uint64_t b) -> int {
         if (a >= b) return NE_OK;
         const size_t off = (a - row_begin) * d, count = (b - a) * d;
-        if (!bf) {
+        if (!bf) {  // on the compute stream, then synchronised: ordered after training, complete on return
             float* dptr = dev_base + (a - base_row) * d;
-            if (host) NE_CUDA(c, cudaMemcpy(host + off, dptr, count * sizeof(float), cudaMemcpyDefault));
-            else NE_CUDA(c, cudaMemcpy(dptr, in + off, count * sizeof(float), cudaMemcpyDefault));
+            if (host) NE_CUDA(c, cudaMemcpyAsync(host + off, dptr, count * sizeof(float), cudaMemcpyDefault, c->stream));
+            else NE_CUDA(c, cudaMemcpyAsync(dptr, in + off, count * sizeof(float), cudaMemcpyDefault, c->stream));
+            NE_CUDA(c, cudaStreamSynchronize(c->stream));
             return NE_OK;
         }
         // bf16 rows: convert through an fp32 device buffer (exact widening / nearest-even rounding)
@@ -1180,6 +1188,9 @@ int ne_export_negatives(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vs
     if (total == 0) return NE_OK;
     NE_TRY(wait_alias(c));
     if (c->tmp_u32_cap < total) {
+        if (c->d_tmp_u32) dfree(c, c->d_tmp_u32);
+        c->d_tmp_u32 = nullptr;
+        c->tmp_u32_cap = 0;
         NE_TRY(dalloc_t(c, &c->d_tmp_u32, total));
         c->tmp_u32_cap = total;
     }
@@ -1193,6 +1204,42 @@ int ne_export_negatives(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vs
     p.episode = episode;
     p.block = vsub * (uint32_t)c->world + (uint32_t)c->rank;
     NE_CUDA(c, ne::launch_export_negatives(p, pos_begin, count, c->d_tmp_u32, c->dev, c->stream));
+    c->launches += 1;
+    NE_CUDA(c, cudaMemcpyAsync(out, c->d_tmp_u32, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    return NE_OK;
+}
+
+int ne_capture_block(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vsub, float lr, uint32_t* out,
+                     size_t cap_u32, uint64_t* count) {
+    NE_TRY(enter(c));
+    NE_TRY(check_loaded(c));
+    if (c->built_episode != (int64_t)episode || c->built_epoch != (int64_t)epoch)
+        return fail(c, NE_ESTATE, "no sample pool for epoch %u episode %u", epoch, episode);
+    if (c->cfg.staging == NE_STAGE_HOST) return fail(c, NE_ESTATE, "capture needs the vertex matrix in HBM");
+    const uint32_t k = c->cfg.subparts, home = (uint32_t)c->rank * k;
+    if (vsub < home || vsub >= home + k)
+        return fail(c, NE_ERANGE, "vsub=%u is not a home sub-part of rank %d ([%u, %u))", vsub, c->rank, home, home + k);
+    NE_TRY(wait_alias(c));
+    NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));
+    c->ring_pending = false;
+    ne::SgnsParams sp = sgns_params(c, vsub, c->vslot[c->cur * k + (vsub - home)], epoch, episode, lr);
+    const uint64_t per = 2ull + c->cfg.negatives, total = sp.count * per;
+    if (count) *count = sp.count;
+    if (!out) return NE_OK;
+    if (cap_u32 < total) return fail(c, NE_ERANGE, "capacity %zu < %llu", cap_u32, (unsigned long long)total);
+    if (total == 0) return NE_OK;
+    if (c->tmp_u32_cap < total) {
+        if (c->d_tmp_u32) dfree(c, c->d_tmp_u32);
+        c->d_tmp_u32 = nullptr;
+        c->tmp_u32_cap = 0;
+        NE_TRY(dalloc_t(c, &c->d_tmp_u32, total));
+        c->tmp_u32_cap = total;
+    }
+    NE_CUDA(c, cudaMemsetAsync(c->d_tmp_u32, 0xFF, total * sizeof(uint32_t), c->stream));
+    sp.deterministic = 0;
+    sp.capture = c->d_tmp_u32;
+    NE_CUDA(c, ne::launch_sgns(sp, c->dev, c->stream));
     c->launches += 1;
     NE_CUDA(c, cudaMemcpyAsync(out, c->d_tmp_u32, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     NE_CUDA(c, cudaStreamSynchronize(c->stream));

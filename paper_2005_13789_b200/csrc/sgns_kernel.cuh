@@ -9,20 +9,15 @@
 
 namespace ne {
 
-constexpr int kSgnsThreads = 256;
 
-// G: lanes per sample (16 or 32); a warp trains S = 32/G samples side by side,
-// each lane owning R float4 of every row (d <= 4 G R).  KT: compile-time K
-// (0 = runtime K <= kMaxK).  MINB: min resident CTAs per SM (register budget).
+// G: lanes per sample (8, 16 or 32); a warp trains S = 32/G samples side by
+// side, each lane owning R float4 of every row (d <= 4 G R).  KT: compile-time K
+// (0 = runtime K <= kMaxK).  T, MINB: threads per CTA and min resident CTAs per
+// SM -- the register budget (65536 / (T MINB) per thread) and the granularity
+// at which CTAs fill the register file (launch shapes below).
 // ADD: Hogwild write-back by vector reduction (red.global.add.v4.f32) of each
 // update's delta instead of a plain store of the new row, so concurrent samples
 // sharing a row never erase each other's updates (they only read stale values).
-// PF: the ids of iteration i+1 are known one iteration early (pairs and
-// negatives are fetched two iterations ahead), so at the top of iteration i
-// every lane prefetches ~2 of the 128-byte lines of iteration i+1's rows into
-// L2 (prefetch.global.L2); the next iteration's row loads then hit L2.  A
-// prefetch never changes values (L2 is the point of coherence), so it is valid
-// in deterministic mode too.
 // p.deterministic: only group 0 of the (single) warp works, one sample at a
 // time in canonical order -- the same arithmetic as the production mapping.
 // ACC: NEXT-4 accumulated-gradient rule (all 1+K dots against the pre-sample
@@ -31,9 +26,12 @@ constexpr int kSgnsThreads = 256;
 // BF: rows stored as bfloat16 (NEXT-4, reading D16): loads widen 4 bf16 to a
 // float4, stores round to nearest even, Hogwild deltas go through a bf16x2
 // vector reduction; all arithmetic stays fp32 (RowIO in sgns_common.cuh).
-template <int G, int R, int KT, int MINB, bool ADD, bool PF, bool ACC = false, bool BF = false>
-__global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) {
-    static_assert(!(PF && BF), "L2 prefetch is an fp32-only developer knob");
+// p.capture (test hook, ne_capture_block): every group also writes the ids it
+// trained -- (src, dst, neg_0 .. neg_{K-1}) at capture[pos * (2 + K)] -- so the
+// lane -> sample -> negative routing of the full production grid is checked
+// against the oracle position by position.
+template <int G, int R, int KT, int T, int MINB, bool ADD, bool ACC, bool BF>
+__global__ void __launch_bounds__(T, MINB) sgns_kernel(SgnsParams p) {
     using IO = RowIO<BF>;
     constexpr int S = 32 / G;
     constexpr int KM = KT > 0 ? KT : kMaxK;
@@ -62,12 +60,9 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
     };
 
     uint64_t base = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * spw;
-    uint2 prA, prB = make_uint2(0, 0);
-    NegDraw negA, negB = NegDraw{0u, 0u, make_uint2(0u, 0u)};
+    uint2 prA, prB;
+    NegDraw negA, negB;
     fetch(base, prA, negA);
-    if (PF) fetch(base + stride, prB, negB);
-    const uint32_t lines = p.d >> 5;                 // 128-byte lines per row
-    const uint32_t plines = (2u + (uint32_t)K) * lines;  // per sample
     for (; base < p.count; base += stride) {
         const uint64_t pos = base + h;
         const bool act = h < spw && pos < p.count;
@@ -78,6 +73,11 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
         // a repeated context id inside a sample is rare: detect it once per iteration
         const uint64_t mkey = (act && (int)sub <= K) ? (((uint64_t)h << 33) | my_id) : ((1ull << 32) | lane);
         const bool dup = __any_sync(0xFFFFFFFFu, __popc(__match_any_sync(0xFFFFFFFFu, mkey)) > 1);
+        if (p.capture && act) {
+            uint32_t* cap = p.capture + pos * (2u + (uint32_t)K);
+            if (sub == 0) cap[0] = prA.x;
+            if ((int)sub <= K) cap[1 + sub] = my_id;
+        }
 
         const uint64_t vr = (uint64_t)(prA.x - p.v_begin);
         float4 v[R], v0[(ADD || ACC) ? R : 1], eacc[ACC ? R : 1];
@@ -101,26 +101,7 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
             }
         }
 
-        uint2 prC = make_uint2(0, 0);
-        NegDraw negC = NegDraw{0u, 0u, make_uint2(0u, 0u)};
-        if constexpr (PF) {
-            // L2-prefetch the rows of iteration i+1 (ids known since iteration i-1)
-            const uint64_t nb = base + stride;
-            const bool nact = h < spw && nb + h < p.count;
-            const uint32_t nid = group_id(prB, negB);
-            for (uint32_t L = sub; L < ((plines + G - 1) / G) * G; L += G) {
-                const uint32_t row = L / lines, line = L % lines;
-                const uint32_t rid = __shfl_sync(0xFFFFFFFFu, nid, h * G + (row == 0 ? 0u : row - 1u));
-                if (nact && L < plines) {
-                    const float* a = row == 0 ? p.V + (uint64_t)(prB.x - p.v_begin) * p.d
-                                              : p.C + (uint64_t)(rid - p.c_begin) * p.d;
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a + line * 32));
-                }
-            }
-            fetch(base + 2 * stride, prC, negC);  // ids two iterations ahead
-        } else {
-            fetch(base + stride, prB, negB);     // ids one iteration ahead
-        }
+        fetch(base + stride, prB, negB);  // ids one iteration ahead
 
         // Alg. 1 lines 10 and 12: positive, then the K negatives, in order.
 #pragma unroll
@@ -176,10 +157,6 @@ __global__ void __launch_bounds__(kSgnsThreads, MINB) sgns_kernel(SgnsParams p) 
         }
         prA = prB;
         negA = negB;
-        if constexpr (PF) {
-            prB = prC;
-            negB = negC;
-        }
     }
     if (sub == 0 && loss != 0.0) atomicAdd(p.loss, loss);
 }
@@ -189,27 +166,26 @@ static int env_int(const char* name, int dflt) {
     return e ? std::atoi(e) : dflt;
 }
 
-template <int G, int R, int KT, int MINB, bool BF>
+// One launch shape: T threads per CTA, at least MINB CTAs per SM.
+template <int T_, int MINB_>
+struct Shape {
+    static constexpr int T = T_, MINB = MINB_;
+};
+
+template <int G, int R, int KT, class SH, bool BF>
 static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStream_t s) {
-    // developer knob: L2 row prefetch (measured: no gain; fp32 rows only)
-    static const bool pf_knob = env_int("NE_SGNS_PF", 0) != 0;
-    const bool pf = pf_knob && !BF;
-    constexpr bool PFB = !BF;  // the prefetch instantiations exist for fp32 rows only
+    constexpr int T = SH::T, MB = SH::MINB;
     if (p.deterministic) {  // one warp, one sample at a time, canonical order, plain stores
-        if (p.accumulate) sgns_kernel<G, R, KT, MINB, false, false, true, BF><<<1, 32, 0, s>>>(p);
-        else if (pf) sgns_kernel<G, R, KT, MINB, false, PFB, false, BF><<<1, 32, 0, s>>>(p);
-        else sgns_kernel<G, R, KT, MINB, false, false, false, BF><<<1, 32, 0, s>>>(p);
+        if (p.accumulate) sgns_kernel<G, R, KT, T, MB, false, true, BF><<<1, 32, 0, s>>>(p);
+        else sgns_kernel<G, R, KT, T, MB, false, false, BF><<<1, 32, 0, s>>>(p);
         return cudaGetLastError();
     }
-    auto kern = p.accumulate
-                    ? (p.atomic_writeback ? sgns_kernel<G, R, KT, MINB, true, false, true, BF>
-                                          : sgns_kernel<G, R, KT, MINB, false, false, true, BF>)
-                : p.atomic_writeback ? (pf ? sgns_kernel<G, R, KT, MINB, true, PFB, false, BF>
-                                           : sgns_kernel<G, R, KT, MINB, true, false, false, BF>)
-                                     : (pf ? sgns_kernel<G, R, KT, MINB, false, PFB, false, BF>
-                                           : sgns_kernel<G, R, KT, MINB, false, false, false, BF>);
+    auto kern = p.accumulate ? (p.atomic_writeback ? sgns_kernel<G, R, KT, T, MB, true, true, BF>
+                                                   : sgns_kernel<G, R, KT, T, MB, false, true, BF>)
+                             : (p.atomic_writeback ? sgns_kernel<G, R, KT, T, MB, true, false, BF>
+                                                   : sgns_kernel<G, R, KT, T, MB, false, false, BF>);
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSgnsThreads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, 0);
     if (e != cudaSuccess) return e;
     per_sm = std::max(per_sm, 1);
     constexpr int S = 32 / G;
@@ -223,40 +199,39 @@ static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStr
     }
     const uint64_t warps = want / S;
     const uint64_t full = (uint64_t)std::max(1, dev.sm_count - p.reserve_sms) * per_sm;
-    const int wpb = kSgnsThreads / 32;
+    constexpr int wpb = T / 32;
     if (warps >= full * wpb) {
-        kern<<<(unsigned)full, kSgnsThreads, 0, s>>>(p);
+        kern<<<(unsigned)full, T, 0, s>>>(p);
     } else if (warps >= (uint64_t)dev.sm_count * wpb) {
-        kern<<<(unsigned)((warps + wpb - 1) / wpb), kSgnsThreads, 0, s>>>(p);
+        kern<<<(unsigned)((warps + wpb - 1) / wpb), T, 0, s>>>(p);
     } else {  // small capped grids: spread single warps over the SMs
         kern<<<(unsigned)warps, 32, 0, s>>>(p);
     }
     return cudaGetLastError();
 }
 
-// Occupancy variant (developer knob NE_SGNS_MINB = 2..3): the register budget
-// __launch_bounds__(256, MINB) gives the compiler.  Defaults: 16-lane groups
-// carry two samples' rows per lane (MINB 2); 32-lane groups MINB 3.
-
+// Launch shapes (measured; registers per thread from -Xptxas -v):
+//  * 16 lanes x 2 float4 (d <= 128) and 32 lanes x 2 (d <= 256): 256 threads,
+//    2 CTAs/SM -> <= 128 registers, 16 warps/SM, spill-free;
+//  * 8 lanes x 3 float4 (64 < d <= 96, K = 5): ~187 registers unconstrained;
+//    with 256-thread CTAs only one CTA fits (8 warps, a quarter of the register
+//    file idle), 64-thread CTAs pack 10 warps per SM with no spills (knob
+//    NE_SGNS_G8SHAPE: 0 = 64 x 5, 1 = 128 x 3 (<= 168 registers), 2 = 256 x 1);
+//  * 32 lanes x 3-4 float4 (d > 256): 200-245 registers, 64-thread CTAs.
 template <int G, int R, int KT, bool BF>
 static cudaError_t launch_sgns_k(const SgnsParams& p, const Device& dev, cudaStream_t s) {
-    if constexpr (R > 2 && G == 32) {  // wide rows (d > 256): the register file holds 2+K rows of up to 2 KB
-        return launch_sgns_v<G, R, KT, 1, BF>(p, dev, s);
-    }
-    static const int knob = env_int("NE_SGNS_MINB", 0);
-    // 16-lane groups hold two samples' rows per lane, 32-lane groups with R = 2
-    // (d <= 256) hold 2 float4 per row: both need the 128-register budget of 2 CTAs
-    // defaults (measured): 8-lane groups 1 CTA/SM (974 vs 841 M/s at 2 with spills,
-    // C4); 16-lane groups and 32-lane R = 2 need 128 registers (2 CTAs); else 3
-    int minb = knob >= 1 && knob <= 4 ? knob : (G == 8 ? 1 : (G == 16 || R == 2 ? 2 : 3));
-    if (KT == 0) minb = std::min(minb, 2);  // runtime K keeps kMaxK+1 rows live: stay spill-free
-    // (the knob's other budgets were measured and dropped: 1 and 4 CTAs/SM lose,
-    // except for 8-lane groups, whose 3 float4 per row fit 1 CTA/SM spill-free)
     if constexpr (G == 8) {
-        if (minb <= 1) return launch_sgns_v<G, R, KT, 1, BF>(p, dev, s);
+        static const int shape = env_int("NE_SGNS_G8SHAPE", 0);
+        if constexpr (!BF) {
+            if (shape == 1) return launch_sgns_v<G, R, KT, Shape<128, 3>, BF>(p, dev, s);
+            if (shape == 2) return launch_sgns_v<G, R, KT, Shape<256, 1>, BF>(p, dev, s);
+        }
+        return launch_sgns_v<G, R, KT, Shape<64, 5>, BF>(p, dev, s);
+    } else if constexpr (R > 2) {
+        return launch_sgns_v<G, R, KT, Shape<64, 1>, BF>(p, dev, s);
+    } else {
+        return launch_sgns_v<G, R, KT, Shape<256, 2>, BF>(p, dev, s);
     }
-    if (minb <= 2) return launch_sgns_v<G, R, KT, 2, BF>(p, dev, s);
-    return launch_sgns_v<G, R, KT, 3, BF>(p, dev, s);
 }
 
 template <int G, int R, bool BF>
@@ -269,19 +244,14 @@ static cudaError_t launch_sgns_r(const SgnsParams& p, const Device& dev, cudaStr
 template <bool BF>
 cudaError_t launch_sgns_rows(const SgnsParams& p, const Device& dev, cudaStream_t s) {
     const uint32_t q = p.d / 4;
-    // d <= 128: 16 lanes x 2 float4 (two samples per warp; developer knob
-    // NE_SGNS_LANES=32 selects one sample per warp); d > 128: 32 lanes x R.
-    static const int lanes = env_int("NE_SGNS_LANES", 16);
     // 64 < d <= 96 at K = 5: 8-lane groups x 3 float4, four samples per warp, so
     // a 384-byte row uses every lane (16-lane groups leave a quarter idle)
-    if (q > 16 && q <= 24 && p.K == 5 && lanes != 32 && env_int("NE_SGNS_G8", 1))
-        return launch_sgns_k<8, 3, 5, BF>(p, dev, s);
-    if (q <= 32 && lanes == 16) {
-        if (q <= 16) return launch_sgns_r<16, 1, BF>(p, dev, s);
-        return launch_sgns_r<16, 2, BF>(p, dev, s);
-    }
-    switch ((q + 31) / 32) {
-        case 1: return launch_sgns_r<32, 1, BF>(p, dev, s);
+    if (q > 16 && q <= 24 && p.K == 5) return launch_sgns_k<8, 3, 5, BF>(p, dev, s);
+    // d <= 128: 16 lanes x 1-2 float4, two samples per warp (measured against
+    // 32 lanes x 1 float4, one sample per warp: 1093 vs 1003 M samples/s on C3)
+    if (q <= 16) return launch_sgns_r<16, 1, BF>(p, dev, s);
+    if (q <= 32) return launch_sgns_r<16, 2, BF>(p, dev, s);
+    switch ((q + 31) / 32) {  // d > 128: 32 lanes x R float4
         case 2: return launch_sgns_r<32, 2, BF>(p, dev, s);
         case 3: return launch_sgns_r<32, 3, BF>(p, dev, s);
         default: return launch_sgns_r<32, 4, BF>(p, dev, s);

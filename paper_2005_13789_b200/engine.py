@@ -61,12 +61,21 @@ class Engine:
         ne.ne_export_negatives(self.ctx, epoch, episode, vsub, pos_begin, count, out)
         return out[:count]
 
+    def capture_block(self, epoch: int, episode: int, vsub: int, lr: float) -> np.ndarray:
+        cnt = ne.ne_capture_block(self.ctx, epoch, episode, vsub, lr, None)
+        out = np.zeros((max(cnt, 1), 2 + self.cfg.negatives), np.uint32)
+        ne.ne_capture_block(self.ctx, epoch, episode, vsub, lr, out)
+        return out[:cnt]
+
     # ---- training
     def train_samples(self, epoch: int, episode: int, lr: float) -> dict:
         return ne.ne_train_samples(self.ctx, epoch, episode, lr).as_dict()
 
     def train_epoch(self, epoch: int, lr: float, reuse: bool = False) -> dict:
         return ne.ne_train_epoch(self.ctx, epoch, lr, ne.NE_REUSE_SAMPLES if reuse else 0).as_dict()
+
+    def join(self) -> None:
+        ne.ne_join(self.ctx)
 
     # ---- embeddings
     def embeddings(self, which: int = ne.NE_VERTEX, rows: tuple[int, int] | None = None) -> np.ndarray:

@@ -29,6 +29,7 @@ NE_WB_ATOMIC_DELTA, NE_WB_STORE = 0, 1
 NE_UPDATE_SEQUENTIAL, NE_UPDATE_ACCUMULATED = 0, 1
 NE_STAGE_DEVICE, NE_STAGE_HOST = 0, 1
 NE_STORE_F32, NE_STORE_BF16 = 0, 1
+NE_STREAM_OWN = (1 << 64) - 1  # ne.h: ((void *)~(uintptr_t)0), the context's own stream
 
 
 class ne_config(C.Structure):
@@ -57,6 +58,7 @@ _sig = {
     "ne_version": (C.c_int, []),
     "ne_create": (C.c_int, [C.POINTER(_P), C.POINTER(ne_config), C.c_int, ALLOC_FN, FREE_FN, _P]),
     "ne_set_stream": (C.c_int, [_P, _P]),
+    "ne_join": (C.c_int, [_P]),
     "ne_get_nccl_id": (C.c_int, [_P]),
     "ne_init_dist": (C.c_int, [_P, C.c_int, C.c_int, _P]),
     "ne_load_graph": (C.c_int, [_P, C.c_uint32, C.c_uint64, _P, _P]),
@@ -71,6 +73,8 @@ _sig = {
     "ne_check_pool": (C.c_int, [_P]),
     "ne_export_samples": (C.c_int, [_P, C.c_uint32, _P, C.c_size_t, C.POINTER(C.c_uint64)]),
     "ne_export_negatives": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, _P]),
+    "ne_capture_block": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float, _P, C.c_size_t,
+                                   C.POINTER(C.c_uint64)]),
     "ne_train_samples_local_ring": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
                                              C.POINTER(ne_stats)]),
     "ne_plan_vsub": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
@@ -95,14 +99,23 @@ def _check(ctx, rc: int) -> None:
         raise NEError(rc, _lib.ne_last_error(ctx).decode())
 
 
-def _ptr(a) -> int:
-    """Address of a numpy array or torch tensor (host or device)."""
+def _ptr(a, itemsize: int | None = None, what: str = "array") -> int:
+    """Address of a C-contiguous numpy array or torch tensor (host or device);
+    with `itemsize`, the element size the C side reads (a wrong one would make
+    it read past the end of the buffer)."""
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        assert a.flags.c_contiguous
+        if not a.flags.c_contiguous:
+            raise ValueError(f"{what} must be C-contiguous")
+        if itemsize is not None and a.itemsize != itemsize:
+            raise TypeError(f"{what} has {a.itemsize}-byte elements, the ABI reads {itemsize}-byte ones")
         return a.ctypes.data
-    return a.data_ptr()  # torch.Tensor
+    if not a.is_contiguous():  # torch.Tensor
+        raise ValueError(f"{what} must be contiguous")
+    if itemsize is not None and a.element_size() != itemsize:
+        raise TypeError(f"{what} has {a.element_size()}-byte elements, the ABI reads {itemsize}-byte ones")
+    return a.data_ptr()
 
 
 # ---------------------------------------------------------------- ABI, same names
@@ -119,7 +132,13 @@ def ne_create(cfg: ne_config, device: int, alloc=None, free_fn=None):
 
 
 def ne_set_stream(ctx, stream: int | None) -> None:
+    """stream: a cudaStream_t handle (0 = the legacy default stream, torch's
+    default stream) or NE_STREAM_OWN."""
     _check(ctx, _lib.ne_set_stream(ctx, stream))
+
+
+def ne_join(ctx) -> None:
+    _check(ctx, _lib.ne_join(ctx))
 
 
 def ne_get_nccl_id() -> bytes:
@@ -138,13 +157,14 @@ def ne_init_dist(ctx, rank: int, world: int, nccl_id: bytes | None) -> None:
 def ne_load_graph(ctx, offsets, targets) -> None:
     n = len(offsets) - 1
     nnz = len(targets)
-    _check(ctx, _lib.ne_load_graph(ctx, n, nnz, _ptr(offsets), _ptr(targets) if nnz else None))
+    _check(ctx, _lib.ne_load_graph(ctx, n, nnz, _ptr(offsets, 8, "offsets (u64)"),
+                                   _ptr(targets, 4, "targets (u32)") if nnz else None))
 
 
 def ne_random_walk(ctx, epoch: int, episode: int, host_walks: np.ndarray | None = None) -> int:
     cnt = C.c_uint64()
     cap = host_walks.size if host_walks is not None else 0
-    _check(ctx, _lib.ne_random_walk(ctx, epoch, episode, _ptr(host_walks), cap, C.byref(cnt)))
+    _check(ctx, _lib.ne_random_walk(ctx, epoch, episode, _ptr(host_walks, 4, "host_walks"), cap, C.byref(cnt)))
     return int(cnt.value)
 
 
@@ -168,11 +188,11 @@ def ne_train_epoch(ctx, epoch: int, lr: float, flags: int = 0) -> ne_stats:
 
 def ne_get_embeddings(ctx, which: int, row_begin: int, row_end: int, out) -> None:
     cap = out.numel() if hasattr(out, "numel") else out.size
-    _check(ctx, _lib.ne_get_embeddings(ctx, which, row_begin, row_end, _ptr(out), cap))
+    _check(ctx, _lib.ne_get_embeddings(ctx, which, row_begin, row_end, _ptr(out, 4, "out (f32)"), cap))
 
 
 def ne_set_embeddings(ctx, which: int, row_begin: int, row_end: int, data) -> None:
-    _check(ctx, _lib.ne_set_embeddings(ctx, which, row_begin, row_end, _ptr(data)))
+    _check(ctx, _lib.ne_set_embeddings(ctx, which, row_begin, row_end, _ptr(data, 4, "data (f32)")))
 
 
 def ne_last_error(ctx) -> str:
@@ -190,13 +210,23 @@ def ne_check_pool(ctx) -> None:
 def ne_export_samples(ctx, vsub: int, out: np.ndarray | None = None) -> int:
     cnt = C.c_uint64()
     cap = out.size // 2 if out is not None else 0
-    _check(ctx, _lib.ne_export_samples(ctx, vsub, _ptr(out), cap, C.byref(cnt)))
+    _check(ctx, _lib.ne_export_samples(ctx, vsub, _ptr(out, 4, "out (u32 pairs)"), cap, C.byref(cnt)))
     return int(cnt.value)
 
 
 def ne_export_negatives(ctx, epoch: int, episode: int, vsub: int, pos_begin: int, count: int,
                         out: np.ndarray) -> None:
-    _check(ctx, _lib.ne_export_negatives(ctx, epoch, episode, vsub, pos_begin, count, _ptr(out)))
+    _check(ctx, _lib.ne_export_negatives(ctx, epoch, episode, vsub, pos_begin, count, _ptr(out, 4, "out (u32)")))
+
+
+def ne_capture_block(ctx, epoch: int, episode: int, vsub: int, lr: float, out: np.ndarray | None = None) -> int:
+    """Test hook: production-kernel training of one home block, recording
+    (src, dst, negatives) per position into out ([count, 2+K] u32)."""
+    cnt = C.c_uint64()
+    cap = out.size if out is not None else 0
+    _check(ctx, _lib.ne_capture_block(ctx, epoch, episode, vsub, lr, _ptr(out, 4, "out (u32)"), cap,
+                                      C.byref(cnt)))
+    return int(cnt.value)
 
 
 def ne_train_samples_local_ring(ctxs, epoch: int, episode: int, lr: float) -> ne_stats:

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     for name in names:
         assert hasattr(lib, name), name
     assert set(names) == set(ne.EXPORTED)
-    assert ne.ne_version() == 1
+    assert ne.ne_version() == 2
 
 
 def test_host_plan_matches_oracle_plan(orc):

@@ -570,3 +570,137 @@ def test_host_staged_set_get_and_hogwild():
     V2 = eng.embeddings(0)
     assert np.isfinite(V2).all() and not np.array_equal(V2, V)
     eng.close()
+
+
+# ---------------------------------------------------------------- production grid, position by position
+def _matching(n):
+    u = np.arange(0, n, 2, dtype=np.int64)
+    return synth.csr_from_undirected(n, u, u + 1)
+
+
+@pytest.mark.parametrize("dim,vsub", [(128, 1), (96, 2)])
+def test_capture_ids_full_grid_c2(dim, vsub):
+    """The production kernel at its full grid on C2 (d = 128: 16-lane groups,
+    2 samples per warp; d = 96: 8-lane groups, 4 samples per warp) records the
+    (src, dst, negatives) every group trained; every position must equal the
+    pool and the oracle's negatives -- the lane -> sample -> negative routing
+    of all S groups of a warp, checked at every position of the block."""
+    off, tgt = synth.workload_graph("c2")
+    n = len(off) - 1
+    eng = engine(dim=dim, deterministic=False)
+    eng.load_graph(off, tgt)
+    eng.random_walk(0, 0)
+    eng.build_samples(0, 0)
+    pool = eng.export_samples(vsub)
+    cap = eng.capture_block(0, 0, vsub, 0.025)
+    assert cap.shape == (len(pool), 7) and len(pool) > 10_000_000
+    assert np.array_equal(cap[:, :2], pool)
+    cfg = ocfg(dim=dim)
+    thr, al = oracle.build_alias_tables(cfg, off)
+    ref = oracle.negatives_range(cfg, thr, al, 0, n, 0, 0, vsub, 0, len(pool))
+    bad = np.flatnonzero((cap[:, 2:] != ref).any(1))
+    assert len(bad) == 0, (len(bad), bad[:5], cap[bad[:3]], ref[bad[:3]])
+    assert np.isfinite(eng.embeddings(0)).all()
+    eng.close()
+
+
+def test_capture_ids_layout_ranks_c1():
+    """Capture at P = 4 (layout-only ranks): block ids vsub * P + rank in the
+    negative counter, context-part alias tables."""
+    off, tgt = synth.workload_graph("c1")
+    n = len(off) - 1
+    P = 4
+    cfg = ocfg(parts=P)
+    thr, al = oracle.build_alias_tables(cfg, off)
+    pb = oracle.partition_bounds(0, n, P).astype(np.int64)
+    for g in (0, 3):
+        eng = engine(rank=g, world=P, deterministic=False)
+        eng.load_graph(off, tgt)
+        eng.random_walk(1, 0)
+        eng.build_samples(1, 0)
+        vs = g * 4 + 1
+        pool = eng.export_samples(vs)
+        cap = eng.capture_block(1, 0, vs, 0.025)
+        assert np.array_equal(cap[:, :2], pool)
+        ref = oracle.negatives_range(cfg, thr, al, int(pb[g]), int(pb[g + 1] - pb[g]), 1, 0, vs * P + g, 0, len(pool))
+        assert np.array_equal(cap[:, 2:], ref)
+        eng.close()
+
+
+@pytest.mark.parametrize("dim", [64, 128, 256])
+def test_hogwild_full_grid_conflict_free_elementwise(dim):
+    """A perfect matching with walk_len = window = 1 and K = 0: every vertex row
+    and every context row is touched by exactly one sample, so the production
+    (Hogwild, atomic-delta) kernel at its full grid has no conflicts and must
+    equal the oracle element by element (fp32 arithmetic vs the fp64 oracle)."""
+    n = 1 << 21
+    off, tgt = _matching(n)
+    kw = dict(dim=dim, negatives=0, walk_len=1, window=1)
+    eng = engine(deterministic=False, **kw)
+    eng.load_graph(off, tgt)
+    st = eng.train_epoch(0, 0.025)
+    assert st["samples"] == n
+    V = oracle.init_vertex(n, dim, 42)
+    Cm = np.zeros_like(V)
+    ns, loss = oracle.train_epoch(ocfg(**kw), off, tgt, V, Cm, 0, 0.025)
+    assert ns == n and abs(st["loss_sum"] - loss) <= 1e-5 * loss
+    dv = np.abs(eng.embeddings(0) - V).max()
+    dc = np.abs(eng.embeddings(1) - Cm).max()
+    eng.close()
+    assert dv <= 1e-6 and dc <= 1e-6, (dv, dc)
+
+
+@pytest.mark.parametrize("deterministic", [True, False])
+def test_sigmoid_clamp_in_kernel(deterministic):
+    """The kernel's +-30 clamp (reading D11; tests/golden/sigma_clamp.txt): with
+    lr = 0 the rows stay put and the loss of a positive sample with v.c = -40
+    is log(1 + e^30) = 30 (no clamp: 40; a +-6 clamp: 6.0025), with v.c = -25
+    it is 25."""
+    from conftest import golden_kv
+    g = golden_kv("sigma_clamp.txt")
+    n, d = 4096, 8
+    off, tgt = _matching(n)
+    for dot, key in ((-40.0, "loss_pos_at_minus_40"), (-25.0, "loss_pos_at_minus_25")):
+        eng = engine(dim=d, negatives=0, walk_len=1, window=1, deterministic=deterministic, subparts=1)
+        eng.load_graph(off, tgt)
+        eng.set_embeddings(0, 0, np.full((n, d), dot / d / -2.0, np.float32))
+        eng.set_embeddings(1, 0, np.full((n, d), -2.0, np.float32))
+        st = eng.train_epoch(0, 0.0)
+        eng.close()
+        assert st["samples"] == n
+        assert abs(st["loss_sum"] / n - float(g[key])) <= 1e-4, (dot, st["loss_sum"] / n)
+
+
+def test_c2_walks_and_pools_match_oracle_hashes():
+    """C2 at full size (SURVEY 8(c) gate "walks and samples bit-exact on C2"):
+    every walk and every 2D block of the pool at P = 1 and at P = 4
+    (layout-only ranks), against SHA-256 hashes the oracle wrote
+    (tests/golden/c2_hashes.txt, tools/make_golden_c2.py -- oracle only)."""
+    import hashlib
+    from conftest import golden_lines
+    want_walk, want_blocks = None, {}
+    for ln in golden_lines("c2_hashes.txt"):
+        f = ln.split()
+        if f[0] == "walks":
+            want_walk = (int(f[1]), f[2])
+        else:
+            want_blocks[(int(f[1]), int(f[2]), int(f[3]))] = (int(f[4]), f[5])
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    off, tgt = synth.workload_graph("c2")
+    n = len(off) - 1
+    eng = engine(deterministic=False)
+    eng.load_graph(off, tgt)
+    walks = eng.random_walk(0, 0, export=True)
+    assert (len(walks), sha(walks)) == want_walk
+    del walks
+    eng.close()
+    for P in (1, 4):
+        for g in range(P):
+            eng = engine(deterministic=False, rank=g, world=P)
+            eng.load_graph(off, tgt)
+            eng.random_walk(3, 0)
+            eng.build_samples(3, 0)
+            for vs in range(P * 4):
+                blk = eng.export_samples(vs)
+                assert (len(blk), sha(blk)) == want_blocks[(P, g, vs)], (P, g, vs)
+            eng.close()

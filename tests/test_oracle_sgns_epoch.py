@@ -29,6 +29,28 @@ def test_sigmoid_examples_and_clamp(orc):
     assert 0.0 < orc.sigmoid(-1e9) < orc.sigmoid(1e9) < 1.0
 
 
+def test_sigmoid_clamp_closed_form(orc):
+    """The +-30 clamp (reading D11) pinned by closed-form values: sigma(10) and
+    sigma(-10) unclamped, sigma strictly increasing up to 30 and constant beyond,
+    and the loss of one update (lr = 0, so rows stay put) at |v.c| = 25 and 40."""
+    g = golden_kv("sigma_clamp.txt")
+    assert abs(orc.sigmoid(10.0) - float(g["sigma_10"])) <= 1e-16
+    assert abs(orc.sigmoid(-10.0) - float(g["sigma_minus_10"])) <= 1e-20
+    b = float(g["clamp"])
+    assert orc.sigmoid(b - 1) < orc.sigmoid(b - 0.5) < orc.sigmoid(b)
+    assert orc.sigmoid(-b) < orc.sigmoid(-b + 0.5) < orc.sigmoid(-b + 1)
+    assert orc.sigmoid(b + 1) == orc.sigmoid(b) == orc.sigmoid(1e6)
+    assert orc.sigmoid(-b - 1) == orc.sigmoid(-b) == orc.sigmoid(-1e6)
+    # -log(1 - s) at s = sigma(30) = 1 - 9.4e-14 loses ~1e-3 of 1 - s to cancellation
+    # (eps / 9.4e-14); a +-6 clamp would give 6.0025 and no clamp 40
+    for x, label, key, tol in ((-25.0, 1, "loss_pos_at_minus_25", 1e-12), (-40.0, 1, "loss_pos_at_minus_40", 1e-12),
+                               (40.0, 0, "loss_neg_at_40", 2e-3)):
+        v = np.array([x / 4] * 4, np.float32)
+        c = np.ones(4, np.float32)
+        loss = orc.sgns_step(v, c, label, 0.0)
+        assert abs(loss - float(g[key])) <= tol, (x, label, loss)
+
+
 def test_worked_update(orc):
     g = golden_kv("sgns_worked_example.txt")
     tol = float(g["tolerance"])
