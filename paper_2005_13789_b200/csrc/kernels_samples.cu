@@ -231,6 +231,181 @@ cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, c
     return cudaGetLastError();
 }
 
+// ---- sharded construction at P > 1: O(N/P) work per rank ----------------------
+// A rank walks only its shard of the episode's walkers and generates ALL their
+// pairs; pairs travel to the rank owning their context part (the exchange in
+// runtime.cpp).  Per walker w of the shard and part g: counts[g * units + w] =
+// the walk's pairs whose context node lies in part g; one exclusive scan over
+// the whole [P][units] array then gives every (part, walker) its offset in a
+// send buffer grouped by part, generation order inside each part -- exactly the
+// order that makes the receiver's part-local index x = base(shard, part) +
+// position (O6).  P <= 32 (one lane per part).
+constexpr uint32_t kMaxShardParts = 32;
+
+__global__ void __launch_bounds__(kThreads) count_parts_kernel(const uint32_t* __restrict__ walks,
+                                                               const uint32_t* __restrict__ slot_tab,
+                                                               PoolParams p, const uint64_t* __restrict__ part_bounds,
+                                                               uint32_t P, uint32_t* __restrict__ counts) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t* sb = reinterpret_cast<uint64_t*>(smem_raw);                        // P + 1 bounds
+    uint32_t* wcnt = reinterpret_cast<uint32_t*>(sb + kMaxShardParts + 1);       // [warp][P]
+    uint32_t* paths = wcnt + kWarps * kMaxShardParts;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint32_t plen = p.k + 1;
+    for (uint32_t i = threadIdx.x; i <= P; i += kThreads) sb[i] = part_bounds[i];
+    __syncthreads();
+    uint32_t* my = paths + warp * 2 * plen;
+    uint32_t* cnt = wcnt + warp * kMaxShardParts;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t buf = 0;
+    stage_walk(my, walks, w, p.units, plen, lane);
+    for (; w < p.units; w += nwarps) {
+        cp_async_wait_all();
+        if (lane < P) cnt[lane] = 0;
+        __syncwarp();
+        const uint32_t* path = my + buf * plen;
+        stage_walk(my + (buf ^ 1) * plen, walks, w + nwarps, p.units, plen, lane);
+        for (uint32_t s0 = 0; s0 < p.Pw; s0 += 32) {
+            const uint32_t s = s0 + lane;
+            uint32_t pg = 0xFFFFFFFFu;
+            if (s < p.Pw) {
+                const uint32_t t = __ldg(slot_tab + s);
+                const uint32_t b = path[(t >> 16) + (t & 0xFFFFu)];
+                if (b != kSentinel) pg = range_of(sb, P, b);
+            }
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, pg);
+            if (pg != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) cnt[pg] += __popc(peers);
+            __syncwarp();
+        }
+        if (lane < P) counts[(uint64_t)lane * p.units + w] = cnt[lane];
+        buf ^= 1;
+        __syncwarp();
+    }
+    cp_async_wait_all();
+}
+
+// Pairs of the shard into the part-grouped send buffer: pair (path[i],
+// path[i+delta]) of walker w goes to out[base[g * units + w] + its rank among
+// the walk's part-g pairs in generation order], g = part of the context node.
+__global__ void __launch_bounds__(kThreads) pairs_parts_kernel(const uint32_t* __restrict__ walks,
+                                                               const uint32_t* __restrict__ slot_tab,
+                                                               PoolParams p, const uint64_t* __restrict__ part_bounds,
+                                                               uint32_t P, const uint64_t* __restrict__ base,
+                                                               uint64_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t* sb = reinterpret_cast<uint64_t*>(smem_raw);                 // P + 1 bounds
+    uint64_t* wcur = sb + kMaxShardParts + 1;                             // [warp][P] cursors
+    uint32_t* paths = reinterpret_cast<uint32_t*>(wcur + kWarps * kMaxShardParts);
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t plen = p.k + 1;
+    for (uint32_t i = threadIdx.x; i <= P; i += kThreads) sb[i] = part_bounds[i];
+    __syncthreads();
+    uint32_t* my = paths + warp * 2 * plen;
+    uint64_t* cur = wcur + warp * kMaxShardParts;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    uint32_t buf = 0;
+    stage_walk(my, walks, w, p.units, plen, lane);
+    for (; w < p.units; w += nwarps) {
+        cp_async_wait_all();
+        if (lane < P) cur[lane] = __ldg(base + (uint64_t)lane * p.units + w);
+        __syncwarp();
+        const uint32_t* path = my + buf * plen;
+        stage_walk(my + (buf ^ 1) * plen, walks, w + nwarps, p.units, plen, lane);
+        for (uint32_t s0 = 0; s0 < p.Pw; s0 += 32) {
+            const uint32_t s = s0 + lane;
+            uint32_t pg = 0xFFFFFFFFu, a = 0, b = 0;
+            if (s < p.Pw) {
+                const uint32_t t = __ldg(slot_tab + s);
+                const uint32_t i = t >> 16;
+                b = path[i + (t & 0xFFFFu)];
+                a = path[i];
+                if (b != kSentinel) pg = range_of(sb, P, b);
+            }
+            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, pg);
+            if (pg != 0xFFFFFFFFu) out[cur[pg] + __popc(peers & lt)] = (uint64_t)a | ((uint64_t)b << 32);
+            __syncwarp();
+            if (pg != 0xFFFFFFFFu && lane == (uint32_t)(__ffs(peers) - 1)) cur[pg] += __popc(peers);
+            __syncwarp();
+        }
+        buf ^= 1;
+        __syncwarp();
+    }
+    cp_async_wait_all();
+}
+
+static size_t shard_smem(uint32_t k, size_t cursor_bytes) {
+    return (kMaxShardParts + 1) * sizeof(uint64_t) + (size_t)kWarps * kMaxShardParts * cursor_bytes +
+           (size_t)kWarps * 2 * (k + 1) * sizeof(uint32_t);
+}
+
+cudaError_t launch_count_parts(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
+                               const uint64_t* part_bounds, uint32_t P, uint32_t* counts, const Device& dev,
+                               cudaStream_t s) {
+    if (P == 0 || P > kMaxShardParts) return cudaErrorInvalidValue;
+    if (p.units == 0) return cudaSuccess;
+    count_parts_kernel<<<grid_cap(ceil_div(p.units, kWarps), dev, 8), kThreads, shard_smem(p.k, 4), s>>>(
+        walks, slot_tab, p, part_bounds, P, counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pairs_parts(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
+                               const uint64_t* part_bounds, uint32_t P, const uint64_t* base, uint64_t* out,
+                               const Device& dev, cudaStream_t s) {
+    if (P == 0 || P > kMaxShardParts) return cudaErrorInvalidValue;
+    if (p.units == 0) return cudaSuccess;
+    pairs_parts_kernel<<<grid_cap(ceil_div(p.units, kWarps), dev, 8), kThreads, shard_smem(p.k, 8), s>>>(
+        walks, slot_tab, p, part_bounds, P, base, out);
+    return cudaGetLastError();
+}
+
+// O6 keys of a part's pool gathered in generation order: key[x] = pi_g(x).
+__global__ void __launch_bounds__(kThreads) feistel_keys_kernel(Feistel f, uint64_t N, uint32_t* __restrict__ key) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < N; x += stride) key[x] = (uint32_t)f(x);
+}
+
+cudaError_t launch_feistel_keys(const PoolParams& p, uint32_t* key, const Device& dev, cudaStream_t s) {
+    if (p.N == 0) return cudaSuccess;
+    feistel_keys_kernel<<<grid_cap(ceil_div(p.N, kThreads), dev, 8), kThreads, 0, s>>>(make_feistel(p), p.N, key);
+    return cudaGetLastError();
+}
+
+// tot[g] = pairs of the shard in part g, from the scanned [P][units] counts.
+__global__ void part_totals_kernel(const uint64_t* __restrict__ base, uint64_t units, uint32_t P,
+                                   const uint64_t* __restrict__ total, uint64_t* __restrict__ tot) {
+    const uint32_t g = threadIdx.x;
+    if (g >= P) return;
+    if (units == 0) { tot[g] = 0; return; }
+    const uint64_t e = g + 1 < P ? base[(uint64_t)(g + 1) * units] : *total;
+    tot[g] = e - base[(uint64_t)g * units];
+}
+
+cudaError_t launch_part_totals(const uint64_t* base, uint64_t units, uint32_t P, const uint64_t* total,
+                               uint64_t* tot, cudaStream_t s) {
+    if (P == 0 || P > kMaxShardParts) return cudaErrorInvalidValue;
+    part_totals_kernel<<<1, 32, 0, s>>>(base, units, P, total, tot);
+    return cudaGetLastError();
+}
+
+// Direct sink for a pool gathered in generation order: out[pi(x)] = in[x].
+__global__ void __launch_bounds__(kThreads) feistel_scatter_kernel(Feistel f, uint64_t N,
+                                                                   const uint64_t* __restrict__ in,
+                                                                   uint64_t* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < N; x += stride) out[f(x)] = in[x];
+}
+
+cudaError_t launch_feistel_scatter(const PoolParams& p, const uint64_t* in, uint64_t* out, const Device& dev,
+                                   cudaStream_t s) {
+    if (p.N == 0) return cudaSuccess;
+    feistel_scatter_kernel<<<grid_cap(ceil_div(p.N, kThreads), dev, 8), kThreads, 0, s>>>(make_feistel(p), p.N,
+                                                                                           in, out);
+    return cudaGetLastError();
+}
+
 // LINE mode: the pool is the CSR edge list; unit = edge id.
 __global__ void __launch_bounds__(kThreads) pairs_line_kernel(const uint64_t* __restrict__ off,
                                                               const uint32_t* __restrict__ tgt,

@@ -78,6 +78,26 @@ cudaError_t launch_pairs_walk(const uint32_t* walks, const uint32_t* slot_tab, c
 cudaError_t launch_pairs_line(const uint64_t* off, const uint32_t* tgt, uint64_t n,
                               const PoolParams& p, const uint64_t* base, const PoolSink& sink,
                               const Device& dev, cudaStream_t s);
+// Sharded construction at P > 1 (walkers sharded over the ranks, O(N/P) per
+// rank): p.units = this shard's walkers (walks[units][k+1]); part_bounds =
+// device copy of the P + 1 context-part bounds, P <= 32.
+// counts[g * units + w] = pairs of walker w whose context node is in part g.
+cudaError_t launch_count_parts(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
+                               const uint64_t* part_bounds, uint32_t P, uint32_t* counts, const Device& dev,
+                               cudaStream_t s);
+// Every pair of the shard to out[base[g * units + w] + rank within (w, g)]
+// (base = exclusive scan of counts): the send buffer, grouped by part.
+cudaError_t launch_pairs_parts(const uint32_t* walks, const uint32_t* slot_tab, const PoolParams& p,
+                               const uint64_t* part_bounds, uint32_t P, const uint64_t* base, uint64_t* out,
+                               const Device& dev, cudaStream_t s);
+// tot[g] (device, P values) = the shard's pairs in part g (from base / total).
+cudaError_t launch_part_totals(const uint64_t* base, uint64_t units, uint32_t P, const uint64_t* total,
+                               uint64_t* tot, cudaStream_t s);
+// out[pi(x)] = in[x] for x in [0, p.N): the direct sink of a gathered pool.
+cudaError_t launch_feistel_scatter(const PoolParams& p, const uint64_t* in, uint64_t* out, const Device& dev,
+                                   cudaStream_t s);
+// key[x] = pi(x) for x in [0, p.N) (O6 Feistel of the part's pool).
+cudaError_t launch_feistel_keys(const PoolParams& p, uint32_t* key, const Device& dev, cudaStream_t s);
 // first pool position outside its 2D block -> *bad (atomicMin; init ~0).
 cudaError_t launch_check_pool(const uint64_t* pool, const uint64_t* boff, uint64_t total,
                               const uint64_t* sub_bounds, uint32_t nb, uint64_t c_begin, uint64_t c_end,

@@ -72,6 +72,10 @@ struct ne_ctx {
     uint64_t* d_pool = nullptr;
     uint64_t* pool_at = nullptr;  // the buffer (d_pool or d_slots) holding the built pool
     bool walk_counts = false;     // d_counts holds the O5 counts of the current walk (unsharded walk)
+    uint64_t shard_units = 0;     // world > 1 with NCCL: walkers of this rank's shard in d_walks (from row 0)
+    uint64_t* d_part_bounds = nullptr;  // P + 1 context-part bounds (sharded construction)
+    uint64_t* d_tmat = nullptr;         // P x P (shard, part) pair counts of the episode (sharded construction)
+    std::vector<uint64_t> tmat;
     uint64_t pool_cap = 0;        // pairs d_slots / d_pool (and d_keys) hold; grown by ensure_pool
     float* d_tmp_f32 = nullptr;   // bf16 rows: fp32 staging of ne_get/set_embeddings
     uint64_t tmp_f32_cap = 0;
@@ -371,34 +375,44 @@ int check_loaded(ne_ctx* c) {
 
 uint32_t nb_local(const ne_ctx* c) { return (uint32_t)c->world * c->cfg.subparts; }
 
+// Walker shard s of an episode of `units` walkers at world P: local walkers
+// [s * chunk, min(units, (s + 1) * chunk)), chunk = ceil(units / P).
+void shard_range(uint64_t units, uint32_t P, uint32_t s, uint64_t* b, uint64_t* cnt) {
+    const uint64_t chunk = (units + P - 1) / P;
+    *b = std::min<uint64_t>(units, (uint64_t)s * chunk);
+    *cnt = std::min<uint64_t>(units, *b + chunk) - *b;
+}
+
 int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     uint64_t u0, units;
     episode_range(c, episode, &u0, &units);
-    const uint64_t row = c->cfg.walk_len + 1;
-    if (c->world > 1 && c->comm && units) {
-        // Walkers sharded over the ranks, walks all-gathered over NVLink: each
-        // rank walks ceil(units/P) walkers into its slice (in place).
-        const uint64_t P = (uint64_t)c->world, chunk = (units + P - 1) / P;
-        const uint64_t mine_b = std::min<uint64_t>(units, (uint64_t)c->rank * chunk);
-        const uint64_t mine = std::min<uint64_t>(units, mine_b + chunk) - mine_b;
-        NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0 + mine_b, mine, c->cfg.walk_len,
+    if (c->world > 1 && c->comm) {
+        // Walkers sharded over the ranks: this rank walks only its shard (rows
+        // from 0); the pool build sends every pair to its context part's owner.
+        uint64_t mb, mine;
+        shard_range(units, (uint32_t)c->world, (uint32_t)c->rank, &mb, &mine);
+        NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0 + mb, mine, c->cfg.walk_len,
                                    c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr,
-                                   c->d_walks + mine_b * row, ne::WalkCount{}, c->dev, c->stream));
+                                   c->d_walks, ne::WalkCount{}, c->dev, c->stream));
         if (mine) c->launches += 1;
-        c->walk_counts = false;  // other ranks' walkers: counted by the pool build
-        NE_NCCL(c, ncclAllGather(c->d_walks + (uint64_t)c->rank * chunk * row, c->d_walks, chunk * row,
-                                 ncclUint32, c->comm_walk, c->stream));
+        c->walk_counts = false;
+        c->shard_units = mine;
     } else {
+        // one GPU: the walk kernel also counts every walker's pairs (O5); a
+        // layout-only rank of P > 1 walks the whole episode and emulates the shards
+        const bool one = c->world == 1;
         NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0, units, c->cfg.walk_len,
                                    c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr, c->d_walks,
-                                   ne::WalkCount{c->d_counts, c->cfg.window, c->c_begin, c->c_begin + c->c_count},
+                                   one ? ne::WalkCount{c->d_counts, c->cfg.window, c->c_begin, c->c_begin + c->c_count}
+                                       : ne::WalkCount{},
                                    c->dev, c->stream));
         if (units) c->launches += 1;
-        c->walk_counts = true;  // O5 counts of this walk are in d_counts
+        c->walk_counts = one;
+        c->shard_units = units;
     }
     c->walked_epoch = epoch;
     c->walked_episode = episode;
-    c->walked_units = units;
+    c->walked_units = c->shard_units;
     c->built_epoch = c->built_episode = -1;
     return NE_OK;
 }
@@ -437,49 +451,11 @@ int ensure_pool(ne_ctx* c, uint64_t N) {
     return NE_OK;
 }
 
-int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
-    uint64_t u0, units;
-    episode_range(c, episode, &u0, &units);
-    ne::PoolParams p{};
-    p.units = units;
-    p.u0 = u0;
-    p.k = c->cfg.walk_len;
-    p.l = c->cfg.window;
-    p.Pw = c->Pw;
-    p.episode = episode;
-    p.epoch = epoch;
-    p.seed = c->cfg.seed;
-    p.c_begin = c->c_begin;
-    p.c_end = c->c_begin + c->c_count;
-    // O5: kept pairs per unit, exclusive scan -> part-local index bases, N_g
-    uint64_t N = 0;
-    if (units) {
-        if (c->cfg.walk_len == 0) {
-            NE_CUDA(c, ne::launch_count_line(c->d_tgt, p, c->d_counts, c->dev, c->stream));
-            c->launches += 1;
-        } else if (!c->walk_counts) {
-            NE_CUDA(c, ne::launch_count_walk(c->d_walks, c->d_slot_tab, p, c->d_counts, c->dev, c->stream));
-            c->launches += 1;
-        }
-        NE_CUDA(c, ne::launch_scan(c->d_counts, units, c->d_base, c->d_total, c->d_scan_scratch, c->stream,
-                                   &c->launches));
-        NE_CUDA(c, cudaMemcpyAsync(&N, c->d_total, sizeof N, cudaMemcpyDeviceToHost, c->stream));
-        NE_CUDA(c, cudaStreamSynchronize(c->stream));
-    }
-    if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
-                                  (unsigned long long)c->N_max);
-    NE_TRY(ensure_pool(c, N));
-    // O6: every kept pair to its position pi(x), then stable bucketing by sub-part
-    p.N = N;
-    const bool keyed = c->d_keys[0] && N > 0 && N <= (1ull << 32);
-    if (N) {
-        ne::PoolSink sink{c->d_slots, keyed ? c->d_keys[0] : nullptr};
-        if (c->cfg.walk_len > 0)
-            NE_CUDA(c, ne::launch_pairs_walk(c->d_walks, c->d_slot_tab, p, c->d_base, sink, c->dev, c->stream));
-        else
-            NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_base, sink, c->dev, c->stream));
-        c->launches += 1;
-    }
+// O6 order + 2D bucketing of the N pairs of this rank's part: the keyed path
+// takes (pairs, keys) in generation order in (d_slots, d_keys[0]); the direct
+// path the dense pi-indexed array in d_slots.  Leaves the pool in pool_at and
+// the block offsets in boff / d_boff.
+int finish_pool(ne_ctx* c, uint64_t N, bool keyed) {
     c->pool_at = c->d_pool;
     if (keyed) {  // radix passes to the window layout (cursors: head of the bucketing scratch)
         const uint64_t* win_pairs = nullptr;
@@ -499,6 +475,179 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     NE_CUDA(c, cudaMemcpyAsync(c->boff.data(), c->d_boff, c->boff.size() * sizeof(uint64_t),
                                cudaMemcpyDeviceToHost, c->stream));
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    return NE_OK;
+}
+
+ne::PoolParams pool_params(const ne_ctx* c, uint32_t epoch, uint32_t episode, uint64_t u0, uint64_t units) {
+    ne::PoolParams p{};
+    p.units = units;
+    p.u0 = u0;
+    p.k = c->cfg.walk_len;
+    p.l = c->cfg.window;
+    p.Pw = c->Pw;
+    p.episode = episode;
+    p.epoch = epoch;
+    p.seed = c->cfg.seed;
+    p.c_begin = c->c_begin;
+    p.c_end = c->c_begin + c->c_count;
+    return p;
+}
+
+// Sharded construction (walks, P > 1; "generate and send edge samples to
+// all node's memory"): every rank counts and generates the pairs of its
+// own walker shard only, grouped by context part; the P x P (shard, part)
+// count matrix is all-gathered; each rank receives its part's pairs from every
+// shard straight into generation order (shard s lands at base(s, g) = the
+// pairs of part g in shards < s), so the part-local index x of O6 is the
+// position -- the same pool as the unsharded construction, O(N/P) per rank.
+// A layout-only rank (no NCCL) runs the same kernels for every shard and copies
+// its part's segment in place of the receive.
+int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
+    const uint32_t P = (uint32_t)c->world, me = (uint32_t)c->rank;
+    uint64_t u0, units;
+    episode_range(c, episode, &u0, &units);
+    const uint64_t row = c->cfg.walk_len + 1;
+    const bool real = c->comm != nullptr;
+    c->tmat.assign((size_t)P * P, 0);
+    // this rank's shard (real) or shard s (emulation): counts -> scan -> part totals
+    auto count_shard = [&](uint32_t s, const uint32_t* walks, uint64_t su, uint64_t* tot_dev) -> int {
+        ne::PoolParams pp = pool_params(c, epoch, episode, u0, su);
+        if (su) {
+            NE_CUDA(c, ne::launch_count_parts(walks, c->d_slot_tab, pp, c->d_part_bounds, P, c->d_counts, c->dev,
+                                              c->stream));
+            NE_CUDA(c, ne::launch_scan(c->d_counts, (uint64_t)P * su, c->d_base, c->d_total, c->d_scan_scratch,
+                                       c->stream, &c->launches));
+            c->launches += 1;
+        }
+        NE_CUDA(c, ne::launch_part_totals(c->d_base, su, P, c->d_total, tot_dev, c->stream));
+        c->launches += 1;
+        (void)s;
+        return NE_OK;
+    };
+    auto shard_walks = [&](uint32_t s, uint64_t* su) -> const uint32_t* {
+        uint64_t b;
+        shard_range(units, P, s, &b, su);
+        return real ? c->d_walks : c->d_walks + b * row;
+    };
+    if (real) {
+        uint64_t su = c->shard_units;
+        NE_TRY(count_shard(me, c->d_walks, su, c->d_tmat + (uint64_t)me * P));
+        NE_NCCL(c, ncclAllGather(c->d_tmat + (uint64_t)me * P, c->d_tmat, P, ncclUint64, c->comm_walk, c->stream));
+    } else {
+        for (uint32_t s = 0; s < P; ++s) {
+            uint64_t su;
+            const uint32_t* w = shard_walks(s, &su);
+            NE_TRY(count_shard(s, w, su, c->d_tmat + (uint64_t)s * P));
+        }
+    }
+    NE_CUDA(c, cudaMemcpyAsync(c->tmat.data(), c->d_tmat, c->tmat.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                               c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    auto M = [&](uint32_t s, uint32_t g) { return c->tmat[(size_t)s * P + g]; };
+    uint64_t N = 0, send_max = 0;
+    std::vector<uint64_t> recv_off(P + 1, 0);
+    for (uint32_t s = 0; s < P; ++s) {
+        recv_off[s] = N;
+        N += M(s, me);
+        uint64_t S = 0;
+        for (uint32_t g = 0; g < P; ++g) S += M(s, g);
+        send_max = std::max(send_max, S);
+    }
+    recv_off[P] = N;
+    if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
+                                  (unsigned long long)c->N_max);
+    NE_TRY(ensure_pool(c, std::max(N, send_max)));
+    // pairs of a shard into the part-grouped send buffer (d_pool), then the
+    // exchange into d_slots in generation order
+    auto send_off = [&](uint32_t s, uint32_t g) {
+        uint64_t o = 0;
+        for (uint32_t q = 0; q < g; ++q) o += M(s, q);
+        return o;
+    };
+    auto gen_shard = [&](uint32_t s, const uint32_t* walks, uint64_t su) -> int {
+        if (!su) return NE_OK;
+        ne::PoolParams pp = pool_params(c, epoch, episode, u0, su);
+        NE_CUDA(c, ne::launch_pairs_parts(walks, c->d_slot_tab, pp, c->d_part_bounds, P, c->d_base, c->d_pool,
+                                          c->dev, c->stream));
+        c->launches += 1;
+        (void)s;
+        return NE_OK;
+    };
+    if (real) {
+        NE_TRY(gen_shard(me, c->d_walks, c->shard_units));
+        NE_NCCL(c, ncclGroupStart());
+        for (uint32_t q = 0; q < P; ++q) {
+            if (M(me, q)) NE_NCCL(c, ncclSend(c->d_pool + send_off(me, q), M(me, q), ncclUint64, (int)q, c->comm_walk,
+                                              c->stream));
+            if (M(q, me)) NE_NCCL(c, ncclRecv(c->d_slots + recv_off[q], M(q, me), ncclUint64, (int)q, c->comm_walk,
+                                              c->stream));
+        }
+        NE_NCCL(c, ncclGroupEnd());
+    } else {
+        for (uint32_t s = 0; s < P; ++s) {
+            uint64_t su;
+            const uint32_t* w = shard_walks(s, &su);
+            if (!M(s, me)) continue;
+            NE_TRY(count_shard(s, w, su, c->d_tmat + (uint64_t)s * P));  // counts / bases of shard s again
+            NE_TRY(gen_shard(s, w, su));
+            NE_CUDA(c, cudaMemcpyAsync(c->d_slots + recv_off[s], c->d_pool + send_off(s, me), M(s, me) * sizeof(uint64_t),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+        }
+    }
+    // O6: pi over the gathered pool, then order + bucketing
+    ne::PoolParams pp = pool_params(c, epoch, episode, u0, units);
+    pp.N = N;
+    const bool keyed = c->d_keys[0] && N > 0 && N <= (1ull << 32);
+    if (N) {
+        if (keyed) {
+            NE_CUDA(c, ne::launch_feistel_keys(pp, c->d_keys[0], c->dev, c->stream));
+        } else {  // direct: dense pi-indexed array in d_slots (via d_pool)
+            NE_CUDA(c, ne::launch_feistel_scatter(pp, c->d_slots, c->d_pool, c->dev, c->stream));
+            std::swap(c->d_slots, c->d_pool);
+        }
+        c->launches += 1;
+    }
+    NE_TRY(finish_pool(c, N, keyed));
+    c->built_epoch = epoch;
+    c->built_episode = episode;
+    return NE_OK;
+}
+
+int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
+    if (c->world > 1 && c->cfg.walk_len > 0) return do_build_sharded(c, epoch, episode);
+    uint64_t u0, units;
+    episode_range(c, episode, &u0, &units);
+    ne::PoolParams p = pool_params(c, epoch, episode, u0, units);
+    // O5: kept pairs per unit, exclusive scan -> part-local index bases, N_g
+    uint64_t N = 0;
+    if (units) {
+        if (c->cfg.walk_len == 0) {
+            NE_CUDA(c, ne::launch_count_line(c->d_tgt, p, c->d_counts, c->dev, c->stream));
+            c->launches += 1;
+        } else if (!c->walk_counts) {
+            NE_CUDA(c, ne::launch_count_walk(c->d_walks, c->d_slot_tab, p, c->d_counts, c->dev, c->stream));
+            c->launches += 1;
+        }
+        NE_CUDA(c, ne::launch_scan(c->d_counts, units, c->d_base, c->d_total, c->d_scan_scratch, c->stream,
+                                   &c->launches));
+        NE_CUDA(c, cudaMemcpyAsync(&N, c->d_total, sizeof N, cudaMemcpyDeviceToHost, c->stream));
+        NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
+                                  (unsigned long long)c->N_max);
+    NE_TRY(ensure_pool(c, N));
+    // O6: every kept pair with its position pi(x), then stable bucketing by sub-part
+    p.N = N;
+    const bool keyed = c->d_keys[0] && N > 0 && N <= (1ull << 32);
+    if (N) {
+        ne::PoolSink sink{c->d_slots, keyed ? c->d_keys[0] : nullptr};
+        if (c->cfg.walk_len > 0)
+            NE_CUDA(c, ne::launch_pairs_walk(c->d_walks, c->d_slot_tab, p, c->d_base, sink, c->dev, c->stream));
+        else
+            NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_base, sink, c->dev, c->stream));
+        c->launches += 1;
+    }
+    NE_TRY(finish_pool(c, N, keyed));
     c->built_epoch = epoch;
     c->built_episode = episode;
     return NE_OK;
@@ -804,6 +953,7 @@ int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
         return fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", world);
     if ((uint64_t)world * c->cfg.subparts > 256 || (uint64_t)world * world * c->cfg.subparts > 4096)
         return fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
+    if (world > 32) return fail(c, NE_EINVAL, "world=%d > 32 (one lane per context part in the pool build)", world);
     if (c->comm_walk) { ncclCommDestroy(c->comm_walk); c->comm_walk = nullptr; }
     if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
     c->rank = rank;
@@ -988,8 +1138,9 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     c->units_max = (c->units_total + g.episodes - 1) / g.episodes;
     c->N_max = c->units_max * c->Pw;
     if (g.walk_len > 0) {
-        // rows padded to a multiple of world for the sharded walk's all-gather
-        const uint64_t wrows = (c->units_max + P - 1) / P * P;
+        // a rank of a world > 1 NCCL job walks only its shard (ceil(units / P)
+        // rows); one GPU and layout-only ranks walk the whole episode
+        const uint64_t wrows = (P > 1 && c->comm) ? (c->units_max + P - 1) / P : c->units_max;
         NE_ALLOC(c->d_walks, std::max<uint64_t>(wrows, 1) * (g.walk_len + 1));
         std::vector<uint32_t> tab_s;
         for (uint32_t i = 0; i < g.walk_len; ++i)
@@ -998,9 +1149,17 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
         NE_CUDA(c, cudaMemcpyAsync(c->d_slot_tab, tab_s.data(), tab_s.size() * sizeof(uint32_t),
                                    cudaMemcpyHostToDevice, c->stream));
     }
-    NE_ALLOC(c->d_counts, std::max<uint64_t>(c->units_max, 1));
-    NE_ALLOC(c->d_base, std::max<uint64_t>(c->units_max, 1));
-    if (!reuse) NE_TRY(dalloc(c, &c->d_scan_scratch, ne::scan_scratch_bytes(c->units_max)));
+    // per-unit counts / bases; the sharded construction (walks, P > 1) keeps P
+    // counts per walker of a shard: P x ceil(units_max / P) entries
+    const uint64_t cnt_len = std::max<uint64_t>(
+        {c->units_max, (g.walk_len > 0 && P > 1) ? (c->units_max + P - 1) / P * P : 0, 1});
+    NE_ALLOC(c->d_counts, cnt_len);
+    NE_ALLOC(c->d_base, cnt_len);
+    if (!reuse) NE_TRY(dalloc(c, &c->d_scan_scratch, ne::scan_scratch_bytes(cnt_len)));
+    NE_ALLOC(c->d_part_bounds, (size_t)P + 1);
+    NE_ALLOC(c->d_tmat, (size_t)P * P);
+    NE_CUDA(c, cudaMemcpyAsync(c->d_part_bounds, c->part_bounds.data(), (P + 1) * sizeof(uint64_t),
+                               cudaMemcpyHostToDevice, c->stream));
     NE_ALLOC(c->d_total, 1);
     // d_slots / d_pool / d_keys: sized by the first episode's pool (ensure_pool)
     if (!reuse) NE_TRY(dalloc(c, &c->d_scratch, ne::bucket_scratch_bytes(c->N_max, nb_local(c))));
