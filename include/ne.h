@@ -137,12 +137,14 @@ typedef struct {
 typedef struct {
     uint64_t samples;        /* positive samples trained                               */
     double   loss_sum;       /* sum over all 1+K updates of -log s / -log(1-s)         */
-    float    ms_walk;        /* walk kernel time                                       */
-    float    ms_build;       /* pair scatter + bucketing time                          */
+    float    ms_walk;        /* walk kernel time (on the stream the walk ran on)       */
+    float    ms_build;       /* pool build time: pairs, exchange, order, bucketing     */
     float    ms_train;       /* sum of SGNS kernel durations                           */
     float    ms_comm_wait;   /* time the compute stream waited for ring receives       */
     uint32_t train_launches; /* SGNS kernel launches                                   */
     uint32_t kernel_launches;/* every kernel this library launched during the call     */
+    float    ms_pool_wait;   /* time the compute stream waited for walk + pool build
+                                (exposed; a build overlapped with training is hidden)  */
 } ne_stats;
 
 /* Library ABI version (NE_ABI_VERSION). */
@@ -225,9 +227,15 @@ int ne_build_samples(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint64_t *n_
 int ne_train_samples(ne_ctx *ctx, uint32_t epoch, uint32_t episode, float lr, ne_stats *stats);
 
 /* One epoch ("one epoch goes over all the sampled edges"): for every
- * episode, walk + build + train.  flags: NE_REUSE_SAMPLES.  lr is constant
- * within the epoch (the caller may decay it between epochs).
- * stats (nullable) accumulates the whole epoch. */
+ * episode, walk + build + train.  The walk and pool of the next episode are
+ * built on a side stream while the current episode trains, into a
+ * third pool buffer allocated when HBM allows; after the last episode the
+ * first episode of epoch+1 is built the same way and kept for the next call
+ * (discarded by ne_load_graph, ne_random_walk, ne_build_samples or a call
+ * with another epoch).  Results are those of the serial order.
+ * flags: NE_REUSE_SAMPLES, NE_CHECK_BLOCKS.  lr is constant within the epoch
+ * (the caller may decay it between epochs).  stats (nullable)
+ * accumulates the whole epoch. */
 int ne_train_epoch(ne_ctx *ctx, uint32_t epoch, float lr, uint32_t flags, ne_stats *stats);
 
 /* Copy rows [row_begin, row_end) of the vertex (which = NE_VERTEX) or context

@@ -32,6 +32,9 @@ struct ne_ctx {
     int device = 0;
     ne::Device dev;
     cudaStream_t own_stream = nullptr, stream = nullptr, comm_stream = nullptr;
+    cudaStream_t build_stream = nullptr;  // walk + pool build of the next episode, behind training
+    cudaStream_t ws = nullptr;            // the stream walk / build kernels go to: stream, or build_stream
+                                          // while a pipelined build runs
     ne_alloc_fn alloc = nullptr;
     ne_free_fn free_fn = nullptr;
     void* user = nullptr;
@@ -67,7 +70,8 @@ struct ne_ctx {
     uint64_t units_total = 0, units_max = 0, N_max = 0;
     uint32_t* d_walks = nullptr;
     uint32_t* d_slot_tab = nullptr;
-    uint64_t* d_slots = nullptr;
+    std::vector<uint64_t*> pbufs;  // 2 pair buffers, or 3 when the next episode's pool is built during training
+    uint64_t* d_slots = nullptr;   // the two pbufs a build uses (sink / radix ping-pong)
     uint32_t* d_keys[2] = {nullptr, nullptr};  // keyed pool sink + radix ping-pong (nullptr: direct sink)
     uint64_t* d_pool = nullptr;
     uint64_t* pool_at = nullptr;  // the buffer (d_pool or d_slots) holding the built pool
@@ -86,6 +90,19 @@ struct ne_ctx {
     uint64_t* d_total = nullptr;    // N_g of the episode
     uint64_t* d_boff = nullptr;
     std::vector<uint64_t> boff;
+    // the next episode's pool, built on build_stream while the current one trains
+    struct NextPool {
+        bool valid = false;
+        uint64_t* at = nullptr;
+        uint64_t* d_boff = nullptr;
+        std::vector<uint64_t> boff;
+        int64_t epoch = -1, episode = -1;
+        float ms_walk = 0.f, ms_build = 0.f;
+    } next;
+    uint64_t* d_boff_alt = nullptr;
+    const uint64_t* keep_pool = nullptr;  // pool in training while a build runs (select_scratch skips it)
+    int sgns_reserve = 0;                 // SMs the SGNS grid leaves free (concurrent pool build)
+    uint64_t pool_gen = 0;                // bumped whenever ensure_pool reallocates the pair buffers
     double* d_loss = nullptr;
     unsigned long long* d_bad = nullptr;
     bool n2v = false;           // node2vec walks (p, q != 1)
@@ -208,6 +225,7 @@ void free_all(ne_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    if (c->build_stream) cudaStreamSynchronize(c->build_stream);
     c->stage_pending = false;
     for (auto& a : c->allocs) {
         if (c->free_fn) c->free_fn(a.p, a.bytes, c->device, (void*)c->stream, c->user);
@@ -219,8 +237,11 @@ void free_all(ne_ctx* c) {
     c->d_tmp_f32 = nullptr;
     c->tmp_f32_cap = 0;
     c->d_keys[0] = c->d_keys[1] = nullptr;
+    c->pbufs.clear();
     c->d_slots = c->d_pool = c->pool_at = nullptr;
     c->pool_cap = 0;
+    c->next = ne_ctx::NextPool{};
+    c->keep_pool = nullptr;
     c->loaded = false;
     c->walked_epoch = c->walked_episode = c->built_epoch = c->built_episode = -1;
 }
@@ -393,7 +414,7 @@ int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         shard_range(units, (uint32_t)c->world, (uint32_t)c->rank, &mb, &mine);
         NE_CUDA(c, ne::launch_walk(c->d_off, c->d_tgt, c->n, u0 + mb, mine, c->cfg.walk_len,
                                    c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr,
-                                   c->d_walks, ne::WalkCount{}, c->dev, c->stream));
+                                   c->d_walks, ne::WalkCount{}, c->dev, c->ws));
         if (mine) c->launches += 1;
         c->walk_counts = false;
         c->shard_units = mine;
@@ -405,7 +426,7 @@ int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
                                    c->cfg.seed, epoch, c->n2v ? c->n2v_thr : nullptr, c->d_walks,
                                    one ? ne::WalkCount{c->d_counts, c->cfg.window, c->c_begin, c->c_begin + c->c_count}
                                        : ne::WalkCount{},
-                                   c->dev, c->stream));
+                                   c->dev, c->ws));
         if (units) c->launches += 1;
         c->walk_counts = one;
         c->shard_units = units;
@@ -422,33 +443,63 @@ int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
 // 3-4x the real pool on power-law graphs).  The key buffers of the keyed path
 // are optional: if they do not fit, the direct path builds the same pool.
 int ensure_pool(ne_ctx* c, uint64_t N) {
-    if (N <= c->pool_cap && c->d_slots) return NE_OK;
-    for (void* p : {(void*)c->d_slots, (void*)c->d_pool, (void*)c->d_keys[0], (void*)c->d_keys[1]})
+    if (N <= c->pool_cap && !c->pbufs.empty()) return NE_OK;
+    // growing: a pool still being trained may live in these buffers -- wait for it
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (void* p : c->pbufs) dfree(c, p);
+    for (void* p : {(void*)c->d_keys[0], (void*)c->d_keys[1]})
         if (p) dfree(c, p);
+    c->pbufs.clear();
     c->d_slots = c->d_pool = c->pool_at = nullptr;
     c->d_keys[0] = c->d_keys[1] = nullptr;
     c->pool_cap = 0;
+    c->pool_gen += 1;
     c->built_epoch = c->built_episode = -1;
+    c->next.valid = false;
     const uint64_t cap = std::max<uint64_t>(1, std::min<uint64_t>(std::max<uint64_t>(c->N_max, 1), N + N / 8));
-    NE_TRY(dalloc_t(c, &c->d_slots, cap));
-    NE_TRY(dalloc_t(c, &c->d_pool, cap));
+    uint64_t *b0 = nullptr, *b1 = nullptr;
+    NE_TRY(dalloc_t(c, &b0, cap));
+    NE_TRY(dalloc_t(c, &b1, cap));
+    c->pbufs = {b0, b1};
+    c->d_slots = b0;
+    c->d_pool = b1;
     c->pool_cap = cap;
-    const char* e = std::getenv("NE_POOL_DIRECT");  // 1: force the direct path (tests, A/B)
-    if (e && std::atoi(e) != 0) return NE_OK;
-    const size_t bytes = cap * sizeof(uint32_t);
     size_t free_b = 0, total_b = 0;
-    if (!c->alloc && !(cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b >= 2 * bytes + (1ull << 30)))
-        return NE_OK;  // keep 1 GiB for the caller
+    auto fits = [&](size_t bytes) {  // keep 1 GiB for the caller
+        return c->alloc || (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && free_b >= bytes + (1ull << 30));
+    };
     const std::string saved = c->err;
-    uint32_t *k0 = nullptr, *k1 = nullptr;
-    if (dalloc_t(c, &k0, cap) == NE_OK && dalloc_t(c, &k1, cap) == NE_OK) {
-        c->d_keys[0] = k0;
-        c->d_keys[1] = k1;
-    } else {
-        if (k0) dfree(c, k0);
-        c->err = saved;  // not an error: the direct path
+    const char* e = std::getenv("NE_POOL_DIRECT");  // 1: force the direct path (tests, A/B)
+    if (!(e && std::atoi(e) != 0) && fits(2 * cap * sizeof(uint32_t))) {
+        uint32_t *k0 = nullptr, *k1 = nullptr;
+        if (dalloc_t(c, &k0, cap) == NE_OK && dalloc_t(c, &k1, cap) == NE_OK) {
+            c->d_keys[0] = k0;
+            c->d_keys[1] = k1;
+        } else {
+            if (k0) dfree(c, k0);
+            c->err = saved;  // not an error: the direct path
+        }
+    }
+    // a third pair buffer lets the next episode's pool be built while this one
+    // trains (ne_train_epoch); without it the build is serial (NE_PIPELINE=0 forces that)
+    const char* pe = std::getenv("NE_PIPELINE");
+    if (!(pe && std::atoi(pe) == 0) && fits(cap * sizeof(uint64_t))) {
+        uint64_t* b2 = nullptr;
+        if (dalloc_t(c, &b2, cap) == NE_OK) c->pbufs.push_back(b2);
+        else c->err = saved;
     }
     return NE_OK;
+}
+
+// The two pair buffers a build may use: every pbuf except `keep` (the pool
+// being trained while the next one is built).
+void select_scratch(ne_ctx* c, const uint64_t* keep) {
+    uint64_t* pick[2] = {nullptr, nullptr};
+    int k = 0;
+    for (uint64_t* b : c->pbufs)
+        if (b != keep && k < 2) pick[k++] = b;
+    c->d_slots = pick[0];
+    c->d_pool = pick[1];
 }
 
 // O6 order + 2D bucketing of the N pairs of this rank's part: the keyed path
@@ -463,18 +514,18 @@ int finish_pool(ne_ctx* c, uint64_t N, bool keyed) {
         uint64_t* spare = nullptr;
         NE_CUDA(c, ne::launch_order(N, c->d_slots, c->d_keys[0], c->d_pool, c->d_keys[1],
                                     static_cast<uint32_t*>(c->d_scratch), &win_pairs, &win_pos, &spare, c->dev,
-                                    c->stream, &c->launches));
+                                    c->ws, &c->launches));
         c->pool_at = spare;
         NE_CUDA(c, ne::launch_bucket(win_pairs, win_pos, N, c->d_sub_bounds, nb_local(c), c->d_scratch,
-                                     c->pool_at, c->d_boff, c->dev, c->stream, &c->launches));
+                                     c->pool_at, c->d_boff, c->dev, c->ws, &c->launches));
     } else {
         NE_CUDA(c, ne::launch_bucket(c->d_slots, nullptr, N, c->d_sub_bounds, nb_local(c), c->d_scratch,
-                                     c->pool_at, c->d_boff, c->dev, c->stream, &c->launches));
+                                     c->pool_at, c->d_boff, c->dev, c->ws, &c->launches));
     }
     c->boff.assign(nb_local(c) + 1, 0);
     NE_CUDA(c, cudaMemcpyAsync(c->boff.data(), c->d_boff, c->boff.size() * sizeof(uint64_t),
-                               cudaMemcpyDeviceToHost, c->stream));
-    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+                               cudaMemcpyDeviceToHost, c->ws));
+    NE_CUDA(c, cudaStreamSynchronize(c->ws));
     return NE_OK;
 }
 
@@ -514,12 +565,12 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         ne::PoolParams pp = pool_params(c, epoch, episode, u0, su);
         if (su) {
             NE_CUDA(c, ne::launch_count_parts(walks, c->d_slot_tab, pp, c->d_part_bounds, P, c->d_counts, c->dev,
-                                              c->stream));
+                                              c->ws));
             NE_CUDA(c, ne::launch_scan(c->d_counts, (uint64_t)P * su, c->d_base, c->d_total, c->d_scan_scratch,
-                                       c->stream, &c->launches));
+                                       c->ws, &c->launches));
             c->launches += 1;
         }
-        NE_CUDA(c, ne::launch_part_totals(c->d_base, su, P, c->d_total, tot_dev, c->stream));
+        NE_CUDA(c, ne::launch_part_totals(c->d_base, su, P, c->d_total, tot_dev, c->ws));
         c->launches += 1;
         (void)s;
         return NE_OK;
@@ -532,7 +583,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     if (real) {
         uint64_t su = c->shard_units;
         NE_TRY(count_shard(me, c->d_walks, su, c->d_tmat + (uint64_t)me * P));
-        NE_NCCL(c, ncclAllGather(c->d_tmat + (uint64_t)me * P, c->d_tmat, P, ncclUint64, c->comm_walk, c->stream));
+        NE_NCCL(c, ncclAllGather(c->d_tmat + (uint64_t)me * P, c->d_tmat, P, ncclUint64, c->comm_walk, c->ws));
     } else {
         for (uint32_t s = 0; s < P; ++s) {
             uint64_t su;
@@ -541,8 +592,8 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         }
     }
     NE_CUDA(c, cudaMemcpyAsync(c->tmat.data(), c->d_tmat, c->tmat.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                               c->stream));
-    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+                               c->ws));
+    NE_CUDA(c, cudaStreamSynchronize(c->ws));
     auto M = [&](uint32_t s, uint32_t g) { return c->tmat[(size_t)s * P + g]; };
     uint64_t N = 0, send_max = 0;
     std::vector<uint64_t> recv_off(P + 1, 0);
@@ -557,6 +608,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
                                   (unsigned long long)c->N_max);
     NE_TRY(ensure_pool(c, std::max(N, send_max)));
+    select_scratch(c, c->keep_pool);
     // pairs of a shard into the part-grouped send buffer (d_pool), then the
     // exchange into d_slots in generation order
     auto send_off = [&](uint32_t s, uint32_t g) {
@@ -568,7 +620,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         if (!su) return NE_OK;
         ne::PoolParams pp = pool_params(c, epoch, episode, u0, su);
         NE_CUDA(c, ne::launch_pairs_parts(walks, c->d_slot_tab, pp, c->d_part_bounds, P, c->d_base, c->d_pool,
-                                          c->dev, c->stream));
+                                          c->dev, c->ws));
         c->launches += 1;
         (void)s;
         return NE_OK;
@@ -578,9 +630,9 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         NE_NCCL(c, ncclGroupStart());
         for (uint32_t q = 0; q < P; ++q) {
             if (M(me, q)) NE_NCCL(c, ncclSend(c->d_pool + send_off(me, q), M(me, q), ncclUint64, (int)q, c->comm_walk,
-                                              c->stream));
+                                              c->ws));
             if (M(q, me)) NE_NCCL(c, ncclRecv(c->d_slots + recv_off[q], M(q, me), ncclUint64, (int)q, c->comm_walk,
-                                              c->stream));
+                                              c->ws));
         }
         NE_NCCL(c, ncclGroupEnd());
     } else {
@@ -591,7 +643,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
             NE_TRY(count_shard(s, w, su, c->d_tmat + (uint64_t)s * P));  // counts / bases of shard s again
             NE_TRY(gen_shard(s, w, su));
             NE_CUDA(c, cudaMemcpyAsync(c->d_slots + recv_off[s], c->d_pool + send_off(s, me), M(s, me) * sizeof(uint64_t),
-                                       cudaMemcpyDeviceToDevice, c->stream));
+                                       cudaMemcpyDeviceToDevice, c->ws));
         }
     }
     // O6: pi over the gathered pool, then order + bucketing
@@ -600,9 +652,9 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     const bool keyed = c->d_keys[0] && N > 0 && N <= (1ull << 32);
     if (N) {
         if (keyed) {
-            NE_CUDA(c, ne::launch_feistel_keys(pp, c->d_keys[0], c->dev, c->stream));
+            NE_CUDA(c, ne::launch_feistel_keys(pp, c->d_keys[0], c->dev, c->ws));
         } else {  // direct: dense pi-indexed array in d_slots (via d_pool)
-            NE_CUDA(c, ne::launch_feistel_scatter(pp, c->d_slots, c->d_pool, c->dev, c->stream));
+            NE_CUDA(c, ne::launch_feistel_scatter(pp, c->d_slots, c->d_pool, c->dev, c->ws));
             std::swap(c->d_slots, c->d_pool);
         }
         c->launches += 1;
@@ -622,29 +674,30 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     uint64_t N = 0;
     if (units) {
         if (c->cfg.walk_len == 0) {
-            NE_CUDA(c, ne::launch_count_line(c->d_tgt, p, c->d_counts, c->dev, c->stream));
+            NE_CUDA(c, ne::launch_count_line(c->d_tgt, p, c->d_counts, c->dev, c->ws));
             c->launches += 1;
         } else if (!c->walk_counts) {
-            NE_CUDA(c, ne::launch_count_walk(c->d_walks, c->d_slot_tab, p, c->d_counts, c->dev, c->stream));
+            NE_CUDA(c, ne::launch_count_walk(c->d_walks, c->d_slot_tab, p, c->d_counts, c->dev, c->ws));
             c->launches += 1;
         }
-        NE_CUDA(c, ne::launch_scan(c->d_counts, units, c->d_base, c->d_total, c->d_scan_scratch, c->stream,
+        NE_CUDA(c, ne::launch_scan(c->d_counts, units, c->d_base, c->d_total, c->d_scan_scratch, c->ws,
                                    &c->launches));
-        NE_CUDA(c, cudaMemcpyAsync(&N, c->d_total, sizeof N, cudaMemcpyDeviceToHost, c->stream));
-        NE_CUDA(c, cudaStreamSynchronize(c->stream));
+        NE_CUDA(c, cudaMemcpyAsync(&N, c->d_total, sizeof N, cudaMemcpyDeviceToHost, c->ws));
+        NE_CUDA(c, cudaStreamSynchronize(c->ws));
     }
     if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
                                   (unsigned long long)c->N_max);
     NE_TRY(ensure_pool(c, N));
+    select_scratch(c, c->keep_pool);
     // O6: every kept pair with its position pi(x), then stable bucketing by sub-part
     p.N = N;
     const bool keyed = c->d_keys[0] && N > 0 && N <= (1ull << 32);
     if (N) {
         ne::PoolSink sink{c->d_slots, keyed ? c->d_keys[0] : nullptr};
         if (c->cfg.walk_len > 0)
-            NE_CUDA(c, ne::launch_pairs_walk(c->d_walks, c->d_slot_tab, p, c->d_base, sink, c->dev, c->stream));
+            NE_CUDA(c, ne::launch_pairs_walk(c->d_walks, c->d_slot_tab, p, c->d_base, sink, c->dev, c->ws));
         else
-            NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_base, sink, c->dev, c->stream));
+            NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_base, sink, c->dev, c->ws));
         c->launches += 1;
     }
     NE_TRY(finish_pool(c, N, keyed));
@@ -688,19 +741,25 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
         const char* e = std::getenv("NE_RING_RESERVE_SMS");
         return e ? std::atoi(e) : 0;
     }();
-    p.reserve_sms = (c->world > 1 && c->comm) ? reserve : 0;
+    p.reserve_sms = std::max((c->world > 1 && c->comm) ? reserve : 0, c->sgns_reserve);
     return p;
 }
+
+// Launched training of one episode: timing events and sample count, read
+// back by finish_train after the stream has run them.
+struct TrainPending {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, waits;
+    uint64_t samples = 0;
+    uint32_t launches = 0;
+};
 
 // NEXT-2 host staging (P:142 stages 2 and 5), one GPU: sub-part t trains in
 // slot t mod 3 while sub-part t+1 is copied in (copy stream) and t-1 copied
 // back (comm stream); a slot is refilled only after its previous D2H.
-int do_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st) {
+int launch_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPending& tp) {
     const uint32_t k = c->cfg.subparts, S = (uint32_t)c->vslot.size();
     const uint64_t d = c->cfg.dim;
-    NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
     std::vector<cudaEvent_t> loaded(k), stored(k);
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
     auto h2d = [&](uint32_t t) -> int {
         if (t >= S) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, stored[t - S], 0));
         else if (c->stage_pending) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->stage_done, 0));
@@ -711,7 +770,6 @@ int do_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_st
         NE_CUDA(c, cudaEventRecord(loaded[t], c->copy_stream));
         return NE_OK;
     };
-    uint64_t samples = 0;
     if (k) NE_TRY(h2d(0));
     for (uint32_t t = 0; t < k; ++t) {
         if (t + 1 < k) NE_TRY(h2d(t + 1));
@@ -721,9 +779,9 @@ int do_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_st
         NE_CUDA(c, cudaEventRecord(e0, c->stream));
         NE_CUDA(c, ne::launch_sgns(sp, c->dev, c->stream));
         NE_CUDA(c, cudaEventRecord(e1, c->stream));
-        if (sp.count) { c->launches += 1; if (st) st->train_launches += 1; }
-        timed.push_back({e0, e1});
-        samples += sp.count;
+        if (sp.count) { c->launches += 1; tp.launches += 1; }
+        tp.timed.push_back({e0, e1});
+        tp.samples += sp.count;
         const uint64_t sb = c->sub_bounds[t], rows = c->sub_bounds[t + 1] - sb;
         NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, e1, 0));
         NE_CUDA(c, cudaMemcpyAsync(host_row(c, sb), c->vslot[t % S], rows * d * elem_bytes(c),
@@ -736,38 +794,24 @@ int do_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_st
     if (!c->stage_done) NE_CUDA(c, cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
     NE_CUDA(c, cudaEventRecord(c->stage_done, c->comm_stream));
     c->stage_pending = true;
-    double loss = 0.0;
-    NE_CUDA(c, cudaMemcpyAsync(&loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    NE_CUDA(c, cudaStreamSynchronize(c->stream));
-    if (st) {
-        st->samples += samples;
-        st->loss_sum += loss;
-        for (auto& pr : timed) {
-            float ms = 0.f;
-            NE_CUDA(c, cudaEventElapsedTime(&ms, pr.first, pr.second));
-            st->ms_train += ms;
-        }
-    }
-    c->ev_used = 0;
     return NE_OK;
 }
 
 // O7 ring: round r, slot t trains block
 // (vsub = ((rank - r) mod P)*k + t, context part rank); the trained sub-part is
 // sent to rank+1 while slot t+1 trains, and the sub-part for round r+1 arrives
-// from rank-1 into the other half of the ping-pong buffers.
-int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st) {
+// from rank-1 into the other half of the ping-pong buffers.  Everything is
+// enqueued (compute stream + comm stream); finish_train waits for it.
+int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPending& tp) {
     NE_TRY(wait_alias(c));
-    if (c->cfg.staging == NE_STAGE_HOST) return do_train_staged(c, epoch, episode, lr, st);
+    NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
+    if (c->cfg.staging == NE_STAGE_HOST) return launch_train_staged(c, epoch, episode, lr, tp);
     const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank;
     const uint64_t d = c->cfg.dim;
     if (P > 1 && !c->comm)
         return fail(c, NE_ESTATE, "world=%u context has no NCCL communicator (layout-only)", P);
-    NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
     std::vector<cudaEvent_t> recv(k, nullptr);
     if (c->ring_pending) recv.assign(k, c->ring_done);  // home-coming sub-parts of the last call
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed, waits;
-    uint64_t samples = 0;
     for (uint32_t r = 0; r < P; ++r) {
         for (uint32_t t = 0; t < k; ++t) {
             const uint32_t vs = (uint32_t)plan_vsub(P, k, r, t, g);
@@ -777,16 +821,16 @@ int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st
                 NE_CUDA(c, cudaEventRecord(w0, c->stream));
                 NE_CUDA(c, cudaStreamWaitEvent(c->stream, recv[t], 0));
                 NE_CUDA(c, cudaEventRecord(w1, c->stream));
-                waits.push_back({w0, w1});
+                tp.waits.push_back({w0, w1});
             }
             const ne::SgnsParams sp = sgns_params(c, vs, V, epoch, episode, lr);
             cudaEvent_t e0 = next_event(c), e1 = next_event(c);
             NE_CUDA(c, cudaEventRecord(e0, c->stream));
             NE_CUDA(c, ne::launch_sgns(sp, c->dev, c->stream));
             NE_CUDA(c, cudaEventRecord(e1, c->stream));
-            if (sp.count) { c->launches += 1; if (st) st->train_launches += 1; }
-            timed.push_back({e0, e1});
-            samples += sp.count;
+            if (sp.count) { c->launches += 1; tp.launches += 1; }
+            tp.timed.push_back({e0, e1});
+            tp.samples += sp.count;
             if (P > 1) {
                 const uint32_t vs_next = (uint32_t)plan_vsub(P, k, r + 1, t, g);
                 const uint64_t send_rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
@@ -815,26 +859,105 @@ int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st
         NE_CUDA(c, cudaEventRecord(c->ring_done, c->comm_stream));
         c->ring_pending = true;
     }
+    return NE_OK;
+}
+
+// Wait for a launched episode, add its loss, samples and kernel times to st.
+int finish_train(ne_ctx* c, TrainPending& tp, ne_stats* st) {
     double loss = 0.0;
     NE_CUDA(c, cudaMemcpyAsync(&loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
     if (st) {
-        st->samples += samples;
+        st->samples += tp.samples;
         st->loss_sum += loss;
-        for (auto& pr : timed) {
+        st->train_launches += tp.launches;
+        for (auto& pr : tp.timed) {
             float ms = 0.f;
             NE_CUDA(c, cudaEventElapsedTime(&ms, pr.first, pr.second));
             st->ms_train += ms;
         }
-        for (auto& pr : waits) {
+        for (auto& pr : tp.waits) {
             float ms = 0.f;
             NE_CUDA(c, cudaEventElapsedTime(&ms, pr.first, pr.second));
             st->ms_comm_wait += ms;
         }
     }
+    return NE_OK;
+}
+
+int do_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_stats* st) {
+    TrainPending tp;
+    NE_TRY(launch_train(c, epoch, episode, lr, tp));
+    NE_TRY(finish_train(c, tp, st));
     c->ev_used = 0;
     return NE_OK;
 }
+
+// Walk + build of (epoch, episode) on stream `s` into the current pool state;
+// ms_walk / ms_build from events on `s`.
+int walk_build(ne_ctx* c, uint32_t epoch, uint32_t episode, cudaStream_t s, float* ms_walk, float* ms_build) {
+    c->ws = s;
+    cudaEvent_t a = next_event(c), b = next_event(c), d = next_event(c);
+    int rc = NE_OK;
+    if (cudaEventRecord(a, s) != cudaSuccess) rc = fail(c, NE_ECUDA, "event record");
+    if (rc == NE_OK && c->cfg.walk_len > 0) rc = do_walk(c, epoch, episode);
+    if (rc == NE_OK && cudaEventRecord(b, s) != cudaSuccess) rc = fail(c, NE_ECUDA, "event record");
+    if (rc == NE_OK) rc = do_build(c, epoch, episode);  // synchronises s
+    if (rc == NE_OK && cudaEventRecord(d, s) != cudaSuccess) rc = fail(c, NE_ECUDA, "event record");
+    c->ws = c->stream;
+    NE_TRY(rc);
+    NE_CUDA(c, cudaEventSynchronize(d));
+    NE_CUDA(c, cudaEventElapsedTime(ms_walk, a, b));
+    NE_CUDA(c, cudaEventElapsedTime(ms_build, b, d));
+    return NE_OK;
+}
+
+// Build (epoch, episode) into c->next on build_stream while the current pool
+// (pool_at) trains on the compute stream: the build uses the two pair buffers
+// the training pool does not occupy and the alternate block-offset array.
+int prebuild_next(ne_ctx* c, uint32_t epoch, uint32_t episode) {
+    // stash the current pool
+    uint64_t* at = c->pool_at;
+    std::vector<uint64_t> boff;
+    boff.swap(c->boff);
+    uint64_t* d_boff = c->d_boff;
+    const int64_t be = c->built_epoch, bp = c->built_episode;
+    const uint64_t gen = c->pool_gen;
+    c->keep_pool = at;
+    c->d_boff = c->d_boff_alt;
+    float mw = 0.f, mb = 0.f;
+    const int rc = walk_build(c, epoch, episode, c->build_stream, &mw, &mb);
+    c->keep_pool = nullptr;
+    c->next.valid = rc == NE_OK && c->built_epoch == (int64_t)epoch;
+    c->next.at = c->pool_at;
+    c->next.d_boff = c->d_boff;
+    c->next.boff.swap(c->boff);
+    c->next.epoch = epoch;
+    c->next.episode = episode;
+    c->next.ms_walk = mw;
+    c->next.ms_build = mb;
+    // restore the current pool (a buffer growth inside the build invalidated it)
+    const bool grown = c->pool_gen != gen;
+    c->pool_at = at;
+    c->boff.swap(boff);
+    c->d_boff = d_boff;  // d_boff_alt stays the array the next pool's offsets are in
+    c->built_epoch = grown ? -1 : be;
+    c->built_episode = grown ? -1 : bp;
+    return rc;
+}
+
+// Make c->next the current pool (the old current's block-offset array becomes
+// the alternate).
+void adopt_next(ne_ctx* c) {
+    c->pool_at = c->next.at;
+    c->boff.swap(c->next.boff);
+    std::swap(c->d_boff, c->d_boff_alt);  // d_boff_alt held next.d_boff
+    c->built_epoch = c->next.epoch;
+    c->built_episode = c->next.episode;
+    c->next.valid = false;
+}
+
+bool pipelined(const ne_ctx* c) { return c->pbufs.size() >= 3; }
 
 }  // namespace
 
@@ -916,17 +1039,18 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
         cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->build_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&c->d_loss, sizeof(double)) != cudaSuccess ||
         cudaMalloc(&c->d_bad, 3 * sizeof(unsigned long long)) != cudaSuccess)
         return bad(fail(c, NE_ECUDA, "stream/scratch setup failed on device %d", device));
-    c->stream = c->own_stream;
+    c->stream = c->ws = c->own_stream;
     *out = c;
     return NE_OK;
 }
 
 int ne_set_stream(ne_ctx* c, void* stream) {
     NE_TRY(enter(c));
-    c->stream = stream == NE_STREAM_OWN ? c->own_stream : stream ? (cudaStream_t)stream : cudaStreamLegacy;
+    c->stream = c->ws = stream == NE_STREAM_OWN ? c->own_stream : stream ? (cudaStream_t)stream : cudaStreamLegacy;
     return NE_OK;
 }
 
@@ -985,6 +1109,7 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     if (!reuse) free_all(c);
     c->loaded = false;
     c->walked_epoch = c->walked_episode = c->built_epoch = c->built_episode = -1;
+    c->next.valid = false;
     const ne_config& g = c->cfg;
     const uint32_t P = (uint32_t)c->world, k = g.subparts;
     c->n = n;
@@ -1164,6 +1289,7 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     // d_slots / d_pool / d_keys: sized by the first episode's pool (ensure_pool)
     if (!reuse) NE_TRY(dalloc(c, &c->d_scratch, ne::bucket_scratch_bytes(c->N_max, nb_local(c))));
     NE_ALLOC(c->d_boff, (size_t)nb_local(c) + 1);
+    NE_ALLOC(c->d_boff_alt, (size_t)nb_local(c) + 1);
 #undef NE_ALLOC
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
     c->loaded = true;
@@ -1177,6 +1303,7 @@ int ne_random_walk(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t* host_w
     if (c->cfg.walk_len == 0) return fail(c, NE_ESTATE, "LINE mode (walk_len=0) has no walks");
     if (episode >= c->cfg.episodes) return fail(c, NE_ERANGE, "episode=%u >= episodes=%u", episode, c->cfg.episodes);
     if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
+    c->next.valid = false;  // the walk and pair buffers are reused
     NE_TRY(do_walk(c, epoch, episode));
     const uint64_t total = c->walked_units * (c->cfg.walk_len + 1);
     if (walkers_out) *walkers_out = c->walked_units;
@@ -1195,6 +1322,7 @@ int ne_build_samples(ne_ctx* c, uint32_t epoch, uint32_t episode, uint64_t* n_sa
     if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
     if (c->cfg.walk_len > 0 && (c->walked_epoch != (int64_t)epoch || c->walked_episode != (int64_t)episode))
         return fail(c, NE_ESTATE, "no walks for epoch %u episode %u (call ne_random_walk)", epoch, episode);
+    c->next.valid = false;
     NE_TRY(do_build(c, epoch, episode));
     if (n_samples_out) *n_samples_out = c->boff.back();
     return NE_OK;
@@ -1223,24 +1351,51 @@ int ne_train_epoch(ne_ctx* c, uint32_t epoch, float lr, uint32_t flags, ne_stats
     if (flags & NE_REUSE_SAMPLES) {
         if (c->cfg.episodes != 1 || c->built_episode != 0)
             return fail(c, NE_ESTATE, "NE_REUSE_SAMPLES needs episodes == 1 and a built pool");
+        c->next.valid = false;
         NE_TRY(do_train(c, epoch, 0, lr, &acc));
     } else {
-        for (uint32_t e = 0; e < c->cfg.episodes; ++e) {
-            cudaEvent_t a = next_event(c), b = next_event(c), d = next_event(c);
-            NE_CUDA(c, cudaEventRecord(a, c->stream));
-            if (c->cfg.walk_len > 0) NE_TRY(do_walk(c, epoch, e));
-            NE_CUDA(c, cudaEventRecord(b, c->stream));
-            NE_TRY(do_build(c, epoch, e));  // synchronises the stream
+        // Walk engine decoupled from training ("we run our walk engine for
+        // the next epoch while embedding training engine trains samples for this
+        // epoch"): while episode e trains on the compute stream, the walk + pool
+        // of the next episode -- (epoch, e+1), or (epoch+1, 0) after the last one,
+        // kept for the next call -- are built on build_stream into the pair
+        // buffers the training pool does not occupy.  Needs the third pair
+        // buffer (ensure_pool); without it every build is serial.
+        static const int build_reserve = [] {  // SMs the SGNS grid leaves to a concurrent build
+            const char* e = std::getenv("NE_BUILD_RESERVE_SMS");
+            return e ? std::max(0, std::atoi(e)) : 0;
+        }();
+        const uint32_t E = c->cfg.episodes;
+        for (uint32_t e = 0; e < E; ++e) {
+            cudaEvent_t w0 = next_event(c), w1 = next_event(c);
+            NE_CUDA(c, cudaEventRecord(w0, c->stream));
+            if (c->next.valid && c->next.epoch == (int64_t)epoch && c->next.episode == (int64_t)e) {
+                acc.ms_walk += c->next.ms_walk;
+                acc.ms_build += c->next.ms_build;
+                adopt_next(c);
+            } else {
+                c->next.valid = false;
+                float mw = 0.f, mb = 0.f;
+                NE_TRY(walk_build(c, epoch, e, c->stream, &mw, &mb));
+                acc.ms_walk += mw;
+                acc.ms_build += mb;
+            }
             if (flags & NE_CHECK_BLOCKS) NE_TRY(ne_check_pool(c));
-            NE_CUDA(c, cudaEventRecord(d, c->stream));
-            NE_CUDA(c, cudaEventSynchronize(d));
-            float mw = 0.f, mb = 0.f;
-            NE_CUDA(c, cudaEventElapsedTime(&mw, a, b));
-            NE_CUDA(c, cudaEventElapsedTime(&mb, b, d));
-            acc.ms_walk += mw;
-            acc.ms_build += mb;
+            NE_CUDA(c, cudaEventRecord(w1, c->stream));
+            const bool more = e + 1 < E || epoch + 1 < (1u << 24);
+            const bool pre = more && pipelined(c);
+            TrainPending tp;
+            c->sgns_reserve = pre ? build_reserve : 0;
+            int rc = launch_train(c, epoch, e, lr, tp);
+            c->sgns_reserve = 0;
+            if (rc == NE_OK && pre) rc = prebuild_next(c, e + 1 < E ? epoch : epoch + 1, e + 1 < E ? e + 1 : 0);
+            const int rf = finish_train(c, tp, &acc);
+            NE_TRY(rc);
+            NE_TRY(rf);
+            float gap = 0.f;
+            NE_CUDA(c, cudaEventElapsedTime(&gap, w0, w1));
+            acc.ms_pool_wait += gap;
             c->ev_used = 0;
-            NE_TRY(do_train(c, epoch, e, lr, &acc));
         }
     }
     acc.kernel_launches = c->launches - l0;
@@ -1478,6 +1633,7 @@ void ne_destroy(ne_ctx* c) {
     if (c->stage_done) cudaEventDestroy(c->stage_done);
     if (c->h_V) cudaFreeHost(c->h_V);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->build_stream) cudaStreamDestroy(c->build_stream);
     if (c->comm_walk) ncclCommDestroy(c->comm_walk);
     if (c->comm) ncclCommDestroy(c->comm);
     if (c->d_loss) cudaFree(c->d_loss);

@@ -44,7 +44,7 @@ class ne_config(C.Structure):
 class ne_stats(C.Structure):
     _fields_ = [("samples", C.c_uint64), ("loss_sum", C.c_double), ("ms_walk", C.c_float),
                 ("ms_build", C.c_float), ("ms_train", C.c_float), ("ms_comm_wait", C.c_float),
-                ("train_launches", C.c_uint32), ("kernel_launches", C.c_uint32)]
+                ("train_launches", C.c_uint32), ("kernel_launches", C.c_uint32), ("ms_pool_wait", C.c_float)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
