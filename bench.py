@@ -297,7 +297,7 @@ def main():
     train_launches = sum(st["train_launches"] for st in stats)
     t = torch.tensor([ms, samples, ms_train, launches, sum(st["ms_walk"] for st in stats),
                       sum(st["ms_build"] for st in stats), sum(st["ms_comm_wait"] for st in stats),
-                      train_launches], dtype=torch.float64, device="cuda")
+                      train_launches, sum(st["ms_pool_wait"] for st in stats)], dtype=torch.float64, device="cuda")
     if world > 1:
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -390,7 +390,10 @@ def main():
             "phases_ms_per_step": {"walk": float(tsum[4]) / world / args.steps,
                                    "build": float(tsum[5]) / world / args.steps,
                                    "train": float(tsum[2]) / world / args.steps,
-                                   "comm_wait": float(tsum[6]) / world / args.steps},
+                                   "comm_wait": float(tsum[6]) / world / args.steps,
+                                   # walk + build time the compute stream waited for (the rest ran
+                                   # on the build stream behind training)
+                                   "pool_wait_exposed": float(tsum[8]) / world / args.steps},
             "cpu_baseline": cpu,
             "e2e": {"value": e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     # trained vertex + context rows of rank 0, CSR validation flags + offsets ends (32 B),

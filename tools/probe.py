@@ -28,5 +28,5 @@ for ep in range(epochs):
     wall = time.time() - t
     B = 8 + 8 * 5 + (4 if storage else 8) * w.dim * 7
     print(f"k={subparts} rule={rule} epoch {ep}: wall {wall:.3f}s samples {st['samples']} walk {st['ms_walk']:.1f}ms build {st['ms_build']:.1f}ms "
-          f"train {st['ms_train']:.1f}ms -> {st['samples']/st['ms_train']/1e3:.1f} M samples/s kernel, "
+          f"train {st['ms_train']:.1f}ms exposed-build {st['ms_pool_wait']:.1f}ms -> {st['samples']/st['ms_train']/1e3:.1f} M samples/s kernel, "
           f"{st['samples']*B/st['ms_train']/1e6:.0f} GB/s alg; loss/sample {st['loss_sum']/max(st['samples'],1)/6:.4f}", flush=True)
