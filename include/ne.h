@@ -66,6 +66,9 @@ enum { NE_UPDATE_SEQUENTIAL = 0, NE_UPDATE_ACCUMULATED = 1 };
 /* ne_config.staging */
 enum { NE_STAGE_DEVICE = 0, NE_STAGE_HOST = 1 };
 
+/* ne_config.transport: how vertex sub-parts travel the ring (world > 1) */
+enum { NE_TRANSPORT_NCCL = 0, NE_TRANSPORT_IPC = 1 };
+
 /* ne_config.storage */
 enum { NE_STORE_F32 = 0, NE_STORE_BF16 = 1 };
 
@@ -129,7 +132,13 @@ typedef struct {
                                 ne_get/set_embeddings still take fp32 host arrays; the
                                 ring and host staging move bf16 sub-parts (half the
                                 bytes).                                                 */
-    uint32_t reserved;       /* must be 0                                               */
+    uint32_t transport;      /* NE_TRANSPORT_NCCL (0): ncclSend/Recv on the comm stream;
+                                NE_TRANSPORT_IPC (1): copy-engine pushes over CUDA IPC
+                                into rank+1's slots, ordered by GPU-side flag waits
+                                (no SM kernels; ne_ipc_export / ne_ipc_connect after
+                                ne_load_graph).  With IPC, ne_init_dist may take
+                                id == NULL: no NCCL at all (each rank then builds its
+                                part's pool from every walker, the layout-only way). */
     uint64_t seed;           /* Philox key (contract R1)                                */
 } ne_config;
 
@@ -180,6 +189,19 @@ int ne_join(ne_ctx *ctx);
  * GPU").  Errors: NE_EINVAL, NE_ESTATE (graph already loaded), NE_ENCCL. */
 int ne_get_nccl_id(uint8_t id[128]);
 int ne_init_dist(ne_ctx *ctx, int rank, int world, const uint8_t id[128]);
+
+/* Copy-engine ring bootstrap (transport == NE_TRANSPORT_IPC, world > 1).
+ * After ne_load_graph every rank exports one blob of ne_ipc_blob_size()
+ * bytes (the CUDA IPC handle of its vertex-slot region); the harness
+ * all-gathers them in rank order (e.g. torch.distributed) and every rank
+ * calls ne_ipc_connect with the world * blob_size bytes.  Must be repeated
+ * after a reload that changes the graph's shape.  Before any rank destroys
+ * its context, all ranks must be done training (ne_destroy drains the ring).
+ * Errors: NE_ESTATE (wrong transport, no graph), NE_EINVAL (blob mismatch),
+ * NE_ECUDA. */
+size_t ne_ipc_blob_size(void);
+int ne_ipc_export(ne_ctx *ctx, void *blob, size_t cap);
+int ne_ipc_connect(ne_ctx *ctx, const void *blobs, size_t blob_size);
 
 /* Load the graph G = (V, E) as CSR: offsets[n+1] (u64),
  * targets[nnz] (u32), validated on the device against S:24 (offsets

@@ -1,0 +1,223 @@
+// ring_ipc.cpp -- the ring of vertex sub-parts (O7) moved by
+// the copy engines over CUDA IPC instead of NCCL's SM kernels
+// (cfg.transport == NE_TRANSPORT_IPC).
+//
+// Every rank allocates its 2k vertex slots (two ping-pong halves of k
+// sub-part slots) and 2k u32 flags as ONE cudaMalloc region, exports it
+// (ne_ipc_export), and maps the regions of ranks g-1 and g+1 (ne_ipc_connect;
+// the harness all-gathers the handles).  After training (round r, slot t) rank
+// g pushes the sub-part with one cudaMemcpyAsync on its comm stream straight
+// into the other half of rank g+1's slot t -- a copy-engine transfer over
+// NVLink between GPUs (a plain device copy when two processes share a GPU),
+// no SM involved.  Ordering uses monotonic per-slot counters in the flag
+// words, waited on and written by the GPU front end (cuStreamWaitValue32 /
+// cuStreamWriteValue32, no kernel, no host round trip):
+//   * push i of slot t into g+1 first waits credit[t] >= i - 1 at g: rank
+//     g+1's own push i-1 of slot t -- the sub-part that occupied the target
+//     half -- has left;
+//   * after the copy, g writes arrived[t] = i at g+1 and credit[t] = i at g-1
+//     (g's push i freed the half g-1's push i+1 will land in);
+//   * before training slot t in every round but the first after a load, g
+//     waits arrived[t] >= (its next expected arrival).
+// The counters never reset while the region lives, so a rank can never clear
+// a flag a fast peer has already advanced.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "ne_ctx.h"
+
+namespace {
+
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct DriverOps {
+    WaitFn wait = nullptr;
+    WriteFn write = nullptr;
+    bool ok = false;
+};
+
+const DriverOps& ops() {
+    static DriverOps d = [] {
+        DriverOps o;
+        cudaDriverEntryPointQueryResult q1, q2;
+        void *w = nullptr, *x = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWriteValue32", &x, cudaEnableDefault, &q2) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess) {
+            o.wait = reinterpret_cast<WaitFn>(w);
+            o.write = reinterpret_cast<WriteFn>(x);
+            o.ok = true;
+        }
+        cudaGetLastError();
+        return o;
+    }();
+    return d;
+}
+
+// The exported description of a rank's region.
+struct Blob {
+    uint32_t magic, rank, world, subparts;
+    uint64_t region_bytes, slot_bytes;
+    cudaIpcMemHandle_t handle;
+};
+constexpr uint32_t kMagic = 0x4E455250u;  // "NERP"
+
+uint32_t* flags_of(const ne_ctx* c, void* region) {
+    return reinterpret_cast<uint32_t*>(static_cast<char*>(region) + 2ull * c->cfg.subparts * c->ipc.slot_bytes);
+}
+
+int wait_ge(ne_ctx* c, cudaStream_t s, const uint32_t* flag, uint32_t value) {
+    const CUresult r = ops().wait((CUstream)s, (CUdeviceptr)flag, value, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return ne_fail(c, NE_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+    return NE_OK;
+}
+
+int write_flag(ne_ctx* c, cudaStream_t s, uint32_t* flag, uint32_t value) {
+    const CUresult r = ops().write((CUstream)s, (CUdeviceptr)flag, value, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return ne_fail(c, NE_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+    return NE_OK;
+}
+
+void close_peers(ne_ctx* c) {
+    if (c->ipc.next_region) cudaIpcCloseMemHandle(c->ipc.next_region);
+    if (c->ipc.prev_region && c->ipc.prev_region != c->ipc.next_region) cudaIpcCloseMemHandle(c->ipc.prev_region);
+    c->ipc.next_region = c->ipc.prev_region = nullptr;
+    c->ipc.connected = false;
+}
+
+}  // namespace
+
+bool ipc_ring(const ne_ctx* c) { return c->world > 1 && c->cfg.transport == NE_TRANSPORT_IPC; }
+
+int ipc_alloc_slots(ne_ctx* c, size_t slot_bytes, size_t nslots) {
+    const uint32_t k = c->cfg.subparts;
+    slot_bytes = (slot_bytes + 255) & ~(size_t)255;
+    const size_t bytes = nslots * slot_bytes + 2ull * k * sizeof(uint32_t);
+    if (!ops().ok) return ne_fail(c, NE_ECUDA, "stream memory operations (cuStreamWaitValue32) unavailable");
+    if (c->ipc.region && c->ipc.region_bytes == bytes) {  // same shape: keep region, flags and counters
+        for (size_t i = 0; i < nslots; ++i) c->vslot[i] = reinterpret_cast<float*>(static_cast<char*>(c->ipc.region) + i * slot_bytes);
+        return NE_OK;
+    }
+    ipc_release(c);
+    NE_CUDA(c, cudaMalloc(&c->ipc.region, bytes));
+    c->ipc.region_bytes = bytes;
+    c->ipc.slot_bytes = slot_bytes;
+    c->ipc.flags = flags_of(c, c->ipc.region);
+    NE_CUDA(c, cudaMemset(c->ipc.flags, 0, 2ull * k * sizeof(uint32_t)));
+    c->ipc.pushed.assign(k, 0);
+    c->ipc.waited.assign(k, 0);
+    c->ipc.started = false;
+    for (size_t i = 0; i < nslots; ++i) c->vslot[i] = reinterpret_cast<float*>(static_cast<char*>(c->ipc.region) + i * slot_bytes);
+    return NE_OK;
+}
+
+int ipc_reset_on_load(ne_ctx* c) {
+    // the previous calls' return-home pushes into this rank were drained; the
+    // re-initialised home sub-parts need no arrival
+    c->ipc.waited = c->ipc.pushed;
+    c->ipc.started = false;
+    return NE_OK;
+}
+
+int ipc_wait_arrival(ne_ctx* c, uint32_t t) {
+    if (!c->ipc.started) return NE_OK;
+    return wait_ge(c, c->stream, c->ipc.flags + t, ++c->ipc.waited[t]);
+}
+
+int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after) {
+    if (!c->ipc.connected) return ne_fail(c, NE_ESTATE, "IPC ring not connected (ne_ipc_export / ne_ipc_connect)");
+    const uint32_t k = c->cfg.subparts;
+    const uint32_t i = ++c->ipc.pushed[t];
+    NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, after, 0));
+    if (i > 1) NE_TRY(wait_ge(c, c->comm_stream, c->ipc.flags + k + t, i - 1));  // credit: the target half is free
+    const size_t half = (size_t)(1 - c->cur) * k + t;                            // the other half of rank + 1
+    char* dst = static_cast<char*>(c->ipc.next_region) + half * c->ipc.slot_bytes;
+    NE_CUDA(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
+    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.next_region) + t, i));      // arrived at rank + 1
+    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.prev_region) + k + t, i));  // credit at rank - 1
+    c->ipc.started = true;
+    return NE_OK;
+}
+
+int ipc_drain(ne_ctx* c, bool host_sync) {
+    if (!c->ipc.region || !c->ipc.connected) return NE_OK;
+    const uint32_t k = c->cfg.subparts;
+    for (uint32_t t = 0; t < k; ++t) {
+        if (!c->ipc.pushed[t]) continue;
+        NE_TRY(wait_ge(c, c->stream, c->ipc.flags + t, c->ipc.pushed[t]));      // every push into me landed
+        NE_TRY(wait_ge(c, c->stream, c->ipc.flags + k + t, c->ipc.pushed[t]));  // rank + 1 is done with mine
+        c->ipc.waited[t] = c->ipc.pushed[t];
+    }
+    c->ipc.started = false;
+    if (host_sync) {
+        NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));
+        NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    return NE_OK;
+}
+
+void ipc_release(ne_ctx* c) {
+    close_peers(c);
+    if (c->ipc.region) cudaFree(c->ipc.region);
+    c->ipc.region = nullptr;
+    c->ipc.flags = nullptr;
+    c->ipc.region_bytes = c->ipc.slot_bytes = 0;
+    c->ipc.started = false;
+}
+
+extern "C" {
+
+size_t ne_ipc_blob_size(void) { return sizeof(Blob); }
+
+int ne_ipc_export(ne_ctx* c, void* blob, size_t cap) {
+    if (!c || !blob) return NE_EINVAL;
+    c->err.clear();
+    NE_CUDA(c, cudaSetDevice(c->device));
+    if (!ipc_ring(c)) return ne_fail(c, NE_ESTATE, "transport is not NE_TRANSPORT_IPC or world == 1");
+    if (!c->ipc.region) return ne_fail(c, NE_ESTATE, "no vertex slots yet (call ne_load_graph first)");
+    if (cap < sizeof(Blob)) return ne_fail(c, NE_ERANGE, "blob capacity %zu < %zu", cap, sizeof(Blob));
+    Blob b{};
+    b.magic = kMagic;
+    b.rank = (uint32_t)c->rank;
+    b.world = (uint32_t)c->world;
+    b.subparts = c->cfg.subparts;
+    b.region_bytes = c->ipc.region_bytes;
+    b.slot_bytes = c->ipc.slot_bytes;
+    NE_CUDA(c, cudaIpcGetMemHandle(&b.handle, c->ipc.region));
+    std::memcpy(blob, &b, sizeof b);
+    return NE_OK;
+}
+
+int ne_ipc_connect(ne_ctx* c, const void* blobs, size_t blob_size) {
+    if (!c || !blobs) return NE_EINVAL;
+    c->err.clear();
+    NE_CUDA(c, cudaSetDevice(c->device));
+    if (!ipc_ring(c)) return ne_fail(c, NE_ESTATE, "transport is not NE_TRANSPORT_IPC or world == 1");
+    if (blob_size != sizeof(Blob)) return ne_fail(c, NE_EINVAL, "blob size %zu != %zu", blob_size, sizeof(Blob));
+    const uint32_t P = (uint32_t)c->world, g = (uint32_t)c->rank;
+    Blob nb, pb;
+    std::memcpy(&nb, static_cast<const char*>(blobs) + ((g + 1) % P) * blob_size, sizeof nb);
+    std::memcpy(&pb, static_cast<const char*>(blobs) + ((g + P - 1) % P) * blob_size, sizeof pb);
+    for (const Blob* b : {&nb, &pb})
+        if (b->magic != kMagic || b->world != P || b->subparts != c->cfg.subparts ||
+            b->region_bytes != c->ipc.region_bytes || b->slot_bytes != c->ipc.slot_bytes)
+            return ne_fail(c, NE_EINVAL, "IPC blob of rank %u does not match this ring (world %u, subparts %u, "
+                                         "region %llu bytes)", b->rank, P, c->cfg.subparts,
+                           (unsigned long long)c->ipc.region_bytes);
+    if (nb.rank != (g + 1) % P || pb.rank != (g + P - 1) % P)
+        return ne_fail(c, NE_EINVAL, "IPC blobs out of rank order");
+    close_peers(c);
+    NE_CUDA(c, cudaIpcOpenMemHandle(&c->ipc.next_region, nb.handle, cudaIpcMemLazyEnablePeerAccess));
+    if (P == 2) {
+        c->ipc.prev_region = c->ipc.next_region;
+    } else {
+        NE_CUDA(c, cudaIpcOpenMemHandle(&c->ipc.prev_region, pb.handle, cudaIpcMemLazyEnablePeerAccess));
+    }
+    c->ipc.connected = true;
+    return NE_OK;
+}
+
+}  // extern "C"

@@ -26,114 +26,9 @@
 
 #include "ne.h"
 #include "ne_internal.h"
+#include "ne_ctx.h"
 
-struct ne_ctx {
-    ne_config cfg{};
-    int device = 0;
-    ne::Device dev;
-    cudaStream_t own_stream = nullptr, stream = nullptr, comm_stream = nullptr;
-    cudaStream_t build_stream = nullptr;  // walk + pool build of the next episode, behind training
-    cudaStream_t ws = nullptr;            // the stream walk / build kernels go to: stream, or build_stream
-                                          // while a pipelined build runs
-    ne_alloc_fn alloc = nullptr;
-    ne_free_fn free_fn = nullptr;
-    void* user = nullptr;
-    int rank = 0, world = 1;
-    ncclComm_t comm = nullptr;
-    ncclComm_t comm_walk = nullptr;  // split of comm for the walk all-gather: NCCL serialises the
-                                     // operations of one communicator, and the ring's last
-                                     // return-home transfers would otherwise delay the next walk
-    std::string err;
-
-    struct Alloc { void* p; size_t bytes; };
-    std::vector<Alloc> allocs;
-
-    bool loaded = false;
-    uint64_t n = 0, nnz = 0;
-    uint64_t* d_off = nullptr;
-    uint32_t* d_tgt = nullptr;
-    std::vector<uint64_t> part_bounds, sub_bounds;
-    uint64_t* d_sub_bounds = nullptr;
-    uint2* d_alias = nullptr;
-    float* d_C = nullptr;
-    uint64_t c_begin = 0, c_count = 0;
-    std::vector<float*> vslot;  // ring: 2k buffers (ping-pong); one GPU: k; host staging: 3
-    float* h_V = nullptr;       // host staging: this rank's vertex rows, pinned
-    size_t h_V_bytes = 0;
-    cudaStream_t copy_stream = nullptr;  // host staging H2D (D2H uses comm_stream)
-    cudaEvent_t stage_done = nullptr;    // last D2H of a call (deferred like ring_done)
-    bool stage_pending = false;
-    int cur = 0;                // half [cur*k, cur*k+k) holds the current sub-parts
-    uint64_t max_sub_rows = 0;
-
-    uint32_t Pw = 1;
-    uint64_t units_total = 0, units_max = 0, N_max = 0;
-    uint32_t* d_walks = nullptr;
-    uint32_t* d_slot_tab = nullptr;
-    std::vector<uint64_t*> pbufs;  // 2 pair buffers, or 3 when the next episode's pool is built during training
-    uint64_t* d_slots = nullptr;   // the two pbufs a build uses (sink / radix ping-pong)
-    uint32_t* d_keys[2] = {nullptr, nullptr};  // keyed pool sink + radix ping-pong (nullptr: direct sink)
-    uint64_t* d_pool = nullptr;
-    uint64_t* pool_at = nullptr;  // the buffer (d_pool or d_slots) holding the built pool
-    bool walk_counts = false;     // d_counts holds the O5 counts of the current walk (unsharded walk)
-    uint64_t shard_units = 0;     // world > 1 with NCCL: walkers of this rank's shard in d_walks (from row 0)
-    uint64_t* d_part_bounds = nullptr;  // P + 1 context-part bounds (sharded construction)
-    uint64_t* d_tmat = nullptr;         // P x P (shard, part) pair counts of the episode (sharded construction)
-    std::vector<uint64_t> tmat;
-    uint64_t pool_cap = 0;        // pairs d_slots / d_pool (and d_keys) hold; grown by ensure_pool
-    float* d_tmp_f32 = nullptr;   // bf16 rows: fp32 staging of ne_get/set_embeddings
-    uint64_t tmp_f32_cap = 0;
-    void* d_scratch = nullptr;
-    uint32_t* d_counts = nullptr;   // per-unit kept-pair counts (O5)
-    uint64_t* d_base = nullptr;     // their exclusive scan: part-local index bases
-    void* d_scan_scratch = nullptr;
-    uint64_t* d_total = nullptr;    // N_g of the episode
-    uint64_t* d_boff = nullptr;
-    std::vector<uint64_t> boff;
-    // the next episode's pool, built on build_stream while the current one trains
-    struct NextPool {
-        bool valid = false;
-        uint64_t* at = nullptr;
-        uint64_t* d_boff = nullptr;
-        std::vector<uint64_t> boff;
-        int64_t epoch = -1, episode = -1;
-        float ms_walk = 0.f, ms_build = 0.f;
-    } next;
-    uint64_t* d_boff_alt = nullptr;
-    const uint64_t* keep_pool = nullptr;  // pool in training while a build runs (select_scratch skips it)
-    int sgns_reserve = 0;                 // SMs the SGNS grid leaves free (concurrent pool build)
-    uint64_t pool_gen = 0;                // bumped whenever ensure_pool reallocates the pair buffers
-    double* d_loss = nullptr;
-    unsigned long long* d_bad = nullptr;
-    bool n2v = false;           // node2vec walks (p, q != 1)
-    uint64_t n2v_thr[3] = {0, 0, 0};
-    uint32_t* d_tmp_u32 = nullptr;
-    size_t tmp_u32_cap = 0;
-
-    int64_t walked_epoch = -1, walked_episode = -1;
-    int64_t built_epoch = -1, built_episode = -1;
-    uint64_t walked_units = 0;
-
-    std::vector<cudaEvent_t> ev_pool;
-    size_t ev_used = 0;
-    // recorded on the comm stream after the last ring transfers of a call (the
-    // "return home" sends, still in flight when ne_train_samples returns); the
-    // next call's first training of every slot waits on it
-    cudaEvent_t ring_done = nullptr;
-    bool ring_pending = false;
-    uint32_t launches = 0;
-    std::shared_ptr<void> alias_scratch;  // host buffers reused across ne_load_graph calls
-    std::vector<uint2> alias_host;
-    std::vector<uint64_t> alias_deg;      // context-part degrees the alias builder reads
-    std::thread alias_thread;             // host alias build, overlapped with walk + pool build
-    bool alias_pending = false;
-};
-
-namespace {
-
-thread_local std::string g_create_error;  // ne_last_error(NULL) after a failed ne_create
-
-int fail(ne_ctx* c, int code, const char* fmt, ...) {
+int ne_fail(ne_ctx* c, int code, const char* fmt, ...) {
     static const char* names[] = {"NE_OK", "NE_EINVAL", "NE_ERANGE", "NE_ENOMEM", "NE_ESTATE",
                                   "NE_ECUDA", "NE_ENCCL", "NE_ESCHED"};
     char buf[512];
@@ -145,26 +40,11 @@ int fail(ne_ctx* c, int code, const char* fmt, ...) {
     return code;
 }
 
-#define NE_CUDA(ctx, call)                                                                  \
-    do {                                                                                    \
-        cudaError_t e_ = (call);                                                            \
-        if (e_ != cudaSuccess)                                                              \
-            return fail(ctx, NE_ECUDA, "%s (%s:%d %s)", cudaGetErrorString(e_), __FILE__,   \
-                        __LINE__, #call);                                                   \
-    } while (0)
 
-#define NE_NCCL(ctx, call)                                                                  \
-    do {                                                                                    \
-        ncclResult_t r_ = (call);                                                           \
-        if (r_ != ncclSuccess)                                                              \
-            return fail(ctx, NE_ENCCL, "%s (%s:%d)", ncclGetErrorString(r_), __FILE__, __LINE__); \
-    } while (0)
+namespace {
 
-#define NE_TRY(expr)            \
-    do {                        \
-        int rc_ = (expr);       \
-        if (rc_ != NE_OK) return rc_; \
-    } while (0)
+thread_local std::string g_create_error;  // ne_last_error(NULL) after a failed ne_create
+
 
 void partition(uint64_t begin, uint64_t end, uint32_t parts, uint64_t* out) {
     const uint64_t len = end - begin, q = len / parts, r = len % parts;
@@ -180,12 +60,12 @@ int dalloc(ne_ctx* c, void** out, size_t bytes) {
     void* p = nullptr;
     if (c->alloc) {
         p = c->alloc(bytes, c->device, (void*)c->stream, c->user);
-        if (!p) return fail(c, NE_ENOMEM, "allocator callback returned NULL for %zu bytes", bytes);
+        if (!p) return ne_fail(c, NE_ENOMEM, "allocator callback returned NULL for %zu bytes", bytes);
     } else {
         cudaError_t e = cudaMalloc(&p, bytes);
         if (e != cudaSuccess) {
             cudaGetLastError();
-            return fail(c, NE_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+            return ne_fail(c, NE_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
         }
     }
     c->allocs.push_back({p, bytes});
@@ -390,7 +270,7 @@ int enter(ne_ctx* c) {
 }
 
 int check_loaded(ne_ctx* c) {
-    if (!c->loaded) return fail(c, NE_ESTATE, "no graph loaded (call ne_load_graph first)");
+    if (!c->loaded) return ne_fail(c, NE_ESTATE, "no graph loaded (call ne_load_graph first)");
     return NE_OK;
 }
 
@@ -605,7 +485,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         send_max = std::max(send_max, S);
     }
     recv_off[P] = N;
-    if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
+    if (N > c->N_max) return ne_fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
                                   (unsigned long long)c->N_max);
     NE_TRY(ensure_pool(c, std::max(N, send_max)));
     select_scratch(c, c->keep_pool);
@@ -685,7 +565,7 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         NE_CUDA(c, cudaMemcpyAsync(&N, c->d_total, sizeof N, cudaMemcpyDeviceToHost, c->ws));
         NE_CUDA(c, cudaStreamSynchronize(c->ws));
     }
-    if (N > c->N_max) return fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
+    if (N > c->N_max) return ne_fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
                                   (unsigned long long)c->N_max);
     NE_TRY(ensure_pool(c, N));
     select_scratch(c, c->keep_pool);
@@ -808,15 +688,22 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
     if (c->cfg.staging == NE_STAGE_HOST) return launch_train_staged(c, epoch, episode, lr, tp);
     const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank;
     const uint64_t d = c->cfg.dim;
-    if (P > 1 && !c->comm)
-        return fail(c, NE_ESTATE, "world=%u context has no NCCL communicator (layout-only)", P);
+    const bool ipc = ipc_ring(c);
+    if (P > 1 && !c->comm && !ipc)
+        return ne_fail(c, NE_ESTATE, "world=%u context has no NCCL communicator (layout-only)", P);
     std::vector<cudaEvent_t> recv(k, nullptr);
     if (c->ring_pending) recv.assign(k, c->ring_done);  // home-coming sub-parts of the last call
     for (uint32_t r = 0; r < P; ++r) {
         for (uint32_t t = 0; t < k; ++t) {
             const uint32_t vs = (uint32_t)plan_vsub(P, k, r, t, g);
             float* V = c->vslot[c->cur * k + t];
-            if (recv[t]) {
+            if (ipc && (r > 0 || c->ipc.started)) {  // the sub-part of this slot has landed
+                cudaEvent_t w0 = next_event(c), w1 = next_event(c);
+                NE_CUDA(c, cudaEventRecord(w0, c->stream));
+                NE_TRY(ipc_wait_arrival(c, t));
+                NE_CUDA(c, cudaEventRecord(w1, c->stream));
+                tp.waits.push_back({w0, w1});
+            } else if (recv[t]) {
                 cudaEvent_t w0 = next_event(c), w1 = next_event(c);
                 NE_CUDA(c, cudaEventRecord(w0, c->stream));
                 NE_CUDA(c, cudaStreamWaitEvent(c->stream, recv[t], 0));
@@ -831,7 +718,10 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
             if (sp.count) { c->launches += 1; tp.launches += 1; }
             tp.timed.push_back({e0, e1});
             tp.samples += sp.count;
-            if (P > 1) {
+            if (P > 1 && ipc) {  // copy-engine push into rank + 1 (ring_ipc.cpp)
+                const uint64_t send_rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
+                NE_TRY(ipc_push(c, t, V, send_rows * d * elem_bytes(c), e1));
+            } else if (P > 1) {
                 const uint32_t vs_next = (uint32_t)plan_vsub(P, k, r + 1, t, g);
                 const uint64_t send_rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
                 const uint64_t recv_rows = c->sub_bounds[vs_next + 1] - c->sub_bounds[vs_next];
@@ -854,7 +744,7 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
     // episode's walk and pool build overlap the transfers); every reader of the
     // vertex slots (get/set embeddings, reload, destroy) drains the comm stream.
     c->ring_pending = false;
-    if (P > 1) {
+    if (P > 1 && !ipc) {
         if (!c->ring_done) NE_CUDA(c, cudaEventCreateWithFlags(&c->ring_done, cudaEventDisableTiming));
         NE_CUDA(c, cudaEventRecord(c->ring_done, c->comm_stream));
         c->ring_pending = true;
@@ -899,11 +789,11 @@ int walk_build(ne_ctx* c, uint32_t epoch, uint32_t episode, cudaStream_t s, floa
     c->ws = s;
     cudaEvent_t a = next_event(c), b = next_event(c), d = next_event(c);
     int rc = NE_OK;
-    if (cudaEventRecord(a, s) != cudaSuccess) rc = fail(c, NE_ECUDA, "event record");
+    if (cudaEventRecord(a, s) != cudaSuccess) rc = ne_fail(c, NE_ECUDA, "event record");
     if (rc == NE_OK && c->cfg.walk_len > 0) rc = do_walk(c, epoch, episode);
-    if (rc == NE_OK && cudaEventRecord(b, s) != cudaSuccess) rc = fail(c, NE_ECUDA, "event record");
+    if (rc == NE_OK && cudaEventRecord(b, s) != cudaSuccess) rc = ne_fail(c, NE_ECUDA, "event record");
     if (rc == NE_OK) rc = do_build(c, epoch, episode);  // synchronises s
-    if (rc == NE_OK && cudaEventRecord(d, s) != cudaSuccess) rc = fail(c, NE_ECUDA, "event record");
+    if (rc == NE_OK && cudaEventRecord(d, s) != cudaSuccess) rc = ne_fail(c, NE_ECUDA, "event record");
     c->ws = c->stream;
     NE_TRY(rc);
     NE_CUDA(c, cudaEventSynchronize(d));
@@ -979,7 +869,7 @@ int ne_partition_bounds(uint64_t n, uint32_t parts, uint64_t* bounds) {
 int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
               ne_free_fn free_fn, void* user) {
     g_create_error.clear();
-    if (!out || !cfg) return fail(nullptr, NE_EINVAL, "null argument");
+    if (!out || !cfg) return ne_fail(nullptr, NE_EINVAL, "null argument");
     *out = nullptr;
     ne_ctx* c = new ne_ctx();
     c->cfg = *cfg;
@@ -994,23 +884,24 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     };
     const ne_config& g = *cfg;
     if (g.dim == 0 || g.dim % 4 || g.dim > 512)
-        return bad(fail(c, NE_EINVAL, "dim=%u must be a multiple of 4 in [4, 512]", g.dim));
-    if (g.negatives > 8) return bad(fail(c, NE_EINVAL, "negatives=%u > 8", g.negatives));
-    if (g.walk_len > 255) return bad(fail(c, NE_EINVAL, "walk_len=%u > 255", g.walk_len));
+        return bad(ne_fail(c, NE_EINVAL, "dim=%u must be a multiple of 4 in [4, 512]", g.dim));
+    if (g.negatives > 8) return bad(ne_fail(c, NE_EINVAL, "negatives=%u > 8", g.negatives));
+    if (g.walk_len > 255) return bad(ne_fail(c, NE_EINVAL, "walk_len=%u > 255", g.walk_len));
     if (g.walk_len > 0 && (g.window == 0 || g.window > g.walk_len))
-        return bad(fail(c, NE_EINVAL, "window=%u not in [1, walk_len=%u]", g.window, g.walk_len));
+        return bad(ne_fail(c, NE_EINVAL, "window=%u not in [1, walk_len=%u]", g.window, g.walk_len));
     if (g.walk_len > 0 && g.walks_per_node == 0)
-        return bad(fail(c, NE_EINVAL, "walks_per_node must be >= 1"));
+        return bad(ne_fail(c, NE_EINVAL, "walks_per_node must be >= 1"));
     if (g.episodes == 0 || g.episodes > 4095)
-        return bad(fail(c, NE_EINVAL, "episodes=%u not in [1, 4095]", g.episodes));
-    if (g.writeback > NE_WB_STORE) return bad(fail(c, NE_EINVAL, "writeback=%u not in {0, 1}", g.writeback));
+        return bad(ne_fail(c, NE_EINVAL, "episodes=%u not in [1, 4095]", g.episodes));
+    if (g.writeback > NE_WB_STORE) return bad(ne_fail(c, NE_EINVAL, "writeback=%u not in {0, 1}", g.writeback));
     if (g.update_rule > NE_UPDATE_ACCUMULATED)
-        return bad(fail(c, NE_EINVAL, "update_rule=%u not in {0, 1}", g.update_rule));
-    if (g.staging > NE_STAGE_HOST) return bad(fail(c, NE_EINVAL, "staging=%u not in {0, 1}", g.staging));
-    if (g.storage > NE_STORE_BF16) return bad(fail(c, NE_EINVAL, "storage=%u not in {0, 1}", g.storage));
-    if (g.reserved != 0) return bad(fail(c, NE_EINVAL, "reserved=%u must be 0", g.reserved));
+        return bad(ne_fail(c, NE_EINVAL, "update_rule=%u not in {0, 1}", g.update_rule));
+    if (g.staging > NE_STAGE_HOST) return bad(ne_fail(c, NE_EINVAL, "staging=%u not in {0, 1}", g.staging));
+    if (g.storage > NE_STORE_BF16) return bad(ne_fail(c, NE_EINVAL, "storage=%u not in {0, 1}", g.storage));
+    if (g.transport > NE_TRANSPORT_IPC)
+        return bad(ne_fail(c, NE_EINVAL, "transport=%u not in {0 (NCCL), 1 (IPC)}", g.transport));
     if (!(g.p >= 0.f) || !(g.q >= 0.f))
-        return bad(fail(c, NE_EINVAL, "node2vec p=%g q=%g must be > 0 (0 = 1)", g.p, g.q));
+        return bad(ne_fail(c, NE_EINVAL, "node2vec p=%g q=%g must be > 0 (0 = 1)", g.p, g.q));
     {
         // node2vec thresholds (NEXT-1): alpha = 1/p, 1, 1/q scaled by their max to 2^32
         const double pp = g.p == 0.f ? 1.0 : (double)g.p, qq = g.q == 0.f ? 1.0 : (double)g.q;
@@ -1021,17 +912,17 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
             c->n2v_thr[i] = w[i] == mx ? (1ull << 32) : (uint64_t)(w[i] / mx * 4294967296.0);
     }
     if (g.subparts == 0 || g.subparts > 256)
-        return bad(fail(c, NE_EINVAL, "subparts=%u not in [1, 256]", g.subparts));
+        return bad(ne_fail(c, NE_EINVAL, "subparts=%u not in [1, 256]", g.subparts));
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || device < 0 || device >= ndev) {
         cudaGetLastError();
-        return bad(fail(c, NE_ECUDA, "no CUDA device %d (%s)", device,
+        return bad(ne_fail(c, NE_ECUDA, "no CUDA device %d (%s)", device,
                         e != cudaSuccess ? cudaGetErrorString(e) : "out of range"));
     }
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major != 10)
-        return bad(fail(c, NE_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device,
+        return bad(ne_fail(c, NE_ECUDA, "device %d is sm_%d%d; this build targets sm_100a", device,
                         prop.major, prop.minor));
     c->dev.sm_count = prop.multiProcessorCount;
     c->dev.max_threads_per_sm = prop.maxThreadsPerMultiProcessor;
@@ -1042,7 +933,7 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
         cudaStreamCreateWithFlags(&c->build_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&c->d_loss, sizeof(double)) != cudaSuccess ||
         cudaMalloc(&c->d_bad, 3 * sizeof(unsigned long long)) != cudaSuccess)
-        return bad(fail(c, NE_ECUDA, "stream/scratch setup failed on device %d", device));
+        return bad(ne_fail(c, NE_ECUDA, "stream/scratch setup failed on device %d", device));
     c->stream = c->ws = c->own_stream;
     *out = c;
     return NE_OK;
@@ -1057,6 +948,7 @@ int ne_set_stream(ne_ctx* c, void* stream) {
 int ne_join(ne_ctx* c) {
     NE_TRY(enter(c));
     if (c->ring_pending) NE_CUDA(c, cudaStreamWaitEvent(c->stream, c->ring_done, 0));
+    if (ipc_ring(c)) NE_TRY(ipc_drain(c, false));
     if (c->stage_pending) NE_CUDA(c, cudaStreamWaitEvent(c->stream, c->stage_done, 0));
     return NE_OK;
 }
@@ -1071,13 +963,13 @@ int ne_get_nccl_id(uint8_t id[128]) {
 
 int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
     NE_TRY(enter(c));
-    if (c->loaded) return fail(c, NE_ESTATE, "ne_init_dist must precede ne_load_graph");
-    if (world < 1 || rank < 0 || rank >= world) return fail(c, NE_EINVAL, "rank=%d world=%d", rank, world);
+    if (c->loaded) return ne_fail(c, NE_ESTATE, "ne_init_dist must precede ne_load_graph");
+    if (world < 1 || rank < 0 || rank >= world) return ne_fail(c, NE_EINVAL, "rank=%d world=%d", rank, world);
     if (world > 1 && c->cfg.staging == NE_STAGE_HOST)
-        return fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", world);
+        return ne_fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", world);
     if ((uint64_t)world * c->cfg.subparts > 256 || (uint64_t)world * world * c->cfg.subparts > 4096)
-        return fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
-    if (world > 32) return fail(c, NE_EINVAL, "world=%d > 32 (one lane per context part in the pool build)", world);
+        return ne_fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
+    if (world > 32) return ne_fail(c, NE_EINVAL, "world=%d > 32 (one lane per context part in the pool build)", world);
     if (c->comm_walk) { ncclCommDestroy(c->comm_walk); c->comm_walk = nullptr; }
     if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
     c->rank = rank;
@@ -1094,11 +986,12 @@ int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
 int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
                   const uint32_t* targets) {
     NE_TRY(enter(c));
-    if (!offsets || (nnz && !targets)) return fail(c, NE_EINVAL, "null offsets/targets");
-    if (n == 0xFFFFFFFFu) return fail(c, NE_ERANGE, "n=%u reserves the sentinel id", n);
-    if (n < (uint32_t)c->world) return fail(c, NE_ERANGE, "n=%u < world=%d", n, c->world);
-    if (nnz >= (1ull << 40)) return fail(c, NE_ERANGE, "nnz=%llu too large", (unsigned long long)nnz);
+    if (!offsets || (nnz && !targets)) return ne_fail(c, NE_EINVAL, "null offsets/targets");
+    if (n == 0xFFFFFFFFu) return ne_fail(c, NE_ERANGE, "n=%u reserves the sentinel id", n);
+    if (n < (uint32_t)c->world) return ne_fail(c, NE_ERANGE, "n=%u < world=%d", n, c->world);
+    if (nnz >= (1ull << 40)) return ne_fail(c, NE_ERANGE, "nnz=%llu too large", (unsigned long long)nnz);
     // A graph of the same shape reuses every device buffer (repeated loads, e2e).
+    NE_TRY(ipc_drain(c, true));                          // IPC ring: pushes into / out of the slots
     NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));  // ring transfers into the vertex slots
     NE_CUDA(c, cudaStreamSynchronize(c->copy_stream));
     c->ring_pending = false;
@@ -1153,25 +1046,25 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     NE_CUDA(c, cudaMemcpyAsync(&ends[0], c->d_off, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     NE_CUDA(c, cudaMemcpyAsync(&ends[1], c->d_off + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
-    if (ends[0] != 0) return fail(c, NE_EINVAL, "offsets[0]=%llu != 0", (unsigned long long)ends[0]);
+    if (ends[0] != 0) return ne_fail(c, NE_EINVAL, "offsets[0]=%llu != 0", (unsigned long long)ends[0]);
     if (bad[0] != ~0ull) {
         uint64_t pair[2];
         NE_CUDA(c, cudaMemcpy(pair, c->d_off + bad[0], sizeof pair, cudaMemcpyDeviceToHost));
-        return fail(c, NE_EINVAL, "offsets[%llu]=%llu < offsets[%llu]=%llu", bad[0] + 1,
+        return ne_fail(c, NE_EINVAL, "offsets[%llu]=%llu < offsets[%llu]=%llu", bad[0] + 1,
                     (unsigned long long)pair[1], bad[0], (unsigned long long)pair[0]);
     }
     if (ends[1] != nnz)
-        return fail(c, NE_EINVAL, "offsets[%u]=%llu != nnz=%llu", n, (unsigned long long)ends[1],
+        return ne_fail(c, NE_EINVAL, "offsets[%u]=%llu != nnz=%llu", n, (unsigned long long)ends[1],
                     (unsigned long long)nnz);
     if (bad[1] != ~0ull) {
         uint32_t t;
         NE_CUDA(c, cudaMemcpy(&t, c->d_tgt + bad[1], sizeof t, cudaMemcpyDeviceToHost));
-        return fail(c, NE_EINVAL, "targets[%llu]=%u >= n=%u", bad[1], t, n);
+        return ne_fail(c, NE_EINVAL, "targets[%llu]=%u >= n=%u", bad[1], t, n);
     }
     if (bad[2] != ~0ull) {
         uint32_t t[2];
         NE_CUDA(c, cudaMemcpy(t, c->d_tgt + bad[2] - 1, sizeof t, cudaMemcpyDeviceToHost));
-        return fail(c, NE_EINVAL, "targets[%llu]=%u < targets[%llu]=%u: node2vec needs rows sorted by target",
+        return ne_fail(c, NE_EINVAL, "targets[%llu]=%u < targets[%llu]=%u: node2vec needs rows sorted by target",
                     bad[2], t[1], bad[2] - 1, t[0]);
     }
 
@@ -1225,10 +1118,16 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     // vertex sub-part slots: the ring needs 2k (ping-pong), one GPU k, host staging 3
     const bool staged = g.staging == NE_STAGE_HOST;
     if (staged && c->world > 1)
-        return fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", c->world);
+        return ne_fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", c->world);
     const size_t nslots = staged ? std::min<size_t>(3, k) : (c->world > 1 ? 2 * (size_t)k : k);
-    if (!reuse) c->vslot.assign(nslots, nullptr);
-    for (size_t i = 0; i < c->vslot.size(); ++i) NE_ALLOC(c->vslot[i], std::max<uint64_t>(c->max_sub_rows, 1) * g.dim * esz / 4);
+    if (!reuse || c->vslot.size() != nslots) c->vslot.assign(nslots, nullptr);
+    const size_t slot_bytes = std::max<uint64_t>(c->max_sub_rows, 1) * g.dim * esz;
+    if (ipc_ring(c) && !staged) {  // one exportable region for the copy-engine ring
+        NE_TRY(ipc_alloc_slots(c, slot_bytes, nslots));
+        NE_TRY(ipc_reset_on_load(c));
+    } else {
+        for (size_t i = 0; i < c->vslot.size(); ++i) NE_ALLOC(c->vslot[i], slot_bytes / 4);
+    }
     c->cur = 0;
     if (staged) {
         const size_t bytes = (c->part_bounds[c->rank + 1] - c->part_bounds[c->rank]) * g.dim * esz;
@@ -1239,7 +1138,7 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
             cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_V), std::max<size_t>(bytes, 16), cudaHostAllocDefault);
             if (e != cudaSuccess) {
                 cudaGetLastError();
-                return fail(c, NE_ENOMEM, "cudaHostAlloc(%zu) for the host-staged vertex matrix: %s", bytes,
+                return ne_fail(c, NE_ENOMEM, "cudaHostAlloc(%zu) for the host-staged vertex matrix: %s", bytes,
                             cudaGetErrorString(e));
             }
             c->h_V_bytes = bytes;
@@ -1300,15 +1199,15 @@ int ne_random_walk(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t* host_w
                    size_t cap_u32, uint64_t* walkers_out) {
     NE_TRY(enter(c));
     NE_TRY(check_loaded(c));
-    if (c->cfg.walk_len == 0) return fail(c, NE_ESTATE, "LINE mode (walk_len=0) has no walks");
-    if (episode >= c->cfg.episodes) return fail(c, NE_ERANGE, "episode=%u >= episodes=%u", episode, c->cfg.episodes);
-    if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
+    if (c->cfg.walk_len == 0) return ne_fail(c, NE_ESTATE, "LINE mode (walk_len=0) has no walks");
+    if (episode >= c->cfg.episodes) return ne_fail(c, NE_ERANGE, "episode=%u >= episodes=%u", episode, c->cfg.episodes);
+    if (epoch >= (1u << 24)) return ne_fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
     c->next.valid = false;  // the walk and pair buffers are reused
     NE_TRY(do_walk(c, epoch, episode));
     const uint64_t total = c->walked_units * (c->cfg.walk_len + 1);
     if (walkers_out) *walkers_out = c->walked_units;
     if (host_walks) {
-        if (cap_u32 < total) return fail(c, NE_ERANGE, "host_walks capacity %zu < %llu", cap_u32, (unsigned long long)total);
+        if (cap_u32 < total) return ne_fail(c, NE_ERANGE, "host_walks capacity %zu < %llu", cap_u32, (unsigned long long)total);
         NE_CUDA(c, cudaMemcpyAsync(host_walks, c->d_walks, total * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     }
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -1318,10 +1217,10 @@ int ne_random_walk(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t* host_w
 int ne_build_samples(ne_ctx* c, uint32_t epoch, uint32_t episode, uint64_t* n_samples_out) {
     NE_TRY(enter(c));
     NE_TRY(check_loaded(c));
-    if (episode >= c->cfg.episodes) return fail(c, NE_ERANGE, "episode=%u >= episodes=%u", episode, c->cfg.episodes);
-    if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
+    if (episode >= c->cfg.episodes) return ne_fail(c, NE_ERANGE, "episode=%u >= episodes=%u", episode, c->cfg.episodes);
+    if (epoch >= (1u << 24)) return ne_fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
     if (c->cfg.walk_len > 0 && (c->walked_epoch != (int64_t)epoch || c->walked_episode != (int64_t)episode))
-        return fail(c, NE_ESTATE, "no walks for epoch %u episode %u (call ne_random_walk)", epoch, episode);
+        return ne_fail(c, NE_ESTATE, "no walks for epoch %u episode %u (call ne_random_walk)", epoch, episode);
     c->next.valid = false;
     NE_TRY(do_build(c, epoch, episode));
     if (n_samples_out) *n_samples_out = c->boff.back();
@@ -1332,8 +1231,8 @@ int ne_train_samples(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_s
     NE_TRY(enter(c));
     NE_TRY(check_loaded(c));
     if (c->built_episode != (int64_t)episode)
-        return fail(c, NE_ESTATE, "no sample pool for episode %u (call ne_build_samples)", episode);
-    if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
+        return ne_fail(c, NE_ESTATE, "no sample pool for episode %u (call ne_build_samples)", episode);
+    if (epoch >= (1u << 24)) return ne_fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
     if (stats) std::memset(stats, 0, sizeof *stats);
     const uint32_t l0 = c->launches;
     NE_TRY(do_train(c, epoch, episode, lr, stats));
@@ -1344,13 +1243,13 @@ int ne_train_samples(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, ne_s
 int ne_train_epoch(ne_ctx* c, uint32_t epoch, float lr, uint32_t flags, ne_stats* stats) {
     NE_TRY(enter(c));
     NE_TRY(check_loaded(c));
-    if (epoch >= (1u << 24)) return fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
+    if (epoch >= (1u << 24)) return ne_fail(c, NE_ERANGE, "epoch=%u >= 2^24", epoch);
     ne_stats acc;
     std::memset(&acc, 0, sizeof acc);
     const uint32_t l0 = c->launches;
     if (flags & NE_REUSE_SAMPLES) {
         if (c->cfg.episodes != 1 || c->built_episode != 0)
-            return fail(c, NE_ESTATE, "NE_REUSE_SAMPLES needs episodes == 1 and a built pool");
+            return ne_fail(c, NE_ESTATE, "NE_REUSE_SAMPLES needs episodes == 1 and a built pool");
         c->next.valid = false;
         NE_TRY(do_train(c, epoch, 0, lr, &acc));
     } else {
@@ -1407,15 +1306,16 @@ static int rows_op(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, f
                    const float* in, size_t cap_floats) {
     NE_TRY(enter(c));
     NE_TRY(check_loaded(c));
-    if (which != NE_VERTEX && which != NE_CONTEXT) return fail(c, NE_EINVAL, "which=%d", which);
+    if (which != NE_VERTEX && which != NE_CONTEXT) return ne_fail(c, NE_EINVAL, "which=%d", which);
     const uint64_t pb = c->part_bounds[c->rank], pe = c->part_bounds[c->rank + 1];
     if (row_begin > row_end || row_begin < pb || row_end > pe)
-        return fail(c, NE_ERANGE, "rows [%u, %u) not in this rank's part [%llu, %llu)", row_begin, row_end,
+        return ne_fail(c, NE_ERANGE, "rows [%u, %u) not in this rank's part [%llu, %llu)", row_begin, row_end,
                     (unsigned long long)pb, (unsigned long long)pe);
     const uint64_t d = c->cfg.dim;
     if (host && cap_floats < (uint64_t)(row_end - row_begin) * d)
-        return fail(c, NE_ERANGE, "capacity %zu < %llu floats", cap_floats,
+        return ne_fail(c, NE_ERANGE, "capacity %zu < %llu floats", cap_floats,
                     (unsigned long long)((row_end - row_begin) * d));
+    NE_TRY(ipc_drain(c, true));
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
     NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));
     const bool bf = c->cfg.storage == NE_STORE_BF16;
@@ -1470,24 +1370,24 @@ static int rows_op(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, f
 
 int ne_get_embeddings(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, float* host_out,
                       size_t cap_floats) {
-    if (!host_out) return c ? fail(c, NE_EINVAL, "null output") : NE_EINVAL;
+    if (!host_out) return c ? ne_fail(c, NE_EINVAL, "null output") : NE_EINVAL;
     return rows_op(c, which, row_begin, row_end, host_out, nullptr, cap_floats);
 }
 
 int ne_set_embeddings(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, const float* in) {
-    if (!in) return c ? fail(c, NE_EINVAL, "null input") : NE_EINVAL;
+    if (!in) return c ? ne_fail(c, NE_EINVAL, "null input") : NE_EINVAL;
     return rows_op(c, which, row_begin, row_end, nullptr, in, 0);
 }
 
 int ne_export_samples(ne_ctx* c, uint32_t vsub, uint32_t* pairs_out, size_t cap_pairs, uint64_t* count) {
     NE_TRY(enter(c));
     NE_TRY(check_loaded(c));
-    if (c->built_episode < 0) return fail(c, NE_ESTATE, "no sample pool built");
-    if (vsub >= nb_local(c)) return fail(c, NE_ERANGE, "vsub=%u >= %u", vsub, nb_local(c));
+    if (c->built_episode < 0) return ne_fail(c, NE_ESTATE, "no sample pool built");
+    if (vsub >= nb_local(c)) return ne_fail(c, NE_ERANGE, "vsub=%u >= %u", vsub, nb_local(c));
     const uint64_t cnt = c->boff[vsub + 1] - c->boff[vsub];
     if (count) *count = cnt;
     if (!pairs_out) return NE_OK;
-    if (cap_pairs < cnt) return fail(c, NE_ERANGE, "capacity %zu < %llu pairs", cap_pairs, (unsigned long long)cnt);
+    if (cap_pairs < cnt) return ne_fail(c, NE_ERANGE, "capacity %zu < %llu pairs", cap_pairs, (unsigned long long)cnt);
     if (cnt) NE_CUDA(c, cudaMemcpy(pairs_out, c->pool_at + c->boff[vsub], cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     return NE_OK;
 }
@@ -1496,8 +1396,8 @@ int ne_export_negatives(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vs
                         uint64_t count, uint32_t* out) {
     NE_TRY(enter(c));
     NE_TRY(check_loaded(c));
-    if (vsub >= nb_local(c)) return fail(c, NE_ERANGE, "vsub=%u >= %u", vsub, nb_local(c));
-    if (!out && count) return fail(c, NE_EINVAL, "null output");
+    if (vsub >= nb_local(c)) return ne_fail(c, NE_ERANGE, "vsub=%u >= %u", vsub, nb_local(c));
+    if (!out && count) return ne_fail(c, NE_EINVAL, "null output");
     const uint64_t total = count * c->cfg.negatives;
     if (total == 0) return NE_OK;
     NE_TRY(wait_alias(c));
@@ -1529,19 +1429,20 @@ int ne_capture_block(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vsub,
     NE_TRY(enter(c));
     NE_TRY(check_loaded(c));
     if (c->built_episode != (int64_t)episode || c->built_epoch != (int64_t)epoch)
-        return fail(c, NE_ESTATE, "no sample pool for epoch %u episode %u", epoch, episode);
-    if (c->cfg.staging == NE_STAGE_HOST) return fail(c, NE_ESTATE, "capture needs the vertex matrix in HBM");
+        return ne_fail(c, NE_ESTATE, "no sample pool for epoch %u episode %u", epoch, episode);
+    if (c->cfg.staging == NE_STAGE_HOST) return ne_fail(c, NE_ESTATE, "capture needs the vertex matrix in HBM");
     const uint32_t k = c->cfg.subparts, home = (uint32_t)c->rank * k;
     if (vsub < home || vsub >= home + k)
-        return fail(c, NE_ERANGE, "vsub=%u is not a home sub-part of rank %d ([%u, %u))", vsub, c->rank, home, home + k);
+        return ne_fail(c, NE_ERANGE, "vsub=%u is not a home sub-part of rank %d ([%u, %u))", vsub, c->rank, home, home + k);
     NE_TRY(wait_alias(c));
+    NE_TRY(ipc_drain(c, true));
     NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));
     c->ring_pending = false;
     ne::SgnsParams sp = sgns_params(c, vsub, c->vslot[c->cur * k + (vsub - home)], epoch, episode, lr);
     const uint64_t per = 2ull + c->cfg.negatives, total = sp.count * per;
     if (count) *count = sp.count;
     if (!out) return NE_OK;
-    if (cap_u32 < total) return fail(c, NE_ERANGE, "capacity %zu < %llu", cap_u32, (unsigned long long)total);
+    if (cap_u32 < total) return ne_fail(c, NE_ERANGE, "capacity %zu < %llu", cap_u32, (unsigned long long)total);
     if (total == 0) return NE_OK;
     if (c->tmp_u32_cap < total) {
         if (c->d_tmp_u32) dfree(c, c->d_tmp_u32);
@@ -1570,10 +1471,10 @@ int ne_train_samples_local_ring(ne_ctx* const* ctxs, uint32_t world, uint32_t ep
         ne_ctx* c = ctxs[g];
         if (!c || !c->loaded || c->comm || c->world != (int)world || c->rank != (int)g ||
             c->device != c0->device || c->cfg.subparts != k || c->cfg.dim != c0->cfg.dim)
-            return fail(c0, NE_EINVAL, "context %u is not layout-only rank %u of %u on device %d", g, g, world,
+            return ne_fail(c0, NE_EINVAL, "context %u is not layout-only rank %u of %u on device %d", g, g, world,
                         c0->device);
         if (c->built_episode != (int64_t)episode)
-            return fail(c0, NE_ESTATE, "context %u has no pool for episode %u", g, episode);
+            return ne_fail(c0, NE_ESTATE, "context %u has no pool for episode %u", g, episode);
     }
     for (uint32_t g = 0; g < world; ++g) NE_TRY(wait_alias(ctxs[g]));
     if (stats) std::memset(stats, 0, sizeof *stats);
@@ -1604,7 +1505,7 @@ int ne_train_samples_local_ring(ne_ctx* const* ctxs, uint32_t world, uint32_t ep
 int ne_check_pool(ne_ctx* c) {
     NE_TRY(enter(c));
     NE_TRY(check_loaded(c));
-    if (c->built_episode < 0) return fail(c, NE_ESTATE, "no sample pool built");
+    if (c->built_episode < 0) return ne_fail(c, NE_ESTATE, "no sample pool built");
     NE_CUDA(c, cudaMemsetAsync(c->d_bad, 0xFF, sizeof(unsigned long long), c->stream));
     NE_CUDA(c, ne::launch_check_pool(c->pool_at, c->d_boff, c->boff.back(), c->d_sub_bounds, nb_local(c),
                                      c->c_begin, c->c_begin + c->c_count, c->d_bad, c->dev, c->stream));
@@ -1616,7 +1517,7 @@ int ne_check_pool(ne_ctx* c) {
     uint64_t rec = 0;
     NE_CUDA(c, cudaMemcpy(&rec, c->pool_at + bad, sizeof rec, cudaMemcpyDeviceToHost));
     const uint32_t b = (uint32_t)(std::upper_bound(c->boff.begin(), c->boff.end(), (uint64_t)bad) - c->boff.begin() - 1);
-    return fail(c, NE_ESCHED, "pool[%llu] = (%u, %u) outside block (vertex sub-part %u = [%llu, %llu), context part [%llu, %llu))",
+    return ne_fail(c, NE_ESCHED, "pool[%llu] = (%u, %u) outside block (vertex sub-part %u = [%llu, %llu), context part [%llu, %llu))",
                 bad, (uint32_t)rec, (uint32_t)(rec >> 32), b, (unsigned long long)c->sub_bounds[b],
                 (unsigned long long)c->sub_bounds[b + 1], (unsigned long long)c->c_begin,
                 (unsigned long long)(c->c_begin + c->c_count));
@@ -1627,7 +1528,9 @@ const char* ne_last_error(const ne_ctx* c) { return c ? c->err.c_str() : g_creat
 void ne_destroy(ne_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    ipc_drain(c, true);
     free_all(c);
+    ipc_release(c);
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->ring_done) cudaEventDestroy(c->ring_done);
     if (c->stage_done) cudaEventDestroy(c->stage_done);

@@ -13,10 +13,10 @@ class Engine:
                  subparts=4, deterministic=False, seed=42, device=0, rank=0, world=1,
                  nccl_id=None, torch_allocator=False, stream=None, conflict_permille=0,
                  writeback=ne.NE_WB_ATOMIC_DELTA, p=1.0, q=1.0, update_rule=ne.NE_UPDATE_SEQUENTIAL,
-                 staging=ne.NE_STAGE_DEVICE, storage=ne.NE_STORE_F32):
+                 staging=ne.NE_STAGE_DEVICE, storage=ne.NE_STORE_F32, transport=ne.NE_TRANSPORT_NCCL):
         self.cfg = ne.ne_config(dim, negatives, walk_len, window, walks_per_node, episodes, subparts,
                                 int(bool(deterministic)), conflict_permille, writeback, p, q, update_rule,
-                                staging, storage, 0, seed)
+                                staging, storage, transport, seed)
         self._alloc = ne.torch_allocator() if torch_allocator else (None, None)
         self.ctx = ne.ne_create(self.cfg, device, *self._alloc)
         self.rank, self.world = rank, world
@@ -27,10 +27,16 @@ class Engine:
         self.n = 0
 
     # ---- graph
-    def load_graph(self, offsets, targets):
+    def load_graph(self, offsets, targets, all_gather=None):
+        """all_gather(bytes) -> [bytes per rank] (e.g. torch.distributed
+        all_gather_object): needed by the IPC transport to connect the ring."""
         ne.ne_load_graph(self.ctx, offsets, targets)
         self.n = len(offsets) - 1
         self.bounds = ne.ne_partition_bounds(self.n, self.world).astype(np.int64)
+        if self.cfg.transport == ne.NE_TRANSPORT_IPC and self.world > 1:
+            if all_gather is None:
+                raise ValueError("the IPC transport needs all_gather to exchange the ring handles")
+            ne.ne_ipc_connect(self.ctx, all_gather(ne.ne_ipc_export(self.ctx)))
 
     @property
     def part(self) -> tuple[int, int]:

@@ -29,6 +29,7 @@ NE_WB_ATOMIC_DELTA, NE_WB_STORE = 0, 1
 NE_UPDATE_SEQUENTIAL, NE_UPDATE_ACCUMULATED = 0, 1
 NE_STAGE_DEVICE, NE_STAGE_HOST = 0, 1
 NE_STORE_F32, NE_STORE_BF16 = 0, 1
+NE_TRANSPORT_NCCL, NE_TRANSPORT_IPC = 0, 1
 NE_STREAM_OWN = (1 << 64) - 1  # ne.h: ((void *)~(uintptr_t)0), the context's own stream
 
 
@@ -38,7 +39,7 @@ class ne_config(C.Structure):
                 ("subparts", C.c_uint32), ("deterministic", C.c_uint32), ("conflict_permille", C.c_uint32),
                 ("writeback", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
                 ("update_rule", C.c_uint32), ("staging", C.c_uint32), ("storage", C.c_uint32),
-                ("reserved", C.c_uint32), ("seed", C.c_uint64)]
+                ("transport", C.c_uint32), ("seed", C.c_uint64)]
 
 
 class ne_stats(C.Structure):
@@ -75,6 +76,9 @@ _sig = {
     "ne_export_negatives": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, _P]),
     "ne_capture_block": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float, _P, C.c_size_t,
                                    C.POINTER(C.c_uint64)]),
+    "ne_ipc_blob_size": (C.c_size_t, []),
+    "ne_ipc_export": (C.c_int, [_P, _P, C.c_size_t]),
+    "ne_ipc_connect": (C.c_int, [_P, _P, C.c_size_t]),
     "ne_train_samples_local_ring": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
                                              C.POINTER(ne_stats)]),
     "ne_plan_vsub": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
@@ -227,6 +231,20 @@ def ne_capture_block(ctx, epoch: int, episode: int, vsub: int, lr: float, out: n
     _check(ctx, _lib.ne_capture_block(ctx, epoch, episode, vsub, lr, _ptr(out, 4, "out (u32)"), cap,
                                       C.byref(cnt)))
     return int(cnt.value)
+
+
+def ne_ipc_export(ctx) -> bytes:
+    n = _lib.ne_ipc_blob_size()
+    buf = (C.c_uint8 * n)()
+    _check(ctx, _lib.ne_ipc_export(ctx, buf, n))
+    return bytes(buf)
+
+
+def ne_ipc_connect(ctx, blobs: list[bytes]) -> None:
+    n = _lib.ne_ipc_blob_size()
+    assert all(len(b) == n for b in blobs)
+    buf = (C.c_uint8 * (n * len(blobs))).from_buffer_copy(b"".join(blobs))
+    _check(ctx, _lib.ne_ipc_connect(ctx, buf, n))
 
 
 def ne_train_samples_local_ring(ctxs, epoch: int, episode: int, lr: float) -> ne_stats:

@@ -77,6 +77,6 @@ def test_create_validates_storage():
     from paper_2005_13789_b200 import ne
     with pytest.raises(ne.NEError, match="NE_EINVAL: storage=2"):
         ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 2, 0, 42), 0)
-    with pytest.raises(ne.NEError, match="NE_EINVAL: reserved=1"):
-        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 0, 1, 42), 0)
+    with pytest.raises(ne.NEError, match="NE_EINVAL: transport=2"):
+        ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 0, 2, 42), 0)
 

@@ -1,0 +1,22 @@
+"""The copy-engine ring over CUDA IPC (NE_TRANSPORT_IPC): real multi-process
+training -- processes share the available GPUs round-robin, so these run on a
+single-GPU box -- compared with the oracle (tools/ipc_parity.py)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world,mode", [(2, "det"), (3, "det"), (2, "hogwild")])
+def test_ipc_ring(world, mode):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={29700 + world + (mode == 'hogwild') * 10}",
+           os.path.join(ROOT, "tools", "ipc_parity.py"), mode]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "IPC " in r.stdout
