@@ -140,6 +140,12 @@ typedef struct {
                                 id == NULL: no NCCL at all (each rank then builds its
                                 part's pool from every walker, the layout-only way). */
     uint64_t seed;           /* Philox key (contract R1)                                */
+    uint32_t groups;         /* NEXT-3 two-level ring (P:150 hierarchical partitioning,
+                                P:190-191): the world's ranks form `groups` groups
+                                ("nodes") of world/groups consecutive ranks; each group
+                                first trains its own vertex parts around its internal
+                                ring, then the groups pass their parts to the next group
+                                (ne_plan_vsub2).  0 or 1 = one ring over all ranks.   */
 } ne_config;
 
 /* Per-call statistics (this rank).  Times are device time from CUDA events. */
@@ -327,6 +333,14 @@ int ne_train_samples_local_ring(ne_ctx *const *ctxs, uint32_t world, uint32_t ep
  * rank g trains at round r, slot t, with `world` ranks and `subparts` slots.
  * Returns -1 on bad arguments. */
 int ne_plan_vsub(uint32_t world, uint32_t subparts, uint32_t r, uint32_t t, uint32_t g);
+
+/* NEXT-3 two-level plan: rank g of `world` in `groups` groups trains vertex
+ * sub-part ne_plan_vsub2(...) at global round rho (0 <= rho < world) and slot
+ * t; groups = 1 is ne_plan_vsub.  ne_ring_peers gives the rank a sub-part
+ * moves to after round rho (dest) and the rank sending to g (src).  No device
+ * needed.  -1 / NE_EINVAL on bad arguments (groups must divide world). */
+int ne_plan_vsub2(uint32_t world, uint32_t groups, uint32_t subparts, uint32_t rho, uint32_t t, uint32_t g);
+int ne_ring_peers(uint32_t world, uint32_t groups, uint32_t rho, uint32_t g, uint32_t *dest, uint32_t *src);
 
 /* Contiguous part bounds used by the library (reading D12): bounds[0..parts]
  * of [0, n).  No device needed.  Returns NE_EINVAL if parts == 0. */

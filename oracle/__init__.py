@@ -47,7 +47,8 @@ class _Config(C.Structure):
     _fields_ = [("dim", C.c_uint32), ("negatives", C.c_uint32), ("walk_len", C.c_uint32),
                 ("window", C.c_uint32), ("walks_per_node", C.c_uint32), ("episodes", C.c_uint32),
                 ("subparts", C.c_uint32), ("parts", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
-                ("update_rule", C.c_uint32), ("storage", C.c_uint32), ("seed", C.c_uint64)]
+                ("update_rule", C.c_uint32), ("storage", C.c_uint32), ("seed", C.c_uint64),
+                ("groups", C.c_uint32)]
 
 
 class _Stats(C.Structure):
@@ -70,11 +71,12 @@ class Config:
     q: float = 1.0   # node2vec in-out parameter
     update_rule: int = 0  # 0 sequential (Alg. 1), 1 accumulated (word2vec, NEXT-4)
     storage: int = 0      # 0 fp32 rows, 1 bf16 rows (NEXT-4, reading D16)
+    groups: int = 1       # NEXT-3 two-level ring: groups of parts/groups ranks (1 = one ring)
 
     def c(self) -> _Config:
         return _Config(self.dim, self.negatives, self.walk_len, self.window, self.walks_per_node,
                        self.episodes, self.subparts, self.parts, self.p, self.q, self.update_rule,
-                       self.storage, self.seed)
+                       self.storage, self.seed, self.groups)
 
 
 _lib = None
@@ -143,6 +145,8 @@ def lib():
                                      C.c_uint32, _f64p, C.POINTER(C.POINTER(C.c_double)), C.POINTER(C.c_double)]
     L.or_plan_vsub.argtypes = [C.c_uint32] * 5
     L.or_plan_vsub.restype = C.c_uint32
+    L.or_plan_vsub2.argtypes = [C.c_uint32] * 6
+    L.or_plan_vsub2.restype = C.c_uint32
     L.or_build_alias_tables.argtypes = [C.POINTER(_Config), C.c_uint64, _u64p, _u32p, _u32p]
     L.or_train_epoch_tables.argtypes = [C.POINTER(_Config), C.c_uint64, _u64p, _u32p, _u32p,
                                         _u32p, C.c_uint32, C.c_float, C.c_uint32, C.c_uint32,
@@ -406,6 +410,11 @@ def train_sample(V, Cm, src: int, dst: int, negs, lr: float) -> float:
 
 def plan_vsub(P: int, k: int, r: int, t: int, g: int) -> int:
     return int(lib().or_plan_vsub(P, k, r, t, g))
+
+
+def plan_vsub2(P: int, G: int, k: int, rho: int, t: int, g: int) -> int:
+    """NEXT-3 two-level ring: sub-part rank g trains at global round rho."""
+    return int(lib().or_plan_vsub2(P, G, k, rho, t, g))
 
 
 def train_sample_accumulated(V, Cm, src: int, dst: int, negs, lr: float) -> float:

@@ -37,6 +37,7 @@ typedef struct {
     uint32_t update_rule;    /* 0 sequential (Alg. 1, D2); 1 accumulated (word2vec, NEXT-4) */
     uint32_t storage;        /* 0 fp32 rows; 1 bf16 rows (NEXT-4, reading D16)  */
     uint64_t seed;           /* Philox key                                      */
+    uint32_t groups;         /* NEXT-3 two-level ring: G groups ("nodes") of P/G ranks; 0 or 1 = one ring */
 } or_config;
 
 typedef struct {
@@ -103,6 +104,7 @@ void     or_sgns_total_grad(const double *v, const double *const *c, const int *
 double   or_train_sample_accumulated(float *V, float *C, uint32_t d, uint32_t src, uint32_t dst,
                                      const uint32_t *negs, uint32_t K, float lr);
 uint32_t or_plan_vsub(uint32_t P, uint32_t k, uint32_t r, uint32_t t, uint32_t g);
+uint32_t or_plan_vsub2(uint32_t P, uint32_t G, uint32_t k, uint32_t rho, uint32_t t, uint32_t g);
 int      or_build_alias_tables(const or_config *cfg, uint64_t n, const uint64_t *offsets,
                                uint32_t *thr, uint32_t *alias);
 int      or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offsets,

@@ -168,10 +168,31 @@ uint32_t or_plan_vsub(uint32_t P, uint32_t k, uint32_t r, uint32_t t, uint32_t g
     return ((g + P - (r % P)) % P) * k + t;
 }
 
+/* NEXT-3, the two-level (hierarchical) ring ("hierarchically partition
+ * the full vertex embedding matrix: first inter-node, then intra-node and
+ * inter-GPU"; "each node forms an internal ring ... all nodes form
+ * another ring"; SPEC build_schedule): P = G*L ranks in G groups of
+ * L, rank g = a*L + j (group a, local index j).  Global round rho = R*L + r:
+ * outer round R (the group holds the vertex parts of group (a - R) mod G, as
+ * "all GPUs from Node0 will first train on half of the vertex embeddings, then
+ * ... swap") and inner rotation r along the group's ring.  Rank g trains
+ * vertex sub-part (((a - R) mod G)*L + ((j - r) mod L))*k + t.  G = 1 and G = P
+ * are both the single ring of or_plan_vsub. */
+uint32_t or_plan_vsub2(uint32_t P, uint32_t G, uint32_t k, uint32_t rho, uint32_t t, uint32_t g)
+{
+    uint32_t L, a, j, R, r;
+    if (G == 0) G = 1;
+    L = P / G;
+    a = g / L; j = g % L;
+    R = (rho / L) % G; r = rho % L;
+    return (((a + G - R) % G) * L + (j + L - r) % L) * k + t;
+}
+
 /* O7 + O11: episodes [episode_begin, episode_end) of one epoch.  Per episode:
  * build the pool (O4-O6), then replay the hierarchical plan:
  *   for round r in 0..P-1, slot t in 0..k-1, context part g in 0..P-1:
  *       train block (vertex sub-part ((g - r) mod P)*k + t, context part g)
+ * (or or_plan_vsub2's sub-part with cfg->groups > 1, the two-level ring)
  * Blocks of one (r, t) step touch disjoint rows ("orthogonal vertex
  * usage"), so the order over g is immaterial; reverse_within_step = 1 replays
  * it backwards to let a test check exactly that.  thr/alias come from
@@ -224,6 +245,7 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
         return -1;
     if (cfg->walk_len > 0 && (cfg->window == 0 || cfg->walks_per_node == 0)) return -1;
     if (cfg->update_rule > 1 || cfg->storage > 1) return -1;
+    if (cfg->groups > 1 && P % cfg->groups != 0) return -1;
     or_partition_bounds(0, n, P, bounds);
     boff = (uint64_t *)malloc((nblocks + 1) * sizeof(uint64_t));
     if (!boff) return -1;
@@ -241,7 +263,8 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
             for (t = 0; t < k; ++t)
                 for (gi = 0; gi < P; ++gi) {
                     uint32_t g = reverse_within_step ? (P - 1 - gi) : gi;
-                    uint32_t s = or_plan_vsub(P, k, r, t, g);
+                    uint32_t s = cfg->groups > 1 ? or_plan_vsub2(P, cfg->groups, k, r, t, g)
+                                                 : or_plan_vsub(P, k, r, t, g);
                     uint32_t B = s * P + g;
                     uint64_t p, cb = bounds[g], cn = bounds[g + 1] - bounds[g];
                     for (p = 0; p < boff[B + 1] - boff[B]; ++p) {

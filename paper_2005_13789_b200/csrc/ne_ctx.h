@@ -120,20 +120,36 @@ struct ne_ctx {
         void* region = nullptr;          // this rank's 2k vertex slots + flags, one exportable cudaMalloc
         size_t region_bytes = 0, slot_bytes = 0;
         uint32_t* flags = nullptr;       // arrived[k] (written by rank - 1), credit[k] (written by rank + 1)
-        void* next_region = nullptr;     // rank + 1's region, opened from its handle
-        void* prev_region = nullptr;     // rank - 1's region (== next_region when world == 2)
+        std::vector<void*> peer;         // regions of the ranks this one pushes to / credits, opened handles
         bool connected = false;
         bool started = false;            // a ring call ran since the last load (arrivals to wait for)
         std::vector<uint32_t> pushed, waited;  // per slot t: pushes issued / arrivals awaited (monotonic)
     } ipc;
 };
 
+// NEXT-3 ring hops (P = G * L ranks, rank g = a * L + j): after global round
+// rho a sub-part moves along the group's ring to (a, j + 1), except after the
+// group's last rotation, when it crosses to the next group, (a + 1, j + 1).
+inline uint32_t ring_dest(uint32_t P, uint32_t G, uint32_t rho, uint32_t g) {
+    const uint32_t L = P / G, a = g / L, j = g % L;
+    const uint32_t na = (rho % L) + 1 < L ? a : (a + 1) % G;
+    return na * L + (j + 1) % L;
+}
+// The rank whose ring_dest after round rho is g.
+inline uint32_t ring_src(uint32_t P, uint32_t G, uint32_t rho, uint32_t g) {
+    const uint32_t L = P / G, a = g / L, j = g % L;
+    const uint32_t pa = (rho % L) + 1 < L ? a : (a + G - 1) % G;
+    return pa * L + (j + L - 1) % L;
+}
+
 // Copy-engine ring over CUDA IPC (ring_ipc.cpp).
 bool ipc_ring(const ne_ctx* c);                      // world > 1 and transport == NE_TRANSPORT_IPC
 int ipc_alloc_slots(ne_ctx* c, size_t slot_bytes, size_t nslots);  // the 2k vertex slots, exportable
 int ipc_reset_on_load(ne_ctx* c);                    // home sub-parts re-initialised: no arrivals owed
 int ipc_wait_arrival(ne_ctx* c, uint32_t t);         // compute stream waits for the sub-part of slot t
-int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after);
+// push slot t's sub-part into rank `dest`; `credit_to` = the rank that pushes into this one next round
+int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after, uint32_t dest,
+             uint32_t credit_to);
 int ipc_drain(ne_ctx* c, bool host_sync);            // every push into / out of this rank has landed
 void ipc_release(ne_ctx* c);
 

@@ -4,19 +4,22 @@
 //
 // Every rank allocates its 2k vertex slots (two ping-pong halves of k
 // sub-part slots) and 2k u32 flags as ONE cudaMalloc region, exports it
-// (ne_ipc_export), and maps the regions of ranks g-1 and g+1 (ne_ipc_connect;
-// the harness all-gathers the handles).  After training (round r, slot t) rank
-// g pushes the sub-part with one cudaMemcpyAsync on its comm stream straight
-// into the other half of rank g+1's slot t -- a copy-engine transfer over
-// NVLink between GPUs (a plain device copy when two processes share a GPU),
-// no SM involved.  Ordering uses monotonic per-slot counters in the flag
-// words, waited on and written by the GPU front end (cuStreamWaitValue32 /
-// cuStreamWriteValue32, no kernel, no host round trip):
-//   * push i of slot t into g+1 first waits credit[t] >= i - 1 at g: rank
-//     g+1's own push i-1 of slot t -- the sub-part that occupied the target
-//     half -- has left;
-//   * after the copy, g writes arrived[t] = i at g+1 and credit[t] = i at g-1
-//     (g's push i freed the half g-1's push i+1 will land in);
+// (ne_ipc_export), and maps the regions of the ranks it pushes to or credits
+// (ne_ipc_connect; the harness all-gathers the handles): g+1 and g-1 on the
+// single ring, the group-ring and next-group neighbours with NEXT-3 groups.
+// After training (round rho, slot t) rank g pushes the sub-part with one
+// cudaMemcpyAsync on its comm stream straight into the other half of slot t of
+// D = ring_dest(rho) -- a copy-engine transfer over NVLink between GPUs (a
+// plain device copy when two processes share a GPU), no SM involved.  Every
+// rank pushes every slot once per round, so push i of slot t is global round
+// i - 1 on every rank, and ordering uses these monotonic per-slot counters in
+// the flag words, waited on and written by the GPU front end
+// (cuStreamWaitValue32 / cuStreamWriteValue32, no kernel, no host round trip):
+//   * push i first waits credit[t] >= i - 1 at g: D's own push i-1 of slot t
+//     -- the sub-part that occupied the target half -- has left;
+//   * after the copy, g writes arrived[t] = i at D and credit[t] = i at the
+//     rank that pushes into g in the next round (g's push i freed the half
+//     that push lands in);
 //   * before training slot t in every round but the first after a load, g
 //     waits arrived[t] >= (its next expected arrival).
 // The counters never reset while the region lives, so a rank can never clear
@@ -82,9 +85,9 @@ int write_flag(ne_ctx* c, cudaStream_t s, uint32_t* flag, uint32_t value) {
 }
 
 void close_peers(ne_ctx* c) {
-    if (c->ipc.next_region) cudaIpcCloseMemHandle(c->ipc.next_region);
-    if (c->ipc.prev_region && c->ipc.prev_region != c->ipc.next_region) cudaIpcCloseMemHandle(c->ipc.prev_region);
-    c->ipc.next_region = c->ipc.prev_region = nullptr;
+    for (void*& p : c->ipc.peer)
+        if (p && p != c->ipc.region) cudaIpcCloseMemHandle(p);
+    c->ipc.peer.clear();
     c->ipc.connected = false;
 }
 
@@ -127,17 +130,21 @@ int ipc_wait_arrival(ne_ctx* c, uint32_t t) {
     return wait_ge(c, c->stream, c->ipc.flags + t, ++c->ipc.waited[t]);
 }
 
-int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after) {
-    if (!c->ipc.connected) return ne_fail(c, NE_ESTATE, "IPC ring not connected (ne_ipc_export / ne_ipc_connect)");
+int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after, uint32_t dest,
+             uint32_t credit_to) {
+    if (!c->ipc.connected || dest >= c->ipc.peer.size() || credit_to >= c->ipc.peer.size() || !c->ipc.peer[dest] ||
+        !c->ipc.peer[credit_to])
+        return ne_fail(c, NE_ESTATE, "IPC ring not connected to ranks %u / %u (ne_ipc_export / ne_ipc_connect)", dest,
+                       credit_to);
     const uint32_t k = c->cfg.subparts;
     const uint32_t i = ++c->ipc.pushed[t];
     NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, after, 0));
     if (i > 1) NE_TRY(wait_ge(c, c->comm_stream, c->ipc.flags + k + t, i - 1));  // credit: the target half is free
-    const size_t half = (size_t)(1 - c->cur) * k + t;                            // the other half of rank + 1
-    char* dst = static_cast<char*>(c->ipc.next_region) + half * c->ipc.slot_bytes;
+    const size_t half = (size_t)(1 - c->cur) * k + t;                            // the other half of dest
+    char* dst = static_cast<char*>(c->ipc.peer[dest]) + half * c->ipc.slot_bytes;
     NE_CUDA(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
-    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.next_region) + t, i));      // arrived at rank + 1
-    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.prev_region) + k + t, i));  // credit at rank - 1
+    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.peer[dest]) + t, i));              // arrived at dest
+    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.peer[credit_to]) + k + t, i));     // credit
     c->ipc.started = true;
     return NE_OK;
 }
@@ -198,23 +205,35 @@ int ne_ipc_connect(ne_ctx* c, const void* blobs, size_t blob_size) {
     if (!ipc_ring(c)) return ne_fail(c, NE_ESTATE, "transport is not NE_TRANSPORT_IPC or world == 1");
     if (blob_size != sizeof(Blob)) return ne_fail(c, NE_EINVAL, "blob size %zu != %zu", blob_size, sizeof(Blob));
     const uint32_t P = (uint32_t)c->world, g = (uint32_t)c->rank;
-    Blob nb, pb;
-    std::memcpy(&nb, static_cast<const char*>(blobs) + ((g + 1) % P) * blob_size, sizeof nb);
-    std::memcpy(&pb, static_cast<const char*>(blobs) + ((g + P - 1) % P) * blob_size, sizeof pb);
-    for (const Blob* b : {&nb, &pb})
-        if (b->magic != kMagic || b->world != P || b->subparts != c->cfg.subparts ||
-            b->region_bytes != c->ipc.region_bytes || b->slot_bytes != c->ipc.slot_bytes)
+    const uint32_t G = c->cfg.groups > 1 ? c->cfg.groups : 1;
+    // the ranks this one pushes into and credits over the P rounds of a call
+    std::vector<bool> need(P, false);
+    for (uint32_t rho = 0; rho < P; ++rho) {
+        need[ring_dest(P, G, rho, g)] = true;
+        need[ring_src(P, G, rho + 1, g)] = true;
+    }
+    for (uint32_t q = 0; q < P; ++q) {
+        if (!need[q]) continue;
+        Blob b;
+        std::memcpy(&b, static_cast<const char*>(blobs) + (size_t)q * blob_size, sizeof b);
+        if (b.magic != kMagic || b.world != P || b.subparts != c->cfg.subparts ||
+            b.region_bytes != c->ipc.region_bytes || b.slot_bytes != c->ipc.slot_bytes)
             return ne_fail(c, NE_EINVAL, "IPC blob of rank %u does not match this ring (world %u, subparts %u, "
-                                         "region %llu bytes)", b->rank, P, c->cfg.subparts,
+                                         "region %llu bytes)", q, P, c->cfg.subparts,
                            (unsigned long long)c->ipc.region_bytes);
-    if (nb.rank != (g + 1) % P || pb.rank != (g + P - 1) % P)
-        return ne_fail(c, NE_EINVAL, "IPC blobs out of rank order");
+        if (b.rank != q) return ne_fail(c, NE_EINVAL, "IPC blobs out of rank order (slot %u holds rank %u)", q, b.rank);
+    }
     close_peers(c);
-    NE_CUDA(c, cudaIpcOpenMemHandle(&c->ipc.next_region, nb.handle, cudaIpcMemLazyEnablePeerAccess));
-    if (P == 2) {
-        c->ipc.prev_region = c->ipc.next_region;
-    } else {
-        NE_CUDA(c, cudaIpcOpenMemHandle(&c->ipc.prev_region, pb.handle, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc.peer.assign(P, nullptr);
+    for (uint32_t q = 0; q < P; ++q) {
+        if (!need[q]) continue;
+        Blob b;
+        std::memcpy(&b, static_cast<const char*>(blobs) + (size_t)q * blob_size, sizeof b);
+        if (q == g) {  // a one-rank group pushes into itself: its own region
+            c->ipc.peer[q] = c->ipc.region;
+            continue;
+        }
+        NE_CUDA(c, cudaIpcOpenMemHandle(&c->ipc.peer[q], b.handle, cudaIpcMemLazyEnablePeerAccess));
     }
     c->ipc.connected = true;
     return NE_OK;

@@ -51,9 +51,18 @@ void partition(uint64_t begin, uint64_t end, uint32_t parts, uint64_t* out) {
     for (uint64_t i = 0; i <= parts; ++i) out[i] = begin + i * q + std::min<uint64_t>(i, r);
 }
 
-int plan_vsub(uint32_t P, uint32_t k, uint32_t r, uint32_t t, uint32_t g) {
-    return (int)(((g + P - (r % P)) % P) * k + t);
+// O7 plan with NEXT-3 groups: P = G * L ranks, rank
+// g = a * L + j; at global round rho = R * L + r rank g trains vertex sub-part
+// (((a - R) mod G) * L + ((j - r) mod L)) * k + t.  G = 1: the single ring,
+// (g - r) mod P.  After round rho a sub-part moves to ring_dest: along the
+// group's ring, (a, j + 1), except after the group's last rotation, when it
+// crosses to the next group, (a + 1, j + 1); rho = P - 1 brings it home.
+int plan_vsub(uint32_t P, uint32_t G, uint32_t k, uint32_t rho, uint32_t t, uint32_t g) {
+    const uint32_t L = P / G, a = g / L, j = g % L, R = (rho / L) % G, r = rho % L;
+    return (int)((((a + G - R) % G) * L + (j + L - r) % L) * k + t);
 }
+
+uint32_t groups_of(const ne_ctx* c) { return c->cfg.groups > 1 ? c->cfg.groups : 1; }
 
 int dalloc(ne_ctx* c, void** out, size_t bytes) {
     bytes = std::max<size_t>(bytes, 16);
@@ -686,7 +695,7 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
     NE_TRY(wait_alias(c));
     NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
     if (c->cfg.staging == NE_STAGE_HOST) return launch_train_staged(c, epoch, episode, lr, tp);
-    const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank;
+    const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank, G = groups_of(c);
     const uint64_t d = c->cfg.dim;
     const bool ipc = ipc_ring(c);
     if (P > 1 && !c->comm && !ipc)
@@ -695,7 +704,7 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
     if (c->ring_pending) recv.assign(k, c->ring_done);  // home-coming sub-parts of the last call
     for (uint32_t r = 0; r < P; ++r) {
         for (uint32_t t = 0; t < k; ++t) {
-            const uint32_t vs = (uint32_t)plan_vsub(P, k, r, t, g);
+            const uint32_t vs = (uint32_t)plan_vsub(P, G, k, r, t, g);
             float* V = c->vslot[c->cur * k + t];
             if (ipc && (r > 0 || c->ipc.started)) {  // the sub-part of this slot has landed
                 cudaEvent_t w0 = next_event(c), w1 = next_event(c);
@@ -720,17 +729,18 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
             tp.samples += sp.count;
             if (P > 1 && ipc) {  // copy-engine push into rank + 1 (ring_ipc.cpp)
                 const uint64_t send_rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
-                NE_TRY(ipc_push(c, t, V, send_rows * d * elem_bytes(c), e1));
+                NE_TRY(ipc_push(c, t, V, send_rows * d * elem_bytes(c), e1, ring_dest(P, G, r, g),
+                                ring_src(P, G, r + 1, g)));
             } else if (P > 1) {
-                const uint32_t vs_next = (uint32_t)plan_vsub(P, k, r + 1, t, g);
+                const uint32_t vs_next = (uint32_t)plan_vsub(P, G, k, r + 1, t, g);
                 const uint64_t send_rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
                 const uint64_t recv_rows = c->sub_bounds[vs_next + 1] - c->sub_bounds[vs_next];
                 float* Vn = c->vslot[(1 - c->cur) * k + t];
                 NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, e1, 0));
                 NE_NCCL(c, ncclGroupStart());
                 const ncclDataType_t dt = c->cfg.storage == NE_STORE_BF16 ? ncclBfloat16 : ncclFloat;
-                NE_NCCL(c, ncclSend(V, send_rows * d, dt, (int)((g + 1) % P), c->comm, c->comm_stream));
-                NE_NCCL(c, ncclRecv(Vn, recv_rows * d, dt, (int)((g + P - 1) % P), c->comm, c->comm_stream));
+                NE_NCCL(c, ncclSend(V, send_rows * d, dt, (int)ring_dest(P, G, r, g), c->comm, c->comm_stream));
+                NE_NCCL(c, ncclRecv(Vn, recv_rows * d, dt, (int)ring_src(P, G, r, g), c->comm, c->comm_stream));
                 NE_NCCL(c, ncclGroupEnd());
                 cudaEvent_t rv = next_event(c);
                 NE_CUDA(c, cudaEventRecord(rv, c->comm_stream));
@@ -857,7 +867,21 @@ int ne_version(void) { return NE_ABI_VERSION; }
 
 int ne_plan_vsub(uint32_t world, uint32_t subparts, uint32_t r, uint32_t t, uint32_t g) {
     if (world == 0 || subparts == 0 || t >= subparts || g >= world) return -1;
-    return plan_vsub(world, subparts, r, t, g);
+    return plan_vsub(world, 1, subparts, r, t, g);
+}
+
+int ne_plan_vsub2(uint32_t world, uint32_t groups, uint32_t subparts, uint32_t rho, uint32_t t, uint32_t g) {
+    if (groups == 0) groups = 1;
+    if (world == 0 || world % groups || subparts == 0 || t >= subparts || g >= world) return -1;
+    return plan_vsub(world, groups, subparts, rho, t, g);
+}
+
+int ne_ring_peers(uint32_t world, uint32_t groups, uint32_t rho, uint32_t g, uint32_t* dest, uint32_t* src) {
+    if (groups == 0) groups = 1;
+    if (world == 0 || world % groups || g >= world || !dest || !src) return NE_EINVAL;
+    *dest = ring_dest(world, groups, rho, g);
+    *src = ring_src(world, groups, rho, g);
+    return NE_OK;
 }
 
 int ne_partition_bounds(uint64_t n, uint32_t parts, uint64_t* bounds) {
@@ -970,6 +994,8 @@ int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
     if ((uint64_t)world * c->cfg.subparts > 256 || (uint64_t)world * world * c->cfg.subparts > 4096)
         return ne_fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
     if (world > 32) return ne_fail(c, NE_EINVAL, "world=%d > 32 (one lane per context part in the pool build)", world);
+    if (c->cfg.groups > 1 && world % c->cfg.groups)
+        return ne_fail(c, NE_EINVAL, "groups=%u does not divide world=%d", c->cfg.groups, world);
     if (c->comm_walk) { ncclCommDestroy(c->comm_walk); c->comm_walk = nullptr; }
     if (c->comm) { ncclCommDestroy(c->comm); c->comm = nullptr; }
     c->rank = rank;
@@ -1482,17 +1508,18 @@ int ne_train_samples_local_ring(ne_ctx* const* ctxs, uint32_t world, uint32_t ep
     // Every rank's launches go to rank 0's stream, in plan order: round r, slot t,
     // rank g; the "send to g+1" is a pointer hand-over of the trained slot.
     std::vector<float*> moved(world);
+    const uint32_t G = groups_of(c0);
     for (uint32_t r = 0; r < world; ++r)
         for (uint32_t t = 0; t < k; ++t) {
             for (uint32_t g = 0; g < world; ++g) {
                 ne_ctx* c = ctxs[g];
-                const uint32_t vs = (uint32_t)plan_vsub(world, k, r, t, g);
+                const uint32_t vs = (uint32_t)plan_vsub(world, G, k, r, t, g);
                 ne::SgnsParams sp = sgns_params(c, vs, c->vslot[c->cur * k + t], epoch, episode, lr);
                 sp.loss = c0->d_loss;
                 NE_CUDA(c0, ne::launch_sgns(sp, c->dev, c0->stream));
                 if (stats) { stats->samples += sp.count; if (sp.count) stats->train_launches += 1; }
             }
-            for (uint32_t g = 0; g < world; ++g) moved[(g + 1) % world] = ctxs[g]->vslot[ctxs[g]->cur * k + t];
+            for (uint32_t g = 0; g < world; ++g) moved[ring_dest(world, G, r, g)] = ctxs[g]->vslot[ctxs[g]->cur * k + t];
             for (uint32_t g = 0; g < world; ++g) ctxs[g]->vslot[ctxs[g]->cur * k + t] = moved[g];
         }
     double loss = 0.0;

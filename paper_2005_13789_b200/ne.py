@@ -39,7 +39,7 @@ class ne_config(C.Structure):
                 ("subparts", C.c_uint32), ("deterministic", C.c_uint32), ("conflict_permille", C.c_uint32),
                 ("writeback", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
                 ("update_rule", C.c_uint32), ("staging", C.c_uint32), ("storage", C.c_uint32),
-                ("transport", C.c_uint32), ("seed", C.c_uint64)]
+                ("transport", C.c_uint32), ("seed", C.c_uint64), ("groups", C.c_uint32)]
 
 
 class ne_stats(C.Structure):
@@ -83,6 +83,9 @@ _sig = {
                                              C.POINTER(ne_stats)]),
     "ne_plan_vsub": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
     "ne_partition_bounds": (C.c_int, [C.c_uint64, C.c_uint32, _P]),
+    "ne_plan_vsub2": (C.c_int, [C.c_uint32] * 6),
+    "ne_ring_peers": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32),
+                                C.POINTER(C.c_uint32)]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -256,6 +259,17 @@ def ne_train_samples_local_ring(ctxs, epoch: int, episode: int, lr: float) -> ne
 
 def ne_plan_vsub(world: int, subparts: int, r: int, t: int, g: int) -> int:
     return _lib.ne_plan_vsub(world, subparts, r, t, g)
+
+
+def ne_plan_vsub2(world: int, groups: int, subparts: int, rho: int, t: int, g: int) -> int:
+    return _lib.ne_plan_vsub2(world, groups, subparts, rho, t, g)
+
+
+def ne_ring_peers(world: int, groups: int, rho: int, g: int) -> tuple[int, int]:
+    d, s_ = C.c_uint32(), C.c_uint32()
+    if _lib.ne_ring_peers(world, groups, rho, g, C.byref(d), C.byref(s_)) != NE_OK:
+        raise NEError(NE_EINVAL, "bad ring arguments")
+    return int(d.value), int(s_.value)
 
 
 def ne_partition_bounds(n: int, parts: int) -> np.ndarray:

@@ -80,3 +80,21 @@ def test_create_validates_storage():
     with pytest.raises(ne.NEError, match="NE_EINVAL: transport=2"):
         ne.ne_create(ne.ne_config(128, 5, 40, 5, 1, 1, 4, 0, 0, 0, 1.0, 1.0, 0, 0, 0, 2, 42), 0)
 
+
+
+def test_two_level_plan_matches_oracle(orc):
+    """NEXT-3: the library's two-level plan and ring hops (host code, no
+    device) against the oracle's or_plan_vsub2."""
+    from paper_2005_13789_b200 import ne
+    for P, G in [(1, 1), (2, 1), (2, 2), (4, 2), (6, 3), (8, 2), (8, 4), (8, 8)]:
+        for k in (1, 3):
+            for rho in range(P):
+                for t in range(k):
+                    for g in range(P):
+                        s = ne.ne_plan_vsub2(P, G, k, rho, t, g)
+                        assert s == orc.plan_vsub2(P, G, k, rho, t, g)
+                        dest, src = ne.ne_ring_peers(P, G, rho, g)
+                        # the sub-part moves to dest, which trains it next round (home after the last)
+                        assert ne.ne_plan_vsub2(P, G, k, rho + 1, t, dest) == s
+                        assert ne.ne_ring_peers(P, G, rho, src)[0] == g
+    assert ne.ne_plan_vsub2(6, 4, 1, 0, 0, 0) == -1

@@ -12,11 +12,12 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world,mode", [(2, "det"), (3, "det"), (2, "hogwild")])
-def test_ipc_ring(world, mode):
+@pytest.mark.parametrize("world,mode,groups", [(2, "det", 1), (3, "det", 1), (2, "hogwild", 1), (4, "det", 2)])
+def test_ipc_ring(world, mode, groups):
+    """groups = 2: the NEXT-3 two-level ring (two groups of two ranks)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr=127.0.0.1", f"--master-port={29700 + world + (mode == 'hogwild') * 10}",
-           os.path.join(ROOT, "tools", "ipc_parity.py"), mode]
+           "--master-addr=127.0.0.1", f"--master-port={29700 + world + (mode == 'hogwild') * 10 + groups * 20}",
+           os.path.join(ROOT, "tools", "ipc_parity.py"), mode, str(groups)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "IPC " in r.stdout

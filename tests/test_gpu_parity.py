@@ -382,21 +382,22 @@ def test_pool_keyed_equals_direct_c2(monkeypatch):
 
 
 # ---------------------------------------------------------------- P-rank ring on one GPU
-@pytest.mark.parametrize("P", [2, 4, 8])
-def test_deterministic_ring_emulation_c1(c1, P):
+@pytest.mark.parametrize("P,G", [(2, 1), (4, 1), (8, 1), (4, 2), (8, 2), (8, 4)])
+def test_deterministic_ring_emulation_c1(c1, P, G):
     """P layout-only ranks on one device, ring plan with pointer hand-over in
-    place of ncclSend/Recv: embeddings within 1e-4 of the oracle's P-part epoch."""
+    place of ncclSend/Recv: embeddings within 1e-4 of the oracle's P-part epoch.
+    G > 1: the NEXT-3 two-level plan (G groups of P/G ranks)."""
     from paper_2005_13789_b200 import ne
     off, tgt = c1
     n = len(off) - 1
-    engs = [engine(rank=g, world=P) for g in range(P)]
+    engs = [engine(rank=g, world=P, groups=G) for g in range(P)]
     total = 0
     for e in engs:
         e.load_graph(off, tgt)
         e.random_walk(0, 0)
         total += e.build_samples(0, 0)
     st = ne.ne_train_samples_local_ring([e.ctx for e in engs], 0, 0, 0.025)
-    cfg = ocfg(parts=P)
+    cfg = ocfg(parts=P, groups=G)
     V = oracle.init_vertex(n, 128, 42)
     Cm = np.zeros_like(V)
     ns, loss = oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025)

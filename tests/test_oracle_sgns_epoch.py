@@ -271,3 +271,77 @@ def test_auc_matches_bruteforce_with_ties(orc):
         assert orc.auc(a, b) == orc.auc_bruteforce(a, b)
         assert orc.auc(a, a) == 0.5
         assert orc.auc(np.exp(a), np.exp(b)) == orc.auc(a, b)
+
+
+# ---------------------------------------------------------------- NEXT-3 two-level ring
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 6, 8])
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_two_level_plan_reduces_to_single_ring(orc, P, k):
+    # one group (one node) or one rank per group: both are the single ring
+    for rho in range(P):
+        for t in range(k):
+            for g in range(P):
+                s = orc.plan_vsub(P, k, rho, t, g)
+                assert orc.plan_vsub2(P, 1, k, rho, t, g) == s
+                assert orc.plan_vsub2(P, P, k, rho, t, g) == s
+
+
+@pytest.mark.parametrize("P,G", [(4, 2), (6, 2), (6, 3), (8, 2), (8, 4), (12, 3)])
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_two_level_plan_invariants(orc, P, G, k):
+    """SPEC build_schedule invariants, brute force: (a) per step no
+    sub-part on two ranks; (c) every (sub-part, context part) exactly once;
+    within a macro-round sub-parts rotate along the group's ring, between
+    macro-rounds the group's sub-parts move to the next group (P:150, P:190);
+    the first macro-round trains the group's own vertex parts ("all GPUs
+    from Node0 will first train on half of the vertex embeddings")."""
+    L = P // G
+    seen = set()
+    for rho in range(P):
+        R, r = divmod(rho, L)
+        for t in range(k):
+            step = [orc.plan_vsub2(P, G, k, rho, t, g) for g in range(P)]
+            assert len(set(step)) == P
+            for g, s in enumerate(step):
+                a, j = divmod(g, L)
+                seen.add((s, g))
+                assert s % k == t
+                part = s // k
+                assert part // L == (a - R) % G          # the group holds group (a - R)'s parts
+                if R == 0:
+                    assert part // L == a                # first macro-round: its own parts
+                nxt = a * L + (j + 1) % L if r < L - 1 else ((a + 1) % G) * L + (j + 1) % L
+                if rho + 1 < P:
+                    assert orc.plan_vsub2(P, G, k, rho + 1, t, nxt) == s
+                else:                                    # the final hop returns it home
+                    assert part == nxt
+    assert seen == {(s, g) for s in range(P * k) for g in range(P)}
+
+
+def test_two_level_epoch_equals_replay(orc):
+    # the oracle's epoch with groups = ordered replay of the two-level plan;
+    # and the plan matters: the single ring gives a different result
+    P, G, k = 4, 2, 2
+    off, tgt = synth.rmat_graph(160, 900, 6)
+    cfg = _cfg(orc, parts=P, subparts=k, groups=G)
+    V = orc.init_vertex(160, 16, 42)
+    Cm = np.zeros_like(V)
+    V2, C2, V3, C3 = V.copy(), Cm.copy(), V.copy(), Cm.copy()
+    orc.train_epoch(cfg, off, tgt, V, Cm, 1, 0.05)
+    thr, al = orc.build_alias_tables(cfg, off)
+    pb = orc.partition_bounds(0, 160, P).astype(np.int64)
+    pairs, boff = orc.build_episode(cfg, off, tgt, 1, 0)
+    L = P // G
+    for rho in range(P):
+        R, r = divmod(rho, L)
+        for t in range(k):
+            for g in range(P):
+                a, j = divmod(g, L)
+                B = ((((a - R) % G) * L + (j - r) % L) * k + t) * P + g
+                for p in range(int(boff[B + 1] - boff[B])):
+                    src, dst = pairs[int(boff[B]) + p]
+                    negs = orc.negatives(cfg, thr, al, int(pb[g]), int(pb[g + 1] - pb[g]), 1, 0, B, p)
+                    orc.train_sample(V2, C2, int(src), int(dst), negs, 0.05)
+    assert np.array_equal(V, V2) and np.array_equal(Cm, C2)
+    orc.train_epoch(_cfg(orc, parts=P, subparts=k), off, tgt, V3, C3, 1, 0.05)
+    assert not np.array_equal(V, V3)

@@ -4,7 +4,7 @@ moves vertex sub-parts with copy-engine pushes over CUDA IPC
 on a single-GPU box too (two or three processes on one device).  Rank 0
 compares with the oracle's P-part epochs: deterministic mode within 1e-4,
 Hogwild mode by held-out AUC within 0.01.  argv: mode (det|hogwild),
-storage (f32|bf16), staging (device)."""
+groups (NEXT-3 two-level ring, default 1)."""
 import os
 import sys
 
@@ -22,6 +22,7 @@ from paper_2005_13789_b200.engine import Engine  # noqa: E402
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     mode = sys.argv[1] if len(sys.argv) > 1 else "det"
+    groups = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     dev = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
     torch.cuda.set_device(dev)
     dist.init_process_group("gloo")
@@ -41,6 +42,7 @@ def main():
     else:
         off, tgt = synth.rmat_graph(3000, 24000, 11)
         epochs, kw = 2, dict(dim=64, walk_len=12, window=3, episodes=2, subparts=3)
+    kw["groups"] = groups
     n = len(off) - 1
     eng = Engine(deterministic=(mode == "det"), device=dev, rank=rank, world=world, nccl_id=None,
                  transport=ne.NE_TRANSPORT_IPC, **kw)
@@ -64,7 +66,7 @@ def main():
         Cg = np.concatenate([p[3] for p in parts])
         if mode == "det":
             dv, dc = float(np.abs(Vg - Vr).max()), float(np.abs(Cg - Cr).max())
-            print(f"IPC det world={world} samples={ns} max|dV|={dv:.3e} max|dC|={dc:.3e}", flush=True)
+            print(f"IPC det world={world} groups={groups} samples={ns} max|dV|={dv:.3e} max|dC|={dc:.3e}", flush=True)
             assert dv <= 1e-4 and dc <= 1e-4, (dv, dc)
         else:
             a_ref = oracle.auc(oracle.score_pairs(Vr, Cr, test), oracle.score_pairs(Vr, Cr, neg))

@@ -22,6 +22,8 @@ def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "det"
     kind = sys.argv[2] if len(sys.argv) > 2 else "deepwalk"
     extra = {"deepwalk": {}, "node2vec": dict(p=0.5, q=2.0), "line": dict(walk_len=0, window=0),
+             "groups2": dict(groups=2),  # NEXT-3 two-level ring: two groups of world/2 ranks
+             "ipc": dict(transport=ne.NE_TRANSPORT_IPC),  # copy-engine ring over CUDA IPC (+ NCCL pool build)
              # NEXT-4 bf16 rows over the ring, on a perfect matching (rows stored ~1+K times, the
              # element-wise bar of tests/test_gpu_bf16.py)
              "bf16": dict(walk_len=1, window=1, storage=1)}[kind]
@@ -44,7 +46,12 @@ def main():
     epochs = 5 if mode == "hogwild" else 2
     eng = Engine(dim=128, deterministic=(mode == "det"), device=local, rank=rank, world=world,
                  nccl_id=obj[0], episodes=2, **extra)
-    eng.load_graph(off, tgt)
+    def all_gather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    eng.load_graph(off, tgt, all_gather=all_gather)
     stats = [eng.train_epoch(ep, 0.025) for ep in range(epochs)]
     a, b = eng.part
     V, Cm = eng.embeddings(0), eng.embeddings(1)
@@ -53,7 +60,7 @@ def main():
     if rank == 0:
         base = dict(dim=128, negatives=5, walk_len=40, window=5, walks_per_node=1, episodes=2,
                     subparts=4, parts=world, seed=42)
-        base.update(extra)
+        base.update({k: v for k, v in extra.items() if k != "transport"})
         cfg = oracle.Config(**base)
         Vr = oracle.init_vertex(n, 128, 42)
         if kind == "bf16":
