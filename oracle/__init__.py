@@ -48,7 +48,7 @@ class _Config(C.Structure):
                 ("window", C.c_uint32), ("walks_per_node", C.c_uint32), ("episodes", C.c_uint32),
                 ("subparts", C.c_uint32), ("parts", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
                 ("update_rule", C.c_uint32), ("storage", C.c_uint32), ("seed", C.c_uint64),
-                ("groups", C.c_uint32)]
+                ("groups", C.c_uint32), ("batch", C.c_uint32)]
 
 
 class _Stats(C.Structure):
@@ -72,11 +72,12 @@ class Config:
     update_rule: int = 0  # 0 sequential (Alg. 1), 1 accumulated (word2vec, NEXT-4)
     storage: int = 0      # 0 fp32 rows, 1 bf16 rows (NEXT-4, reading D16)
     groups: int = 1       # NEXT-3 two-level ring: groups of parts/groups ranks (1 = one ring)
+    batch: int = 128      # update_rule 2 (NEXT-4 shared negatives): samples per mini-batch
 
     def c(self) -> _Config:
         return _Config(self.dim, self.negatives, self.walk_len, self.window, self.walks_per_node,
                        self.episodes, self.subparts, self.parts, self.p, self.q, self.update_rule,
-                       self.storage, self.seed, self.groups)
+                       self.storage, self.seed, self.groups, self.batch)
 
 
 _lib = None
@@ -146,6 +147,13 @@ def lib():
     L.or_plan_vsub.argtypes = [C.c_uint32] * 5
     L.or_plan_vsub.restype = C.c_uint32
     L.or_plan_vsub2.argtypes = [C.c_uint32] * 6
+    L.or_batch_negatives.argtypes = [C.POINTER(_Config), _u32p, _u32p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                     C.c_uint32, C.c_uint32, C.c_uint64, _u32p]
+    L.or_batch_loss_grad.argtypes = [_f32p, _f32p, C.c_uint32, _u32p, C.c_uint32, _u32p, C.c_uint32, _u32p,
+                                     _f64p, C.POINTER(C.c_uint32)]
+    L.or_batch_loss_grad.restype = C.c_double
+    L.or_train_batch.argtypes = [_f32p, _f32p, C.c_uint32, _u32p, C.c_uint32, _u32p, C.c_uint32, C.c_float]
+    L.or_train_batch.restype = C.c_double
     L.or_plan_vsub2.restype = C.c_uint32
     L.or_build_alias_tables.argtypes = [C.POINTER(_Config), C.c_uint64, _u64p, _u32p, _u32p]
     L.or_train_epoch_tables.argtypes = [C.POINTER(_Config), C.c_uint64, _u64p, _u32p, _u32p,
@@ -410,6 +418,40 @@ def train_sample(V, Cm, src: int, dst: int, negs, lr: float) -> float:
 
 def plan_vsub(P: int, k: int, r: int, t: int, g: int) -> int:
     return int(lib().or_plan_vsub(P, k, r, t, g))
+
+
+def batch_negatives(cfg: Config, thr, al, c_begin: int, c_count: int, epoch: int, episode: int,
+                    block: int, batch_index: int) -> np.ndarray:
+    out = np.zeros(max(cfg.negatives, 1), np.uint32)
+    c = cfg.c()
+    lib().or_batch_negatives(C.byref(c), np.ascontiguousarray(thr[c_begin:c_begin + c_count]),
+                             np.ascontiguousarray(al[c_begin:c_begin + c_count]), c_begin, c_count,
+                             epoch, episode, block, batch_index, out)
+    return out[: cfg.negatives]
+
+
+def batch_loss_grad(V, Cm, pairs, negs):
+    """NEXT-4 batch loss and its gradient: (L, {('v'|'c', row): grad[d]})."""
+    pairs = np.ascontiguousarray(pairs, np.uint32).reshape(-1)
+    negs = np.ascontiguousarray(negs, np.uint32)
+    B, Kp, d = len(pairs) // 2, len(negs), V.shape[1]
+    rows = np.zeros(2 * B + Kp, np.uint32)
+    grad = np.zeros((2 * B + Kp) * d, np.float64)
+    nr = C.c_uint32()
+    L = lib().or_batch_loss_grad(V.reshape(-1), Cm.reshape(-1), d, pairs, B, negs if Kp else np.zeros(1, np.uint32),
+                                 Kp, rows, grad, C.byref(nr))
+    out = {}
+    for i in range(nr.value):
+        key = ("c", int(rows[i]) & 0x7FFFFFFF) if rows[i] & 0x80000000 else ("v", int(rows[i]))
+        out[key] = grad[i * d:(i + 1) * d].copy()
+    return float(L), out
+
+
+def train_batch(V, Cm, pairs, negs, lr: float) -> float:
+    pairs = np.ascontiguousarray(pairs, np.uint32).reshape(-1)
+    negs = np.ascontiguousarray(negs, np.uint32)
+    return float(lib().or_train_batch(V.reshape(-1), Cm.reshape(-1), V.shape[1], pairs, len(pairs) // 2,
+                                      negs if len(negs) else np.zeros(1, np.uint32), len(negs), lr))
 
 
 def plan_vsub2(P: int, G: int, k: int, rho: int, t: int, g: int) -> int:

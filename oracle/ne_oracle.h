@@ -21,7 +21,7 @@
 #include <stddef.h>
 
 /* Philox counter tags (R1): c3 = (TAG << 24) | epoch. */
-enum { OR_TAG_WALK = 1, OR_TAG_NEG = 2, OR_TAG_SHUF = 3, OR_TAG_INIT = 4 };
+enum { OR_TAG_WALK = 1, OR_TAG_NEG = 2, OR_TAG_SHUF = 3, OR_TAG_INIT = 4, OR_TAG_BNEG = 8 };
 
 /* Configuration of one training run (mirrors the ABI's ne_config fields). */
 typedef struct {
@@ -34,10 +34,13 @@ typedef struct {
     uint32_t subparts;       /* vertex sub-parts per part, k=4         */
     uint32_t parts;          /* P context/vertex parts (GPUs)   */
     float    p, q;           /* node2vec return / in-out parameters; 1, 1 (or 0) = first order */
-    uint32_t update_rule;    /* 0 sequential (Alg. 1, D2); 1 accumulated (word2vec, NEXT-4) */
+    uint32_t update_rule;    /* 0 sequential (Alg. 1, D2); 1 accumulated (word2vec, NEXT-4);
+                                2 shared-negative mini-batch (NEXT-4, reading D17): batches of
+                                `batch` consecutive samples share `negatives` negatives */
     uint32_t storage;        /* 0 fp32 rows; 1 bf16 rows (NEXT-4, reading D16)  */
     uint64_t seed;           /* Philox key                                      */
     uint32_t groups;         /* NEXT-3 two-level ring: G groups ("nodes") of P/G ranks; 0 or 1 = one ring */
+    uint32_t batch;          /* update_rule 2: samples per mini-batch (B)        */
 } or_config;
 
 typedef struct {
@@ -104,6 +107,13 @@ void     or_sgns_total_grad(const double *v, const double *const *c, const int *
 double   or_train_sample_accumulated(float *V, float *C, uint32_t d, uint32_t src, uint32_t dst,
                                      const uint32_t *negs, uint32_t K, float lr);
 uint32_t or_plan_vsub(uint32_t P, uint32_t k, uint32_t r, uint32_t t, uint32_t g);
+void     or_batch_negatives(const or_config *cfg, const uint32_t *thr, const uint32_t *alias,
+                            uint64_t c_begin, uint64_t c_count, uint32_t epoch, uint32_t episode,
+                            uint32_t block, uint64_t batch_index, uint32_t *out);
+double   or_batch_loss_grad(const float *V, const float *C, uint32_t d, const uint32_t *pairs, uint32_t B,
+                            const uint32_t *negs, uint32_t Kp, uint32_t *rows, double *grad, uint32_t *nrows);
+double   or_train_batch(float *V, float *C, uint32_t d, const uint32_t *pairs, uint32_t B,
+                        const uint32_t *negs, uint32_t Kp, float lr);
 uint32_t or_plan_vsub2(uint32_t P, uint32_t G, uint32_t k, uint32_t rho, uint32_t t, uint32_t g);
 int      or_build_alias_tables(const or_config *cfg, uint64_t n, const uint64_t *offsets,
                                uint32_t *thr, uint32_t *alias);

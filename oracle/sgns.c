@@ -139,6 +139,77 @@ double or_train_sample_accumulated(float *V, float *C, uint32_t d, uint32_t src,
     return loss;
 }
 
+/* NEXT-4 shared-negative mini-batch (Ji et al. 2019, BlazingText; cited
+ * P:363-364 "forming the computation into mini-batches, they can share the
+ * negative samples within one mini-batch ... level-1 BLAS operations can be
+ * converted into level-3 BLAS"; reading D17).  The batch loss
+ *   L = sum_i [ l(v_{s_i} . c_{d_i}, 1) + sum_j l(v_{s_i} . c_{n_j}, 0) ],
+ *   l(x, y) = -y log s(x) - (1 - y) log(1 - s(x)), s clamped as in or_sigmoid,
+ * over the batch's B pairs (s_i, d_i) and its K' shared negatives n_j, and its
+ * gradient at the given V, C: dL/dv_r = sum over the terms whose vertex row is
+ * r of (s(x) - y) c, dL/dc_r = sum over the terms whose context row is r of
+ * (s(x) - y) v (a row used several times gets the sum).  rows[] receives the
+ * distinct rows touched -- vertex rows as their id, context rows as id | 2^31
+ * -- and grad[r * d ..] their gradients (fp64); returns L.  Capacity: 2B + K'
+ * rows. */
+static uint32_t row_slot(uint32_t *rows, uint32_t *nrows, uint32_t key)
+{
+    uint32_t i;
+    for (i = 0; i < *nrows; ++i)
+        if (rows[i] == key) return i;
+    rows[*nrows] = key;
+    return (*nrows)++;
+}
+
+double or_batch_loss_grad(const float *V, const float *C, uint32_t d, const uint32_t *pairs, uint32_t B,
+                          const uint32_t *negs, uint32_t Kp, uint32_t *rows, double *grad, uint32_t *nrows)
+{
+    uint32_t i, j, m;
+    double L = 0.0;
+    *nrows = 0;
+    for (i = 0; i < 2 * B + Kp; ++i)
+        for (m = 0; m < d; ++m) grad[(size_t)i * d + m] = 0.0;
+    for (i = 0; i < B; ++i) {
+        const float *v = V + (size_t)pairs[2 * i] * d;
+        const uint32_t rv = row_slot(rows, nrows, pairs[2 * i]);
+        for (j = 0; j <= Kp; ++j) {
+            const uint32_t cid = j == 0 ? pairs[2 * i + 1] : negs[j - 1];
+            const float *c = C + (size_t)cid * d;
+            const uint32_t rc = row_slot(rows, nrows, cid | 0x80000000u);
+            double x = 0.0, s, g;
+            for (m = 0; m < d; ++m) x += (double)v[m] * (double)c[m];
+            s = or_sigmoid(x);
+            g = s - (j == 0 ? 1.0 : 0.0);
+            L += j == 0 ? -log(s) : -log(1.0 - s);
+            for (m = 0; m < d; ++m) {
+                grad[(size_t)rv * d + m] += g * (double)c[m];
+                grad[(size_t)rc * d + m] += g * (double)v[m];
+            }
+        }
+    }
+    return L;
+}
+
+/* One SGD step on the batch loss from the batch-start values (the whole
+ * mini-batch sees the same V, C -- its dots are one matrix product): every
+ * touched row r <- (float)(r - lr * dL/dr).  Returns L. */
+double or_train_batch(float *V, float *C, uint32_t d, const uint32_t *pairs, uint32_t B,
+                      const uint32_t *negs, uint32_t Kp, float lr)
+{
+    const uint32_t cap = 2 * B + Kp;
+    uint32_t *rows = (uint32_t *)malloc(cap * sizeof(uint32_t)), nrows = 0, r, m;
+    double *grad = (double *)malloc((size_t)cap * d * sizeof(double)), L, eta = (double)lr;
+    if (!rows || !grad) { free(rows); free(grad); return NAN; }
+    L = or_batch_loss_grad(V, C, d, pairs, B, negs, Kp, rows, grad, &nrows);
+    for (r = 0; r < nrows; ++r) {
+        float *row = (rows[r] & 0x80000000u) ? C + (size_t)(rows[r] & 0x7FFFFFFFu) * d : V + (size_t)rows[r] * d;
+        for (m = 0; m < d; ++m) row[m] = (float)((double)row[m] - eta * grad[(size_t)r * d + m]);
+    }
+    free(rows);
+    free(grad);
+    return L;
+}
+
 /* Alias tables of every context part (O3), part-local ids, stored at the
  * global row index of each part's first row. */
 int or_build_alias_tables(const or_config *cfg, uint64_t n, const uint64_t *offsets,
@@ -241,10 +312,11 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
     uint64_t *boff = NULL;
     uint32_t *pairs = NULL, negs[256], e;
     if (P == 0 || P > 256 || k == 0 || nblocks > 4096 || K > 256 || d == 0 || d > 4096 ||
+        (cfg->update_rule == 2 && (cfg->batch == 0 || cfg->batch > 4096)) ||
         cfg->episodes == 0 || cfg->episodes > 4096 || epoch >= (1u << 24))
         return -1;
     if (cfg->walk_len > 0 && (cfg->window == 0 || cfg->walks_per_node == 0)) return -1;
-    if (cfg->update_rule > 1 || cfg->storage > 1) return -1;
+    if (cfg->update_rule > 2 || cfg->storage > 1 || (cfg->update_rule == 2 && cfg->storage != 0)) return -1;
     if (cfg->groups > 1 && P % cfg->groups != 0) return -1;
     or_partition_bounds(0, n, P, bounds);
     boff = (uint64_t *)malloc((nblocks + 1) * sizeof(uint64_t));
@@ -267,6 +339,17 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
                                                  : or_plan_vsub(P, k, r, t, g);
                     uint32_t B = s * P + g;
                     uint64_t p, cb = bounds[g], cn = bounds[g + 1] - bounds[g];
+                    if (cfg->update_rule == 2) {  /* NEXT-4: consecutive mini-batches of the block */
+                        const uint64_t cnt = boff[B + 1] - boff[B], Bt = cfg->batch;
+                        for (p = 0; p < cnt; p += Bt) {
+                            const uint32_t nb = (uint32_t)(cnt - p < Bt ? cnt - p : Bt);
+                            double loss;
+                            if (K > 0) or_batch_negatives(cfg, thr + cb, alias + cb, cb, cn, epoch, e, B, p / Bt, negs);
+                            loss = or_train_batch(V, C, d, pairs + 2 * (boff[B] + p), nb, negs, K, lr);
+                            if (stats) { stats->samples += nb; stats->loss_sum += loss; }
+                        }
+                        continue;
+                    }
                     for (p = 0; p < boff[B + 1] - boff[B]; ++p) {
                         const uint32_t *pr = pairs + 2 * (boff[B] + p);
                         double loss;
