@@ -61,7 +61,7 @@ enum {
 enum { NE_WB_ATOMIC_DELTA = 0, NE_WB_STORE = 1 };
 
 /* ne_config.update_rule */
-enum { NE_UPDATE_SEQUENTIAL = 0, NE_UPDATE_ACCUMULATED = 1 };
+enum { NE_UPDATE_SEQUENTIAL = 0, NE_UPDATE_ACCUMULATED = 1, NE_UPDATE_SHARED_BATCH = 2 };
 
 /* ne_config.staging */
 enum { NE_STAGE_DEVICE = 0, NE_STAGE_HOST = 1 };
@@ -117,7 +117,13 @@ typedef struct {
                                 in order, each seeing the updated vertex row (D2);
                                 NE_UPDATE_ACCUMULATED (1): word2vec / GraphVite style --
                                 all 1+K dots use the pre-sample vertex row, whose
-                                accumulated gradient is applied once (NEXT-4)       */
+                                accumulated gradient is applied once (NEXT-4);
+                                NE_UPDATE_SHARED_BATCH (2): mini-batches of 128
+                                consecutive samples share `negatives` (32 or 64)
+                                negatives and take one SGD step on the batch loss
+                                (Ji et al. / BlazingText; DESIGN D17) --
+                                three tf32 tensor-core products per batch (tcgen05,
+                                TMEM accumulators); dim must be 128, fp32 rows      */
     uint32_t staging;        /* NE_STAGE_DEVICE (0): the vertex matrix lives in HBM;
                                 NE_STAGE_HOST (1): in pinned host memory, streamed
                                 through 3 device sub-part slots -- H2D of sub-part t+1

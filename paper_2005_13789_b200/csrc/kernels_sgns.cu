@@ -29,6 +29,7 @@ namespace ne {
 
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s) {
     if (p.count == 0) return cudaSuccess;
+    if (p.accumulate == 2) return launch_sgns_batch(p, dev, s);  // NEXT-4 shared negatives (tcgen05)
     if (p.K > (uint32_t)kMaxK || p.d % 4 != 0 || p.d == 0 || p.d > 512) return cudaErrorInvalidValue;
     if (p.bf16) return launch_sgns_bf16(p, dev, s);
     return launch_sgns_rows<false>(p, dev, s);

@@ -1,0 +1,372 @@
+// kernels_sgns_batch.cu -- NEXT-4 shared-negative mini-batch SGNS on the 5th
+// generation tensor cores (sm_100a tcgen05 + TMEM).
+//
+// Rule (reading D17; Ji et al. 2019 and BlazingText, cited P:363-364: "forming
+// the computation into mini-batches, they can share the negative samples
+// within one mini-batch ... level-1 BLAS operations can be converted into
+// level-3 BLAS matrix multiply operations"): a block's samples are taken in
+// canonical order in mini-batches of B = 128; the batch's K' negatives are
+// shared by all its samples; the batch takes ONE SGD step on its loss
+//   L = sum_i [ l(v_i . c+_i, 1) + sum_j l(v_i . n_j, 0) ]
+// from the batch-start values.  With V (B x d), N (K' x d), the negative part
+// is three dense contractions:
+//   S  = V N^T              (B x K')   logits            -> TMEM
+//   G  = lr * sigma(S)      (B x K')   (epilogue, in smem)
+//   dV = G N                (B x d)    vertex gradients  -> TMEM
+//   dN^T = V^T G            (d x K')   negative gradients -> TMEM
+// each issued as tcgen05.mma.kind::tf32 (fp32 rows, tf32 products, fp32
+// accumulation in TMEM) by one thread.  The positive term of each sample is a
+// d-long dot (CUDA cores, from shared memory).
+//
+// One CTA of 128 threads (thread i <-> batch row i <-> TMEM lane i) per batch;
+// the persistent grid strides over the block's batches (Hogwild: concurrent
+// batches share rows; every write-back is a red.global.add of the delta), the
+// deterministic mode runs one CTA over the batches in order.
+//
+// Shared-memory tiles use the UMMA canonical no-swizzle ("interleaved") layout:
+// 8-row x 16-byte core matrices, row r chunk c (4 floats) at byte
+//   ((r / 8) * (cols / 4) + c) * 128 + (r % 8) * 16.
+// The same bytes serve as a K-major operand (K = the column index; LBO = 128 B
+// between K chunks, SBO = cols * 32 B between row groups) and as an MN-major
+// operand (MN = the column index; SBO = 128 B between column groups of 4,
+// LBO = cols * 32 B between groups of 8 rows = 8 K values), so no tile is ever
+// transposed: MMA1 reads V and N K-major, MMA2 reads G K-major and N MN-major,
+// MMA3 reads V and G MN-major.
+#include <algorithm>
+
+#include "ne_device.cuh"
+#include "ne_internal.h"
+
+namespace ne {
+
+namespace {
+
+constexpr int kBatch = 128;      // B = UMMA M = threads per CTA = TMEM lanes
+constexpr uint32_t kTagBNeg = 8;
+
+// ---- tcgen05 / mbarrier primitives (PTX ISA 8.7, sm_100a) ----------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_NONE (layout type 0), version 1.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;  // version = 1 (sm_100)
+    return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE
+}
+
+// Instruction descriptor of kind::tf32: D fp32, A/B tf32, M x N, majors.
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N, bool a_mn, bool b_mn) {
+    return (1u << 4)                      // c_format = F32
+         | (2u << 7)                      // a_format = TF32
+         | (2u << 10)                     // b_format = TF32
+         | ((a_mn ? 1u : 0u) << 15)       // a_major
+         | ((b_mn ? 1u : 0u) << 16)       // b_major
+         | ((N >> 3) << 17)               // n_dim
+         | ((M >> 4) << 24);              // m_dim
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, bool acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"((uint32_t)acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}\n"
+        ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// 32 consecutive TMEM columns of this thread's lane (32x32b shape, x32).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Byte offset of (row, 4-float chunk) in a no-swizzle tile with `cols` columns.
+__device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t chunk, uint32_t cols) {
+    return ((row >> 3) * (cols >> 2) + chunk) * 128u + (row & 7u) * 16u;
+}
+
+__device__ __forceinline__ float sigmoid_clamped(float x, float& ex) {
+    x = fminf(fmaxf(x, -30.f), 30.f);
+    ex = __expf(-x);
+    return __fdividef(1.f, 1.f + ex);
+}
+
+}  // namespace
+
+// D: embedding dimension (UMMA M of the dN^T product: 128); KP: shared
+// negatives per batch (UMMA N of S and dN^T).
+template <int D, int KP>
+__global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
+    static_assert(D == 128, "the dN^T product has M = d: 128");
+    static_assert(KP == 32 || KP == 64, "K' in {32, 64} (shared memory: 2 x 64 KB + 2 x 32 KB at 64)");
+    constexpr uint32_t kTileV = kBatch * D * 4, kTileN = KP * D * 4, kTileG = kBatch * KP * 4;
+    constexpr uint32_t kTmemCols = 256;  // S: KP, dV: D, dN^T: KP (<= 256)
+    static_assert(2 * KP + D <= (int)kTmemCols, "TMEM columns");
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* sV = smem;                  // batch vertex rows, B x D
+    unsigned char* sC = sV + kTileV;           // batch positive context rows, B x D
+    unsigned char* sN = sC + kTileV;           // shared negative rows, KP x D
+    unsigned char* sG = sN + kTileN;           // G = lr sigma(S), B x KP; later dN rows (KP x D, row-major)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sG + kTileG);   // [0]: S ready, [1]: dV, dN^T ready
+    uint32_t* tmem_base = reinterpret_cast<uint32_t*>(bar + 2);
+    uint32_t* s_src = tmem_base + 4;           // kBatch
+    uint32_t* s_dst = s_src + kBatch;          // kBatch
+    uint32_t* s_neg = s_dst + kBatch;          // KP
+
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                     ::"r"(smem_u32(tmem_base)), "n"(kTmemCols) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_base;
+    const uint32_t t_S = tmem, t_dV = tmem + KP, t_dNt = tmem + KP + D;
+    const uint32_t lane_base = (warp * 32u) << 16;  // this warp's TMEM lanes
+
+    const uint2 key = key_of(p.seed);
+    const uint32_t tagw = tag_word(kTagBNeg, p.epoch);
+    const float lr = p.lr;
+    const uint64_t nbatch = (p.count + kBatch - 1) / kBatch;
+    const uint32_t i = tid;  // batch row of this thread
+    constexpr uint32_t idesc1 = idesc_tf32(kBatch, KP, false, false);  // S = V N^T
+    constexpr uint32_t idesc2 = idesc_tf32(kBatch, D, false, true);    // dV = G N
+    constexpr uint32_t idesc3 = idesc_tf32(D, KP, true, true);         // dN^T = V^T G
+    double loss = 0.0;
+    uint32_t phase = 0;
+
+    for (uint64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
+        const uint64_t p0 = b * kBatch;
+        const uint32_t nb = (uint32_t)(p.count - p0 < (uint64_t)kBatch ? p.count - p0 : (uint64_t)kBatch);
+        // ---- ids: pairs, shared negatives (O8 with the batch counter, tag BNEG)
+        if (i < nb) {
+            const uint2 pr = p.pool[p0 + i];
+            s_src[i] = pr.x;
+            s_dst[i] = pr.y;
+        }
+        if (i < (uint32_t)KP) {
+            const uint4 x = philox(make_uint4((uint32_t)b, (uint32_t)(b >> 32), (p.episode << 20) | (p.block << 8) | i,
+                                              tagw), key);
+            const uint32_t col = (uint32_t)uniform_index(x.x, x.y, p.c_count);
+            const uint2 ta = __ldg(p.alias + col);
+            s_neg[i] = (uint32_t)(p.c_begin + (x.z < ta.x ? col : ta.y));
+        }
+        __syncthreads();
+        // ---- gather rows into the UMMA tiles (cp.async, 16 B per lane; a warp
+        // covers 8 rows x 4 chunks so each quarter-warp writes 128 contiguous bytes)
+        constexpr uint32_t KC = D / 4;
+        for (uint32_t f = tid; f < kBatch * KC; f += kBatch) {
+            const uint32_t q = f >> 5, l = f & 31u;
+            const uint32_t row = (q / (KC / 4)) * 8 + (l & 7u), chunk = (q % (KC / 4)) * 4 + (l >> 3);
+            const uint32_t off = tile_off(row, chunk, D);
+            if (row < nb) {
+                cp_async16(sV + off, p.V + (uint64_t)(s_src[row] - p.v_begin) * D + chunk * 4);
+                cp_async16(sC + off, p.C + (uint64_t)(s_dst[row] - p.c_begin) * D + chunk * 4);
+            } else {
+                *reinterpret_cast<float4*>(sV + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(sC + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            if (row < (uint32_t)KP)
+                cp_async16(sN + off, p.C + (uint64_t)(s_neg[row] - p.c_begin) * D + chunk * 4);
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        fence_async_smem();
+        __syncthreads();
+        // ---- MMA1: S = V N^T (K = D, 8 per instruction = 2 chunks = 256 B)
+        if (tid == 0) {
+            fence_after();
+#pragma unroll
+            for (uint32_t ks = 0; ks < D / 8; ++ks) {
+                const uint64_t a = umma_desc(smem_u32(sV) + ks * 256u, 128u, D * 32u);
+                const uint64_t bb = umma_desc(smem_u32(sN) + ks * 256u, 128u, D * 32u);
+                mma_tf32(t_S, a, bb, idesc1, ks > 0);
+            }
+            mma_commit(&bar[0]);
+        }
+        // ---- positive term of row i (CUDA cores, overlapping MMA1)
+        float gpos = 0.f;
+        if (i < nb) {
+            float x = 0.f;
+#pragma unroll 8
+            for (uint32_t c = 0; c < KC; ++c) {
+                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(i, c, D));
+                const float4 cc = *reinterpret_cast<const float4*>(sC + tile_off(i, c, D));
+                x = fmaf(v.x, cc.x, fmaf(v.y, cc.y, fmaf(v.z, cc.z, fmaf(v.w, cc.w, x))));
+            }
+            float ex;
+            const float s = sigmoid_clamped(x, ex);
+            gpos = lr * (s - 1.f);
+            loss += (double)__logf(1.f + ex);  // -log s
+        }
+        // ---- epilogue 1: G = lr sigma(S) (rows of padding stay 0)
+        mbar_wait(&bar[0], phase);
+        fence_after();
+#pragma unroll
+        for (uint32_t j0 = 0; j0 < (uint32_t)KP; j0 += 32) {
+            float sv[32];
+            tmem_ld32(t_S + lane_base + j0, sv);
+#pragma unroll
+            for (uint32_t c = 0; c < 8; ++c) {
+                float4 g;
+                float* gp = &g.x;
+#pragma unroll
+                for (uint32_t e = 0; e < 4; ++e) {
+                    float ex;
+                    const float xcl = fminf(fmaxf(sv[c * 4 + e], -30.f), 30.f);
+                    const float s = sigmoid_clamped(sv[c * 4 + e], ex);
+                    gp[e] = i < nb ? lr * s : 0.f;
+                    if (i < nb) loss += (double)(__logf(1.f + ex) + xcl);  // -log(1 - s)
+                }
+                *reinterpret_cast<float4*>(sG + tile_off(i, (j0 >> 2) + c, KP)) = g;
+            }
+        }
+        fence_async_smem();
+        fence_before();
+        __syncthreads();
+        // ---- MMA2: dV = G N (K = KP); MMA3: dN^T = V^T G (K = B)
+        if (tid == 0) {
+            fence_after();
+#pragma unroll
+            for (uint32_t ks = 0; ks < (uint32_t)KP / 8; ++ks) {
+                const uint64_t a = umma_desc(smem_u32(sG) + ks * 256u, 128u, KP * 32u);       // G, K-major
+                const uint64_t bb = umma_desc(smem_u32(sN) + ks * D * 32u, D * 32u, 128u);    // N, MN-major
+                mma_tf32(t_dV, a, bb, idesc2, ks > 0);
+            }
+#pragma unroll
+            for (uint32_t ks = 0; ks < (uint32_t)kBatch / 8; ++ks) {
+                const uint64_t a = umma_desc(smem_u32(sV) + ks * D * 32u, D * 32u, 128u);     // V^T, MN-major
+                const uint64_t bb = umma_desc(smem_u32(sG) + ks * KP * 32u, KP * 32u, 128u);  // G, MN-major
+                mma_tf32(t_dNt, a, bb, idesc3, ks > 0);
+            }
+            mma_commit(&bar[1]);
+        }
+        mbar_wait(&bar[1], phase);
+        fence_after();
+        // ---- write-back, all deltas from the batch-start snapshot (the
+        // tcgen05.ld are warp-collective: every thread runs them, padding rows
+        // skip only the stores)
+        {
+            const bool live = i < nb;
+            float* vrow = p.V + (uint64_t)((live ? s_src[i] : p.v_begin) - p.v_begin) * D;
+            float* crow = p.C + (uint64_t)((live ? s_dst[i] : p.c_begin) - p.c_begin) * D;
+#pragma unroll 1
+            for (uint32_t d0 = 0; d0 < (uint32_t)D; d0 += 32) {
+                float dv[32];
+                tmem_ld32(t_dV + lane_base + d0, dv);
+                if (!live) continue;
+#pragma unroll
+                for (uint32_t c = 0; c < 8; ++c) {
+                    const uint32_t ch = (d0 >> 2) + c;
+                    const float4 cc = *reinterpret_cast<const float4*>(sC + tile_off(i, ch, D));
+                    const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(i, ch, D));
+                    atomicAdd(reinterpret_cast<float4*>(vrow) + ch,
+                              make_float4(-(dv[4 * c] + gpos * cc.x), -(dv[4 * c + 1] + gpos * cc.y),
+                                          -(dv[4 * c + 2] + gpos * cc.z), -(dv[4 * c + 3] + gpos * cc.w)));
+                    atomicAdd(reinterpret_cast<float4*>(crow) + ch,
+                              make_float4(-gpos * v.x, -gpos * v.y, -gpos * v.z, -gpos * v.w));
+                }
+            }
+        }
+        // dN^T: TMEM lane = dimension, column = negative j; stage dN rows in the
+        // G tile (MMA3 has consumed it) and add them with coalesced row reductions
+        __syncthreads();
+        float* sDN = reinterpret_cast<float*>(sG);  // KP x D, row-major
+#pragma unroll
+        for (uint32_t j0 = 0; j0 < (uint32_t)KP; j0 += 32) {
+            float dn[32];
+            tmem_ld32(t_dNt + lane_base + j0, dn);
+#pragma unroll
+            for (uint32_t e = 0; e < 32; ++e) sDN[(j0 + e) * D + i] = dn[e];
+        }
+        fence_before();
+        __syncthreads();
+        for (uint32_t j = warp; j < (uint32_t)KP; j += kBatch / 32) {
+            float* nrow = p.C + (uint64_t)(s_neg[j] - p.c_begin) * D;
+            for (uint32_t ch = lane; ch < KC; ch += 32) {
+                const float4 g = reinterpret_cast<const float4*>(sDN + j * D)[ch];
+                atomicAdd(reinterpret_cast<float4*>(nrow) + ch, make_float4(-g.x, -g.y, -g.z, -g.w));
+            }
+        }
+        __syncthreads();
+        phase ^= 1u;
+    }
+    if (loss != 0.0) atomicAdd(p.loss, loss);
+    fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols) : "memory");
+}
+
+template <int D, int KP>
+static cudaError_t launch_batch(const SgnsParams& p, const Device& dev, cudaStream_t s) {
+    constexpr size_t smem = 2ull * kBatch * D * 4 + (size_t)KP * D * 4 + (size_t)kBatch * KP * 4 + 16 + 16 +
+                            (2 * kBatch + KP) * 4;
+    auto kern = sgns_batch_kernel<D, KP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t nbatch = (p.count + kBatch - 1) / kBatch;
+    const unsigned grid = p.deterministic ? 1u : (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(
+                                                     nbatch, (uint64_t)std::max(1, dev.sm_count - p.reserve_sms)));
+    kern<<<grid, kBatch, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sgns_batch(const SgnsParams& p, const Device& dev, cudaStream_t s) {
+    if (p.count == 0) return cudaSuccess;
+    if (p.d != 128 || p.bf16) return cudaErrorNotSupported;
+    switch (p.K) {
+        case 32: return launch_batch<128, 32>(p, dev, s);
+        case 64: return launch_batch<128, 64>(p, dev, s);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+}  // namespace ne

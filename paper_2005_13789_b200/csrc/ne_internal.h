@@ -140,12 +140,15 @@ struct SgnsParams {
     int atomic_writeback;       // Hogwild: red.add row deltas instead of storing rows
     int reserve_sms;            // SMs left free for the concurrent NCCL ring kernels
     int bf16;                   // rows stored as bfloat16 (NEXT-4, reading D16); V, C point at them
-    int accumulate;             // NEXT-4 accumulated-gradient update (word2vec order)
+    int accumulate;             // update rule: 0 sequential, 1 accumulated (word2vec), 2 shared-negative batch
     uint32_t* capture;          // test hook: (src, dst, negs) per position, [count][2+K] (nullptr: off)
 };
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s);
 // bf16-row instantiations (kernels_sgns_bf16.cu); launch_sgns dispatches on p.bf16.
 cudaError_t launch_sgns_bf16(const SgnsParams& p, const Device& dev, cudaStream_t s);
+// NEXT-4 shared-negative mini-batch rule (p.accumulate == 2; kernels_sgns_batch.cu):
+// batches of 128 samples share p.K negatives; tcgen05 tf32 products.  d == 128.
+cudaError_t launch_sgns_batch(const SgnsParams& p, const Device& dev, cudaStream_t s);
 cudaError_t launch_export_negatives(const SgnsParams& p, uint64_t pos_begin, uint64_t count,
                                     uint32_t* out, const Device& dev, cudaStream_t s);
 

@@ -909,7 +909,13 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     const ne_config& g = *cfg;
     if (g.dim == 0 || g.dim % 4 || g.dim > 512)
         return bad(ne_fail(c, NE_EINVAL, "dim=%u must be a multiple of 4 in [4, 512]", g.dim));
-    if (g.negatives > 8) return bad(ne_fail(c, NE_EINVAL, "negatives=%u > 8", g.negatives));
+    if (g.update_rule == NE_UPDATE_SHARED_BATCH) {
+        if (g.dim != 128 || (g.negatives != 32 && g.negatives != 64) || g.storage != NE_STORE_F32)
+            return bad(ne_fail(c, NE_EINVAL, "update_rule=2 (shared-negative batches) needs dim=128, negatives in "
+                                             "{32, 64} and fp32 storage (dim=%u negatives=%u)", g.dim, g.negatives));
+    } else if (g.negatives > 8) {
+        return bad(ne_fail(c, NE_EINVAL, "negatives=%u > 8", g.negatives));
+    }
     if (g.walk_len > 255) return bad(ne_fail(c, NE_EINVAL, "walk_len=%u > 255", g.walk_len));
     if (g.walk_len > 0 && (g.window == 0 || g.window > g.walk_len))
         return bad(ne_fail(c, NE_EINVAL, "window=%u not in [1, walk_len=%u]", g.window, g.walk_len));
@@ -918,8 +924,8 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     if (g.episodes == 0 || g.episodes > 4095)
         return bad(ne_fail(c, NE_EINVAL, "episodes=%u not in [1, 4095]", g.episodes));
     if (g.writeback > NE_WB_STORE) return bad(ne_fail(c, NE_EINVAL, "writeback=%u not in {0, 1}", g.writeback));
-    if (g.update_rule > NE_UPDATE_ACCUMULATED)
-        return bad(ne_fail(c, NE_EINVAL, "update_rule=%u not in {0, 1}", g.update_rule));
+    if (g.update_rule > NE_UPDATE_SHARED_BATCH)
+        return bad(ne_fail(c, NE_EINVAL, "update_rule=%u not in {0, 1, 2}", g.update_rule));
     if (g.staging > NE_STAGE_HOST) return bad(ne_fail(c, NE_EINVAL, "staging=%u not in {0, 1}", g.staging));
     if (g.storage > NE_STORE_BF16) return bad(ne_fail(c, NE_EINVAL, "storage=%u not in {0, 1}", g.storage));
     if (g.transport > NE_TRANSPORT_IPC)

@@ -26,7 +26,7 @@ NE_REUSE_SAMPLES = 1
 NE_CHECK_BLOCKS = 2
 NE_VERTEX, NE_CONTEXT = 0, 1
 NE_WB_ATOMIC_DELTA, NE_WB_STORE = 0, 1
-NE_UPDATE_SEQUENTIAL, NE_UPDATE_ACCUMULATED = 0, 1
+NE_UPDATE_SEQUENTIAL, NE_UPDATE_ACCUMULATED, NE_UPDATE_SHARED_BATCH = 0, 1, 2
 NE_STAGE_DEVICE, NE_STAGE_HOST = 0, 1
 NE_STORE_F32, NE_STORE_BF16 = 0, 1
 NE_TRANSPORT_NCCL, NE_TRANSPORT_IPC = 0, 1
