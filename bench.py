@@ -230,6 +230,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--episodes", type=int, default=0, help="episodes per epoch (0 = workload default)")
     ap.add_argument("--subparts", type=int, default=4, help="vertex sub-parts per GPU (the paper's k, P:152)")
+    ap.add_argument("--staging", default="device", choices=["device", "host"],
+                    help="vertex matrix in HBM (device) or in pinned host memory streamed through device slots "
+                         "(host: NEXT-2, the paper's pipeline stages 2 and 5, P:142)")
+    ap.add_argument("--rule", default="sequential", choices=["sequential", "accumulated", "batch"],
+                    help="update rule: Alg. 1 sequential (the headline), accumulated (word2vec), or batch "
+                         "(NEXT-4 shared negatives: 128-sample batches share 64 negatives, tcgen05 tf32)")
     ap.add_argument("--storage", default="f32", choices=["f32", "bf16"],
                     help="row storage: f32 (the paper's, the headline) or bf16 (NEXT-4 option, reading D16)")
     args = ap.parse_args()
@@ -265,8 +271,12 @@ def main():
     # transfers, left on the library's comm stream, into it)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    eng = Engine(dim=w.dim, negatives=w.negatives, walk_len=w.walk_len, window=w.window,
+    rule = {"sequential": ne.NE_UPDATE_SEQUENTIAL, "accumulated": ne.NE_UPDATE_ACCUMULATED,
+            "batch": ne.NE_UPDATE_SHARED_BATCH}[args.rule]
+    negatives = 64 if args.rule == "batch" else w.negatives
+    eng = Engine(dim=w.dim, negatives=negatives, walk_len=w.walk_len, window=w.window,
                  walks_per_node=1, episodes=episodes, subparts=args.subparts, deterministic=False, seed=42,
+                 update_rule=rule, staging=ne.NE_STAGE_HOST if args.staging == "host" else ne.NE_STAGE_DEVICE,
                  p=w.p, q=w.q, storage=ne.NE_STORE_BF16 if args.storage == "bf16" else ne.NE_STORE_F32,
                  device=local, rank=rank, world=world, nccl_id=nccl_id, torch_allocator=True,
                  stream=stream.cuda_stream)
@@ -312,6 +322,8 @@ def main():
     # roofline of the dominant kernel (SGNS), this rank's launches
     esz = 2 if args.storage == "bf16" else 4
     B = alg_bytes_per_sample(w.dim, w.negatives, esz)
+    if args.rule == "batch":  # per sample: pair, its vertex + positive rows (read + write), 64/128 of a shared
+        B = 8 + 8 * 64 / 128 + 2 * esz * w.dim * (2 + 64 / 128)  # negative row and of its alias entry
     achieved = samples * B / (ms_train / 1e3) / 1e9 if ms_train > 0 else 0.0
     peak, peak_src = hbm_peak()
     traffic = dram_achieved = None
@@ -371,10 +383,15 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-            "dtype": "f32" if esz == 4 else "bf16 rows, f32 arithmetic (NEXT-4 option; not the headline)",
+            "dtype": ("f32 rows, tf32 tensor-core products (NEXT-4 shared-negative batches; not the headline)"
+                      if args.rule == "batch" else
+                      "f32" if esz == 4 else "bf16 rows, f32 arithmetic (NEXT-4 option; not the headline)"),
             "data": "synthetic",
             "config": {"workload": desc, "step": "one epoch: walk + augment + order/bucket + SGNS (+ ring)",
                        "samples_per_step": samples_all / args.steps, "episodes": episodes, "subparts": args.subparts,
+                       "update_rule": args.rule + (" (K'=64 negatives shared per 128-sample batch)"
+                                                   if args.rule == "batch" else ""),
+                       "staging": args.staging,
                        "mode": "hogwild", "parallelism": f"2D ring x{world}",
                        "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * esz / 1e9),
                        "graph_generator": "numpy Philox (host)" if w.m <= 200_000_000 else "torch CUDA generator"},
@@ -384,7 +401,8 @@ def main():
                          # profile) x this run's samples / SGNS time -- frac counts L2 hits as HBM bytes
                          "dram_achieved": dram_achieved,
                          "dram_frac": dram_achieved / peak if dram_achieved else None,
-                         "kernel": sgns_kernel_name(w.dim, w.negatives, esz == 2),
+                         "kernel": ("ne::sgns_batch_kernel<128,64> (tcgen05.mma kind::tf32, TMEM accumulators)"
+                                    if args.rule == "batch" else sgns_kernel_name(w.dim, w.negatives, esz == 2)),
                          "bytes_per_sample": B, "launches": train_launches,
                          "avg_launch_ms": ms_train / max(train_launches, 1), "peak_source": peak_src},
             "phases_ms_per_step": {"walk": float(tsum[4]) / world / args.steps,
