@@ -125,11 +125,14 @@ typedef struct {
                                 three tf32 tensor-core products per batch (tcgen05,
                                 TMEM accumulators); dim must be 128, fp32 rows      */
     uint32_t staging;        /* NE_STAGE_DEVICE (0): the vertex matrix lives in HBM;
-                                NE_STAGE_HOST (1): in pinned host memory, streamed
-                                through 3 device sub-part slots -- H2D of sub-part t+1
-                                and D2H of t-1 overlap the training of t (the paper's
-                                pipeline stages 5 and 2; NEXT-2).
-                                Single rank only (world == 1).                         */
+                                NE_STAGE_HOST (1): in pinned host memory (each rank its
+                                own part), streamed through device sub-part slots --
+                                one GPU: 3 slots, H2D of sub-part t+1 and D2H of t-1
+                                overlap the training of t (the paper's pipeline stages
+                                5 and 2; NEXT-2); world > 1 (NCCL
+                                transport): the sub-parts go around the ring in windows
+                                of stage_window slots (3 x stage_window device slots,
+                                stages 5, 3, 4, 2), DESIGN reading D18.               */
     uint32_t storage;        /* NE_STORE_F32 (0): fp32 rows, the paper's precision;
                                 NE_STORE_BF16 (1): rows stored as bfloat16 (NEXT-4,
                                 DESIGN reading D16) -- half the bytes per sample;
@@ -146,6 +149,9 @@ typedef struct {
                                 id == NULL: no NCCL at all (each rank then builds its
                                 part's pool from every walker, the layout-only way). */
     uint64_t seed;           /* Philox key (contract R1)                                */
+    uint32_t stage_window;   /* NE_STAGE_HOST with world > 1: sub-parts per ring window
+                                (w <= subparts; 0 = 2).  The plan trains the windows one
+                                after the other, each through all world rounds.       */
     uint32_t groups;         /* NEXT-3 two-level ring (P:150 hierarchical partitioning,
                                 P:190-191): the world's ranks form `groups` groups
                                 ("nodes") of world/groups consecutive ranks; each group

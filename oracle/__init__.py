@@ -48,7 +48,7 @@ class _Config(C.Structure):
                 ("window", C.c_uint32), ("walks_per_node", C.c_uint32), ("episodes", C.c_uint32),
                 ("subparts", C.c_uint32), ("parts", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
                 ("update_rule", C.c_uint32), ("storage", C.c_uint32), ("seed", C.c_uint64),
-                ("groups", C.c_uint32), ("batch", C.c_uint32)]
+                ("groups", C.c_uint32), ("batch", C.c_uint32), ("window_slots", C.c_uint32)]
 
 
 class _Stats(C.Structure):
@@ -73,11 +73,12 @@ class Config:
     storage: int = 0      # 0 fp32 rows, 1 bf16 rows (NEXT-4, reading D16)
     groups: int = 1       # NEXT-3 two-level ring: groups of parts/groups ranks (1 = one ring)
     batch: int = 128      # update_rule 2 (NEXT-4 shared negatives): samples per mini-batch
+    window_slots: int = 0  # NEXT-2 staged ring: sub-part slots per ring window (0 = all)
 
     def c(self) -> _Config:
         return _Config(self.dim, self.negatives, self.walk_len, self.window, self.walks_per_node,
                        self.episodes, self.subparts, self.parts, self.p, self.q, self.update_rule,
-                       self.storage, self.seed, self.groups, self.batch)
+                       self.storage, self.seed, self.groups, self.batch, self.window_slots)
 
 
 _lib = None

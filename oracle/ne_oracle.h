@@ -41,6 +41,7 @@ typedef struct {
     uint64_t seed;           /* Philox key                                      */
     uint32_t groups;         /* NEXT-3 two-level ring: G groups ("nodes") of P/G ranks; 0 or 1 = one ring */
     uint32_t batch;          /* update_rule 2: samples per mini-batch (B)        */
+    uint32_t window_slots;   /* NEXT-2 staged ring: slots per window (w); 0 = all k */
 } or_config;
 
 typedef struct {

@@ -263,7 +263,9 @@ uint32_t or_plan_vsub2(uint32_t P, uint32_t G, uint32_t k, uint32_t rho, uint32_
  * build the pool (O4-O6), then replay the hierarchical plan:
  *   for round r in 0..P-1, slot t in 0..k-1, context part g in 0..P-1:
  *       train block (vertex sub-part ((g - r) mod P)*k + t, context part g)
- * (or or_plan_vsub2's sub-part with cfg->groups > 1, the two-level ring)
+ * (or or_plan_vsub2's sub-part with cfg->groups > 1, the two-level ring;
+ * with cfg->window_slots = w < k the slots run in windows of w, each window
+ * through all P rounds before the next -- the staged ring's order)
  * Blocks of one (r, t) step touch disjoint rows ("orthogonal vertex
  * usage"), so the order over g is immaterial; reverse_within_step = 1 replays
  * it backwards to let a test check exactly that.  thr/alias come from
@@ -308,6 +310,7 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
                           int reverse_within_step, float *V, float *C, or_stats *stats)
 {
     uint32_t P = cfg->parts, k = cfg->subparts, d = cfg->dim, K = cfg->negatives;
+    uint32_t w = (cfg->window_slots == 0 || cfg->window_slots > k) ? k : cfg->window_slots, t0;
     uint64_t nblocks = (uint64_t)P * k * P, bounds[257], nnz = offsets[n];
     uint64_t *boff = NULL;
     uint32_t *pairs = NULL, negs[256], e;
@@ -331,8 +334,11 @@ int or_train_epoch_tables(const or_config *cfg, uint64_t n, const uint64_t *offs
         if (!pairs) { free(boff); return -1; }
         cnt = or_build_episode(cfg, n, offsets, targets, epoch, e, pairs, cap, boff);
         if (cnt < 0) { free(pairs); free(boff); return -1; }
+        /* windows of w slots (NEXT-2 staged ring, reading D18): all P rounds of
+         * slots [t0, t0 + w) before the next window; w = k is the plain plan */
+        for (t0 = 0; t0 < k; t0 += w)
         for (r = 0; r < P; ++r)
-            for (t = 0; t < k; ++t)
+            for (t = t0; t < t0 + w && t < k; ++t)
                 for (gi = 0; gi < P; ++gi) {
                     uint32_t g = reverse_within_step ? (P - 1 - gi) : gi;
                     uint32_t s = cfg->groups > 1 ? or_plan_vsub2(P, cfg->groups, k, r, t, g)

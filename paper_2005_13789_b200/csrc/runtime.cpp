@@ -64,6 +64,12 @@ int plan_vsub(uint32_t P, uint32_t G, uint32_t k, uint32_t rho, uint32_t t, uint
 
 uint32_t groups_of(const ne_ctx* c) { return c->cfg.groups > 1 ? c->cfg.groups : 1; }
 
+// NEXT-2 staged ring: vertex sub-parts per ring window (w <= k).
+uint32_t stage_window(const ne_ctx* c) {
+    const uint32_t w = c->cfg.stage_window ? c->cfg.stage_window : 2;
+    return std::min(w, c->cfg.subparts);
+}
+
 int dalloc(ne_ctx* c, void** out, size_t bytes) {
     bytes = std::max<size_t>(bytes, 16);
     void* p = nullptr;
@@ -686,6 +692,94 @@ int launch_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, T
     return NE_OK;
 }
 
+// NEXT-2 with the ring (P:142 pipeline stages 5, 3, 4, 2; "ping-pong
+// buffers"; reading D18): this rank's vertex part lives in pinned host memory;
+// its k sub-parts run in windows of w slots.  A window's home sub-parts are
+// prefetched into one set of w device slots (stage 5, copy stream) while the
+// previous window trains; the window then goes around the ring exactly like
+// the in-HBM plan (train set `cur`, send it, receive the next round's
+// sub-parts into set `nxt`, swap), and after the last round its sub-parts are
+// home again and copied back (stage 2, comm stream).  Device memory: 3 w
+// sub-parts instead of 2 k.
+int launch_train_staged_ring(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPending& tp) {
+    const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank, G = groups_of(c);
+    const uint32_t w = stage_window(c);
+    const uint64_t d = c->cfg.dim, esz = elem_bytes(c);
+    if (!c->comm) return ne_fail(c, NE_ESTATE, "world=%u context has no NCCL communicator (layout-only)", P);
+    const ncclDataType_t dt = c->cfg.storage == NE_STORE_BF16 ? ncclBfloat16 : ncclFloat;
+    auto slot = [&](uint32_t set, uint32_t t) { return c->vslot[(size_t)set * w + t]; };
+    const uint32_t nwin = (k + w - 1) / w;
+    uint32_t cur = 0, nxt = 1, pre = 2;
+    std::vector<cudaEvent_t> loaded(w, nullptr), drained(w, nullptr);
+    auto prefetch = [&](uint32_t win, uint32_t set) -> int {  // stage 5: H2D of the window's home sub-parts
+        for (uint32_t t = 0; t < w && win * w + t < k; ++t) {
+            if (drained[t]) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, drained[t], 0));
+            else if (c->stage_pending) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->stage_done, 0));
+            const uint64_t vs = (uint64_t)g * k + win * w + t, sb = c->sub_bounds[vs];
+            NE_CUDA(c, cudaMemcpyAsync(slot(set, t), host_row(c, sb), (c->sub_bounds[vs + 1] - sb) * d * esz,
+                                       cudaMemcpyHostToDevice, c->copy_stream));
+            loaded[t] = next_event(c);
+            NE_CUDA(c, cudaEventRecord(loaded[t], c->copy_stream));
+        }
+        return NE_OK;
+    };
+    NE_TRY(prefetch(0, cur));
+    std::vector<cudaEvent_t> recv(w, nullptr);
+    for (uint32_t win = 0; win < nwin; ++win) {
+        const uint32_t t0 = win * w, wn = std::min(w, k - t0);
+        for (uint32_t t = 0; t < wn; ++t) recv[t] = loaded[t];
+        if (win + 1 < nwin) NE_TRY(prefetch(win + 1, pre));  // overlaps this whole window
+        for (uint32_t r = 0; r < P; ++r) {
+            for (uint32_t t = 0; t < wn; ++t) {
+                const uint32_t vs = (uint32_t)plan_vsub(P, G, k, r, t0 + t, g);
+                float* V = slot(cur, t);
+                cudaEvent_t w0 = next_event(c), w1 = next_event(c);
+                NE_CUDA(c, cudaEventRecord(w0, c->stream));
+                NE_CUDA(c, cudaStreamWaitEvent(c->stream, recv[t], 0));
+                NE_CUDA(c, cudaEventRecord(w1, c->stream));
+                tp.waits.push_back({w0, w1});
+                const ne::SgnsParams sp = sgns_params(c, vs, V, epoch, episode, lr);
+                cudaEvent_t e0 = next_event(c), e1 = next_event(c);
+                NE_CUDA(c, cudaEventRecord(e0, c->stream));
+                NE_CUDA(c, ne::launch_sgns(sp, c->dev, c->stream));
+                NE_CUDA(c, cudaEventRecord(e1, c->stream));
+                if (sp.count) { c->launches += 1; tp.launches += 1; }
+                tp.timed.push_back({e0, e1});
+                tp.samples += sp.count;
+                const uint32_t vs_next = (uint32_t)plan_vsub(P, G, k, r + 1, t0 + t, g);
+                NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, e1, 0));
+                NE_NCCL(c, ncclGroupStart());
+                NE_NCCL(c, ncclSend(V, (c->sub_bounds[vs + 1] - c->sub_bounds[vs]) * d, dt,
+                                    (int)ring_dest(P, G, r, g), c->comm, c->comm_stream));
+                NE_NCCL(c, ncclRecv(slot(nxt, t), (c->sub_bounds[vs_next + 1] - c->sub_bounds[vs_next]) * d, dt,
+                                    (int)ring_src(P, G, r, g), c->comm, c->comm_stream));
+                NE_NCCL(c, ncclGroupEnd());
+                recv[t] = next_event(c);
+                NE_CUDA(c, cudaEventRecord(recv[t], c->comm_stream));
+            }
+            std::swap(cur, nxt);
+        }
+        // home again (set cur): stage 2, D2H on the comm stream after the last receive
+        for (uint32_t t = 0; t < wn; ++t) {
+            const uint64_t vs = (uint64_t)g * k + t0 + t, sb = c->sub_bounds[vs];
+            NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, recv[t], 0));
+            NE_CUDA(c, cudaMemcpyAsync(host_row(c, sb), slot(cur, t), (c->sub_bounds[vs + 1] - sb) * d * esz,
+                                       cudaMemcpyDeviceToHost, c->comm_stream));
+            drained[t] = next_event(c);
+            NE_CUDA(c, cudaEventRecord(drained[t], c->comm_stream));
+        }
+        // next window trains the prefetched set; this window's home set drains
+        // and then takes the prefetch of the window after
+        const uint32_t home = cur;
+        cur = pre;
+        pre = home;
+    }
+    if (!c->stage_done) NE_CUDA(c, cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
+    NE_CUDA(c, cudaEventRecord(c->stage_done, c->comm_stream));
+    c->stage_pending = true;
+    return NE_OK;
+}
+
 // O7 ring: round r, slot t trains block
 // (vsub = ((rank - r) mod P)*k + t, context part rank); the trained sub-part is
 // sent to rank+1 while slot t+1 trains, and the sub-part for round r+1 arrives
@@ -694,6 +788,7 @@ int launch_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, T
 int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPending& tp) {
     NE_TRY(wait_alias(c));
     NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
+    if (c->cfg.staging == NE_STAGE_HOST && c->world > 1) return launch_train_staged_ring(c, epoch, episode, lr, tp);
     if (c->cfg.staging == NE_STAGE_HOST) return launch_train_staged(c, epoch, episode, lr, tp);
     const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank, G = groups_of(c);
     const uint64_t d = c->cfg.dim;
@@ -995,8 +1090,8 @@ int ne_init_dist(ne_ctx* c, int rank, int world, const uint8_t id[128]) {
     NE_TRY(enter(c));
     if (c->loaded) return ne_fail(c, NE_ESTATE, "ne_init_dist must precede ne_load_graph");
     if (world < 1 || rank < 0 || rank >= world) return ne_fail(c, NE_EINVAL, "rank=%d world=%d", rank, world);
-    if (world > 1 && c->cfg.staging == NE_STAGE_HOST)
-        return ne_fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", world);
+    if (world > 1 && c->cfg.staging == NE_STAGE_HOST && c->cfg.transport == NE_TRANSPORT_IPC)
+        return ne_fail(c, NE_EINVAL, "staging=NE_STAGE_HOST with world > 1 runs its ring over NCCL (transport=0)");
     if ((uint64_t)world * c->cfg.subparts > 256 || (uint64_t)world * world * c->cfg.subparts > 4096)
         return ne_fail(c, NE_EINVAL, "world=%d x subparts=%u exceeds the block-id range", world, c->cfg.subparts);
     if (world > 32) return ne_fail(c, NE_EINVAL, "world=%d > 32 (one lane per context part in the pool build)", world);
@@ -1149,9 +1244,12 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     NE_CUDA(c, cudaMemsetAsync(c->d_C, 0, c->c_count * g.dim * esz, c->stream));
     // vertex sub-part slots: the ring needs 2k (ping-pong), one GPU k, host staging 3
     const bool staged = g.staging == NE_STAGE_HOST;
-    if (staged && c->world > 1)
-        return ne_fail(c, NE_EINVAL, "staging=NE_STAGE_HOST needs world == 1 (world=%d)", c->world);
-    const size_t nslots = staged ? std::min<size_t>(3, k) : (c->world > 1 ? 2 * (size_t)k : k);
+    // slots: one GPU k; ring 2k (ping-pong halves); host staging, one GPU: 3
+    // (H2D next / train / D2H last); host staging with a ring: 3 sets of w
+    // (the window trains in one set, receives into another, the third
+    // prefetches the next window / drains the last one)
+    const size_t nslots = staged ? (c->world > 1 ? 3 * (size_t)stage_window(c) : std::min<size_t>(3, k))
+                                 : (c->world > 1 ? 2 * (size_t)k : k);
     if (!reuse || c->vslot.size() != nslots) c->vslot.assign(nslots, nullptr);
     const size_t slot_bytes = std::max<uint64_t>(c->max_sub_rows, 1) * g.dim * esz;
     if (ipc_ring(c) && !staged) {  // one exportable region for the copy-engine ring
@@ -1515,6 +1613,40 @@ int ne_train_samples_local_ring(ne_ctx* const* ctxs, uint32_t world, uint32_t ep
     // rank g; the "send to g+1" is a pointer hand-over of the trained slot.
     std::vector<float*> moved(world);
     const uint32_t G = groups_of(c0);
+    if (c0->cfg.staging == NE_STAGE_HOST) {  // NEXT-2 staged ring, windows of w slots (launch_train_staged_ring)
+        const uint32_t w = stage_window(c0);
+        const uint64_t d = c0->cfg.dim, esz = elem_bytes(c0);
+        for (uint32_t t0 = 0; t0 < k; t0 += w) {
+            const uint32_t wn = std::min(w, k - t0);
+            for (uint32_t g = 0; g < world; ++g)
+                for (uint32_t t = 0; t < wn; ++t) {  // stage 5: home sub-parts to the device
+                    ne_ctx* c = ctxs[g];
+                    const uint64_t vs = (uint64_t)g * k + t0 + t, sb = c->sub_bounds[vs];
+                    NE_CUDA(c0, cudaMemcpyAsync(c->vslot[t], host_row(c, sb), (c->sub_bounds[vs + 1] - sb) * d * esz,
+                                                cudaMemcpyHostToDevice, c0->stream));
+                }
+            for (uint32_t r = 0; r < world; ++r)
+                for (uint32_t t = 0; t < wn; ++t) {
+                    for (uint32_t g = 0; g < world; ++g) {
+                        ne_ctx* c = ctxs[g];
+                        ne::SgnsParams sp = sgns_params(c, (uint32_t)plan_vsub(world, G, k, r, t0 + t, g), c->vslot[t],
+                                                        epoch, episode, lr);
+                        sp.loss = c0->d_loss;
+                        NE_CUDA(c0, ne::launch_sgns(sp, c->dev, c0->stream));
+                        if (stats) { stats->samples += sp.count; if (sp.count) stats->train_launches += 1; }
+                    }
+                    for (uint32_t g = 0; g < world; ++g) moved[ring_dest(world, G, r, g)] = ctxs[g]->vslot[t];
+                    for (uint32_t g = 0; g < world; ++g) ctxs[g]->vslot[t] = moved[g];
+                }
+            for (uint32_t g = 0; g < world; ++g)
+                for (uint32_t t = 0; t < wn; ++t) {  // stage 2: home again, back to the host
+                    ne_ctx* c = ctxs[g];
+                    const uint64_t vs = (uint64_t)g * k + t0 + t, sb = c->sub_bounds[vs];
+                    NE_CUDA(c0, cudaMemcpyAsync(host_row(c, sb), c->vslot[t], (c->sub_bounds[vs + 1] - sb) * d * esz,
+                                                cudaMemcpyDeviceToHost, c0->stream));
+                }
+        }
+    } else
     for (uint32_t r = 0; r < world; ++r)
         for (uint32_t t = 0; t < k; ++t) {
             for (uint32_t g = 0; g < world; ++g) {

@@ -14,10 +14,10 @@ class Engine:
                  nccl_id=None, torch_allocator=False, stream=None, conflict_permille=0,
                  writeback=ne.NE_WB_ATOMIC_DELTA, p=1.0, q=1.0, update_rule=ne.NE_UPDATE_SEQUENTIAL,
                  staging=ne.NE_STAGE_DEVICE, storage=ne.NE_STORE_F32, transport=ne.NE_TRANSPORT_NCCL,
-                 groups=1):
+                 groups=1, stage_window=0):
         self.cfg = ne.ne_config(dim, negatives, walk_len, window, walks_per_node, episodes, subparts,
                                 int(bool(deterministic)), conflict_permille, writeback, p, q, update_rule,
-                                staging, storage, transport, seed, groups)
+                                staging, storage, transport, seed, stage_window, groups)
         self._alloc = ne.torch_allocator() if torch_allocator else (None, None)
         self.ctx = ne.ne_create(self.cfg, device, *self._alloc)
         self.rank, self.world = rank, world

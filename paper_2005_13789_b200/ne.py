@@ -39,7 +39,8 @@ class ne_config(C.Structure):
                 ("subparts", C.c_uint32), ("deterministic", C.c_uint32), ("conflict_permille", C.c_uint32),
                 ("writeback", C.c_uint32), ("p", C.c_float), ("q", C.c_float),
                 ("update_rule", C.c_uint32), ("staging", C.c_uint32), ("storage", C.c_uint32),
-                ("transport", C.c_uint32), ("seed", C.c_uint64), ("groups", C.c_uint32)]
+                ("transport", C.c_uint32), ("seed", C.c_uint64), ("stage_window", C.c_uint32),
+                ("groups", C.c_uint32)]
 
 
 class ne_stats(C.Structure):

@@ -20,6 +20,7 @@ def _ngpus():
     (2, "det", "deepwalk"), (2, "hogwild", "deepwalk"), (4, "det", "deepwalk"), (4, "hogwild", "deepwalk"),
     (2, "det", "node2vec"), (2, "det", "line"), (4, "det", "line"), (2, "det", "bf16"), (4, "det", "bf16"),
     (4, "det", "groups2"), (2, "det", "ipc"), (4, "det", "ipc"), (4, "hogwild", "ipc"),
+    (2, "det", "staged"), (4, "det", "staged"),
 ])
 def test_nccl_ring(world, mode, kind):
     if _ngpus() < world:

@@ -202,7 +202,8 @@ def test_negatives_bit_exact(c1, P):
 # ---------------------------------------------------------------- O10/O11 training
 def _det_epoch(off, tgt, epochs=1, lr=0.025, **kw):
     n = len(off) - 1
-    cfg = ocfg(**{k: v for k, v in kw.items() if k not in ("deterministic", "conflict_permille", "writeback", "staging")})
+    cfg = ocfg(**{k: v for k, v in kw.items() if k not in ("deterministic", "conflict_permille", "writeback", "staging",
+                                                           "stage_window")})
     eng = engine(**kw)
     eng.load_graph(off, tgt)
     V = oracle.init_vertex(n, cfg.dim, 42)
@@ -403,6 +404,33 @@ def test_deterministic_ring_emulation_c1(c1, P, G):
     ns, loss = oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025)
     assert st.samples == ns == total
     assert abs(st.loss_sum - loss) <= 1e-3 * loss
+    for e in engs:
+        a, b = e.part
+        assert np.abs(e.embeddings(0) - V[a:b]).max() <= TOL
+        assert np.abs(e.embeddings(1) - Cm[a:b]).max() <= TOL
+        e.close()
+
+
+@pytest.mark.parametrize("P,w", [(2, 2), (4, 2), (4, 1), (2, 4)])
+def test_staged_ring_emulation_c1(c1, P, w):
+    """NEXT-2 with the ring (reading D18): every rank's vertex part in pinned
+    host memory, its sub-parts going around the ring in windows of w slots
+    (H2D of the window, P rounds with hand-over, D2H) -- P layout-only ranks on
+    one device: within 1e-4 of the oracle's windowed plan."""
+    from paper_2005_13789_b200 import ne
+    off, tgt = c1
+    n = len(off) - 1
+    engs = [engine(rank=g, world=P, staging=1, stage_window=w) for g in range(P)]
+    for e in engs:
+        e.load_graph(off, tgt)
+        e.random_walk(0, 0)
+        e.build_samples(0, 0)
+    st = ne.ne_train_samples_local_ring([e.ctx for e in engs], 0, 0, 0.025)
+    cfg = ocfg(parts=P, window_slots=w)
+    V = oracle.init_vertex(n, 128, 42)
+    Cm = np.zeros_like(V)
+    ns, loss = oracle.train_epoch(cfg, off, tgt, V, Cm, 0, 0.025)
+    assert st.samples == ns
     for e in engs:
         a, b = e.part
         assert np.abs(e.embeddings(0) - V[a:b]).max() <= TOL

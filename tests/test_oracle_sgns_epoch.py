@@ -345,3 +345,35 @@ def test_two_level_epoch_equals_replay(orc):
     assert np.array_equal(V, V2) and np.array_equal(Cm, C2)
     orc.train_epoch(_cfg(orc, parts=P, subparts=k), off, tgt, V3, C3, 1, 0.05)
     assert not np.array_equal(V, V3)
+
+
+def test_windowed_plan_order(orc):
+    """NEXT-2 staged ring (reading D18): with window_slots = w the epoch trains
+    the slots in windows of w, every window through all P rounds before the
+    next; w = k (or 0) is the plain plan, and w < k is the same set of blocks
+    in that order (replay)."""
+    P, k, w = 2, 4, 2
+    off, tgt = synth.rmat_graph(150, 900, 12)
+    V = orc.init_vertex(150, 16, 42)
+    Cm = np.zeros_like(V)
+    ref = [(V.copy(), Cm.copy()) for _ in range(3)]
+    orc.train_epoch(_cfg(orc, parts=P, subparts=k), off, tgt, *ref[0], 0, 0.05)
+    orc.train_epoch(_cfg(orc, parts=P, subparts=k, window_slots=k), off, tgt, *ref[1], 0, 0.05)
+    assert np.array_equal(ref[0][0], ref[1][0]) and np.array_equal(ref[0][1], ref[1][1])
+    cfg = _cfg(orc, parts=P, subparts=k, window_slots=w)
+    orc.train_epoch(cfg, off, tgt, *ref[2], 0, 0.05)
+    assert not np.array_equal(ref[2][0], ref[0][0])
+    thr, al = orc.build_alias_tables(cfg, off)
+    pb = orc.partition_bounds(0, 150, P).astype(np.int64)
+    pairs, boff = orc.build_episode(cfg, off, tgt, 0, 0)
+    V2, C2 = V.copy(), Cm.copy()
+    for t0 in range(0, k, w):
+        for r in range(P):
+            for t in range(t0, t0 + w):
+                for g in range(P):
+                    B = (((g - r) % P) * k + t) * P + g
+                    for p in range(int(boff[B + 1] - boff[B])):
+                        src, dst = pairs[int(boff[B]) + p]
+                        negs = orc.negatives(cfg, thr, al, int(pb[g]), int(pb[g + 1] - pb[g]), 0, 0, B, p)
+                        orc.train_sample(V2, C2, int(src), int(dst), negs, 0.05)
+    assert np.array_equal(ref[2][0], V2) and np.array_equal(ref[2][1], C2)

@@ -24,6 +24,7 @@ def main():
     extra = {"deepwalk": {}, "node2vec": dict(p=0.5, q=2.0), "line": dict(walk_len=0, window=0),
              "groups2": dict(groups=2),  # NEXT-3 two-level ring: two groups of world/2 ranks
              "ipc": dict(transport=ne.NE_TRANSPORT_IPC),  # copy-engine ring over CUDA IPC (+ NCCL pool build)
+             "staged": dict(staging=1, stage_window=2),   # NEXT-2 with the ring: host-staged parts, windows of 2
              # NEXT-4 bf16 rows over the ring, on a perfect matching (rows stored ~1+K times, the
              # element-wise bar of tests/test_gpu_bf16.py)
              "bf16": dict(walk_len=1, window=1, storage=1)}[kind]
@@ -60,7 +61,9 @@ def main():
     if rank == 0:
         base = dict(dim=128, negatives=5, walk_len=40, window=5, walks_per_node=1, episodes=2,
                     subparts=4, parts=world, seed=42)
-        base.update({k: v for k, v in extra.items() if k != "transport"})
+        base.update({k: v for k, v in extra.items() if k not in ("transport", "staging", "stage_window")})
+        if kind == "staged":
+            base["window_slots"] = 2
         cfg = oracle.Config(**base)
         Vr = oracle.init_vertex(n, 128, 42)
         if kind == "bf16":
