@@ -161,6 +161,163 @@ __global__ void __launch_bounds__(T, MINB) sgns_kernel(SgnsParams p) {
     if (sub == 0 && loss != 0.0) atomicAdd(p.loss, loss);
 }
 
+// Shared-memory-staged production kernel (fp32 rows, Alg. 1 sequential rule,
+// atomic-delta write-back, K = 5; knob NE_SGNS_STAGED): the same per-lane
+// arithmetic (sgns_step) as sgns_kernel, but the 2+K rows of the NEXT
+// iteration are copied global -> shared with cp.async (no registers) while the
+// current iteration computes, double-buffered per warp, so every warp keeps a
+// full iteration of row traffic in flight through its compute phase instead of
+// alternating load and compute.  Rows are read from shared memory one step at
+// a time (a repeated context id reads the slot its earlier occurrence was
+// updated in).  Pairs and negatives run two iterations ahead.  Hogwild only:
+// prefetching iteration i+1 before i's write-back is the same staleness
+// concurrent warps already have; the deterministic mode keeps sgns_kernel.
+template <int G, int R, int KT>
+__global__ void __launch_bounds__(256, 2) sgns_staged_kernel(SgnsParams p) {
+    constexpr int S = 32 / G, KM = KT > 0 ? KT : kMaxK, ROWS = 2 + KM, ROWF4 = G * R;
+    const int K = KT > 0 ? KT : (int)p.K;
+    constexpr int BUF = S * ROWS * ROWF4;  // float4 per buffer
+    extern __shared__ float4 smem_rows[];
+    const uint32_t lane = lane_id(), sub = lane % G, h = lane / G;
+    float4* wbuf = smem_rows + (size_t)(threadIdx.x >> 5) * 2 * BUF;
+    const uint64_t stride = (((uint64_t)gridDim.x * blockDim.x) >> 5) * S;
+    const uint32_t q = p.d >> 2;
+    const uint2 key = key_of(p.seed);
+    const uint32_t tagw = tag_word(kTagNeg, p.epoch);
+    double loss = 0.0;
+    auto fetch = [&](uint64_t b, uint2& pr, NegDraw& neg) {
+        pr = (b + h < p.count) ? p.pool[b + h] : make_uint2(0, 0);
+        const uint64_t ps = b + lane / (uint32_t)(K > 0 ? K : 1);
+        if (K > 0 && lane < S * (uint32_t)K && ps < p.count) neg = issue_negative(p, key, tagw, ps, lane % K);
+        else neg = NegDraw{0u, 0u, make_uint2(0u, 0u)};
+    };
+    auto group_id = [&](const uint2& pr, const NegDraw& neg) -> uint32_t {
+        const uint32_t nj = __shfl_sync(0xFFFFFFFFu, finish_negative(p, neg), (h * K + sub + 31) & 31);
+        return sub == 0 ? pr.y : nj;
+    };
+    // rows of the iteration at b (ids: this lane's group id list) into buffer buf
+    auto stage = [&](uint64_t b, const uint2& pr, uint32_t my_id, float4* buf) {
+        const bool act = b + h < p.count;
+#pragma unroll
+        for (int j = 0; j < ROWS; ++j) {
+            if (j >= 2 + K) break;
+            const uint32_t id = j == 0 ? pr.x : __shfl_sync(0xFFFFFFFFu, my_id, h * G + (j - 1));
+            const float* rowp = j == 0 ? p.V + (uint64_t)(id - p.v_begin) * p.d : p.C + (uint64_t)(id - p.c_begin) * p.d;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t e = sub + G * r;
+                if (act && e < q) {
+                    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(buf + (h * ROWS + j) * ROWF4 + e);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
+                                 "l"(reinterpret_cast<const float4*>(rowp) + e)
+                                 : "memory");
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+
+    uint64_t base = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * S;
+    uint2 prA, prB, prC;
+    NegDraw negA, negB, negC;
+    fetch(base, prA, negA);
+    fetch(base + stride, prB, negB);
+    uint32_t idA = group_id(prA, negA);
+    stage(base, prA, idA, wbuf);
+    uint32_t cur = 0;
+    for (; base < p.count; base += stride) {
+        const uint64_t pos = base + h;
+        const bool act = pos < p.count;
+        // the next iteration's rows start moving now; its pairs / negatives were
+        // fetched one iteration ago, the one after it is fetched here
+        const uint32_t idB = group_id(prB, negB);
+        stage(base + stride, prB, idB, wbuf + (cur ^ 1) * BUF);
+        fetch(base + 2 * stride, prC, negC);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncwarp();
+        float4* buf = wbuf + cur * BUF + h * ROWS * ROWF4;
+        uint32_t ids[KM + 1];
+#pragma unroll
+        for (int j = 0; j <= KM; ++j) ids[j] = __shfl_sync(0xFFFFFFFFu, idA, h * G + j);
+        const uint64_t mkey = (act && (int)sub <= K) ? (((uint64_t)h << 33) | idA) : ((1ull << 32) | lane);
+        const bool dup = __any_sync(0xFFFFFFFFu, __popc(__match_any_sync(0xFFFFFFFFu, mkey)) > 1);
+        if (p.capture && act) {
+            uint32_t* capp = p.capture + pos * (2u + (uint32_t)K);
+            if (sub == 0) capp[0] = prA.x;
+            if ((int)sub <= K) capp[1 + sub] = idA;
+        }
+        float4 v[R], v0[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t e = sub + G * r;
+            v[r] = (act && e < q) ? buf[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+            v0[r] = v[r];
+        }
+#pragma unroll
+        for (int j = 0; j <= KM; ++j) {
+            if (j > K) break;
+            int slot = j;  // a repeated id reads the slot its latest earlier occurrence was updated in
+            if (dup) {
+#pragma unroll
+                for (int i2 = 0; i2 < j; ++i2)
+                    if (ids[i2] == ids[j]) slot = i2;
+            }
+            float4 c[R], vo[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t e = sub + G * r;
+                c[r] = (act && e < q) ? buf[(1 + slot) * ROWF4 + e] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float lt;
+            const float a = sgns_step<G, R>(v, c, vo, p.lr, j == 0, lt);
+            if (sub == 0 && act) loss += (double)lt;
+            const uint64_t cr = (uint64_t)(ids[j] - p.c_begin);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint32_t e = sub + G * r;
+                if (act && e < q) {
+                    RowIO<false>::add(p.C, cr, p.d, e, scaled(-a, vo[r]));
+                    if (dup) buf[(1 + slot) * ROWF4 + e] = c[r];
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t e = sub + G * r;
+            if (act && e < q)
+                RowIO<false>::add(p.V, (uint64_t)(prA.x - p.v_begin), p.d, e,
+                                  make_float4(v[r].x - v0[r].x, v[r].y - v0[r].y, v[r].z - v0[r].z, v[r].w - v0[r].w));
+        }
+        __syncwarp();  // every lane is done with this buffer before it is restaged
+        prA = prB;
+        negA = negB;
+        idA = idB;
+        prB = prC;
+        negB = negC;
+        cur ^= 1u;
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (sub == 0 && loss != 0.0) atomicAdd(p.loss, loss);
+}
+
+template <int G, int R, int KT>
+static cudaError_t launch_sgns_staged(const SgnsParams& p, const Device& dev, cudaStream_t s) {
+    constexpr int S = 32 / G, ROWS = 2 + (KT > 0 ? KT : kMaxK), ROWF4 = G * R;
+    constexpr size_t smem = (size_t)(256 / 32) * 2 * S * ROWS * ROWF4 * sizeof(float4);
+    auto kern = sgns_staged_kernel<G, R, KT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t want = std::min<uint64_t>(p.count, std::max<uint64_t>(p.max_warps, 1));
+    const uint64_t warps = std::max<uint64_t>(1, want / S);
+    const uint64_t full = (uint64_t)std::max(1, dev.sm_count - p.reserve_sms) * std::max(per_sm, 1);
+    const uint64_t blocks = std::min<uint64_t>(full, (warps + 7) / 8);
+    kern<<<(unsigned)std::max<uint64_t>(1, blocks), 256, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
 static int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e ? std::atoi(e) : dflt;
@@ -247,6 +404,12 @@ cudaError_t launch_sgns_rows(const SgnsParams& p, const Device& dev, cudaStream_
     // 64 < d <= 96 at K = 5: 8-lane groups x 3 float4, four samples per warp, so
     // a 384-byte row uses every lane (16-lane groups leave a quarter idle)
     if (q > 16 && q <= 24 && p.K == 5) return launch_sgns_k<8, 3, 5, BF>(p, dev, s);
+    if constexpr (!BF) {  // developer knob: the shared-memory-staged kernel (d <= 128, K = 5, Hogwild)
+        const int staged = env_int("NE_SGNS_STAGED", 0);  // read per launch: tests toggle it
+        if (staged && q > 16 && q <= 32 && !p.deterministic && p.atomic_writeback && !p.accumulate &&
+            p.max_warps >= 2)
+            return p.K == 5 ? launch_sgns_staged<16, 2, 5>(p, dev, s) : launch_sgns_staged<16, 2, 0>(p, dev, s);
+    }
     // d <= 128: 16 lanes x 1-2 float4, two samples per warp (measured against
     // 32 lanes x 1 float4, one sample per warp: 1093 vs 1003 M samples/s on C3)
     if (q <= 16) return launch_sgns_r<16, 1, BF>(p, dev, s);

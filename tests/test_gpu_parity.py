@@ -500,9 +500,12 @@ def test_node2vec_requires_sorted_rows():
     eng.close()
 
 
-def test_hogwild_auc_gate_c1():
+@pytest.mark.parametrize("staged", ["0", "1"])
+def test_hogwild_auc_gate_c1(staged, monkeypatch):
     """SURVEY 8(c) gate: production (Hogwild) AUC within 0.01 of the oracle on
-    C1 with 10% held-out edges after 5 epochs (several production runs)."""
+    C1 with 10% held-out edges after 5 epochs (several production runs); also
+    for the shared-memory-staged kernel (NE_SGNS_STAGED=1)."""
+    monkeypatch.setenv("NE_SGNS_STAGED", staged)
     w = synth.CONFIGS["c1"]
     u, v = synth.rmat_edges(w.n, w.m, w.graph_seed)
     off, tgt, test = synth.split_edges(w.n, u, v, 0.1, synth.EVAL_SEED)
@@ -607,13 +610,14 @@ def _matching(n):
     return synth.csr_from_undirected(n, u, u + 1)
 
 
-@pytest.mark.parametrize("dim,vsub", [(128, 1), (96, 2)])
-def test_capture_ids_full_grid_c2(dim, vsub):
+@pytest.mark.parametrize("dim,vsub,staged", [(128, 1, "0"), (96, 2, "0"), (128, 3, "1")])
+def test_capture_ids_full_grid_c2(dim, vsub, staged, monkeypatch):
     """The production kernel at its full grid on C2 (d = 128: 16-lane groups,
     2 samples per warp; d = 96: 8-lane groups, 4 samples per warp) records the
     (src, dst, negatives) every group trained; every position must equal the
     pool and the oracle's negatives -- the lane -> sample -> negative routing
     of all S groups of a warp, checked at every position of the block."""
+    monkeypatch.setenv("NE_SGNS_STAGED", staged)  # "1": the shared-memory-staged kernel
     off, tgt = synth.workload_graph("c2")
     n = len(off) - 1
     eng = engine(dim=dim, deterministic=False)
@@ -656,12 +660,13 @@ def test_capture_ids_layout_ranks_c1():
         eng.close()
 
 
-@pytest.mark.parametrize("dim", [64, 128, 256])
-def test_hogwild_full_grid_conflict_free_elementwise(dim):
+@pytest.mark.parametrize("dim,staged", [(64, "0"), (128, "0"), (256, "0"), (128, "1")])
+def test_hogwild_full_grid_conflict_free_elementwise(dim, staged, monkeypatch):
     """A perfect matching with walk_len = window = 1 and K = 0: every vertex row
     and every context row is touched by exactly one sample, so the production
     (Hogwild, atomic-delta) kernel at its full grid has no conflicts and must
     equal the oracle element by element (fp32 arithmetic vs the fp64 oracle)."""
+    monkeypatch.setenv("NE_SGNS_STAGED", staged)
     n = 1 << 21
     off, tgt = _matching(n)
     kw = dict(dim=dim, negatives=0, walk_len=1, window=1)
