@@ -27,6 +27,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "ne_ctx.h"
@@ -72,13 +74,20 @@ uint32_t* flags_of(const ne_ctx* c, void* region) {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(region) + 2ull * c->cfg.subparts * c->ipc.slot_bytes);
 }
 
+bool ipc_debug() {
+    static const bool on = std::getenv("NE_IPC_DEBUG") != nullptr;
+    return on;
+}
+
 int wait_ge(ne_ctx* c, cudaStream_t s, const uint32_t* flag, uint32_t value) {
+    if (ipc_debug()) std::fprintf(stderr, "[ipc rank %d] wait flag %p >= %u\n", c->rank, (const void*)flag, value);
     const CUresult r = ops().wait((CUstream)s, (CUdeviceptr)flag, value, CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS) return ne_fail(c, NE_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
     return NE_OK;
 }
 
 int write_flag(ne_ctx* c, cudaStream_t s, uint32_t* flag, uint32_t value) {
+    if (ipc_debug()) std::fprintf(stderr, "[ipc rank %d] write flag %p = %u\n", c->rank, (void*)flag, value);
     const CUresult r = ops().write((CUstream)s, (CUdeviceptr)flag, value, CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS) return ne_fail(c, NE_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
     return NE_OK;
@@ -109,7 +118,10 @@ int ipc_alloc_slots(ne_ctx* c, size_t slot_bytes, size_t nslots) {
     c->ipc.region_bytes = bytes;
     c->ipc.slot_bytes = slot_bytes;
     c->ipc.flags = flags_of(c, c->ipc.region);
-    NE_CUDA(c, cudaMemset(c->ipc.flags, 0, 2ull * k * sizeof(uint32_t)));
+    // on the compute stream and waited for: the flags must be zero before any
+    // peer can write them (the handles are exported after the load returns)
+    NE_CUDA(c, cudaMemsetAsync(c->ipc.flags, 0, 2ull * k * sizeof(uint32_t), c->stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->stream));
     c->ipc.pushed.assign(k, 0);
     c->ipc.waited.assign(k, 0);
     c->ipc.started = false;

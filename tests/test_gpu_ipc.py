@@ -18,6 +18,6 @@ def test_ipc_ring(world, mode, groups):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={29700 + world + (mode == 'hogwild') * 10 + groups * 20}",
            os.path.join(ROOT, "tools", "ipc_parity.py"), mode, str(groups)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "IPC " in r.stdout
