@@ -330,6 +330,13 @@ int ne_export_negatives(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint32_t 
 int ne_capture_block(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint32_t vsub, float lr,
                      uint32_t *out, size_t cap_u32, uint64_t *count);
 
+/* NEXT-4 test hook: the shared-negative batch kernel's three tcgen05 tf32
+ * products on the current device, through its shared-memory tiles,
+ * descriptors and TMEM read-back: host row-major V[128][128], N[64][128],
+ * G[128][64] -> S = V N^T [128][64], dV = G N [128][128], dNt = V^T G
+ * [128][64].  Errors: NE_EINVAL, NE_ECUDA. */
+int ne_umma_products(const float *V, const float *N, const float *G, float *S, float *dV, float *dNt);
+
 /* Single-GPU emulation of the P-rank ring for parity tests: ctxs[g] are
  * layout-only contexts (ne_init_dist(ctx, g, world, NULL)) on ONE device, each
  * with the pool of `episode` built.  Runs the same plan as ne_train_samples

@@ -132,6 +132,36 @@ __device__ __forceinline__ float sigmoid_clamped(float x, float& ex) {
     return __fdividef(1.f, 1.f + ex);
 }
 
+// The three products of a batch, issued by one thread (tiles in the layout of
+// tile_off; D = dimension, KP = shared negatives, B = 128 rows):
+//   S[B x KP]    = V N^T   A = V   K-major, B = N K-major      (K = D)
+//   dV[B x D]    = G N     A = G   K-major, B = N MN-major     (K = KP)
+//   dN^T[D x KP] = V^T G   A = V^T MN-major, B = G MN-major    (K = B)
+template <int D, int KP>
+__device__ __forceinline__ void issue_S(uint32_t sV, uint32_t sN, uint32_t t_S) {
+    constexpr uint32_t idesc = idesc_tf32(kBatch, KP, false, false);
+#pragma unroll
+    for (uint32_t ks = 0; ks < D / 8; ++ks)
+        mma_tf32(t_S, umma_desc(sV + ks * 256u, 128u, D * 32u), umma_desc(sN + ks * 256u, 128u, D * 32u), idesc,
+                 ks > 0);
+}
+template <int D, int KP>
+__device__ __forceinline__ void issue_dV(uint32_t sG, uint32_t sN, uint32_t t_dV) {
+    constexpr uint32_t idesc = idesc_tf32(kBatch, D, false, true);
+#pragma unroll
+    for (uint32_t ks = 0; ks < (uint32_t)KP / 8; ++ks)
+        mma_tf32(t_dV, umma_desc(sG + ks * 256u, 128u, KP * 32u), umma_desc(sN + ks * D * 32u, D * 32u, 128u), idesc,
+                 ks > 0);
+}
+template <int D, int KP>
+__device__ __forceinline__ void issue_dNt(uint32_t sV, uint32_t sG, uint32_t t_dNt) {
+    constexpr uint32_t idesc = idesc_tf32(D, KP, true, true);
+#pragma unroll
+    for (uint32_t ks = 0; ks < (uint32_t)kBatch / 8; ++ks)
+        mma_tf32(t_dNt, umma_desc(sV + ks * D * 32u, D * 32u, 128u), umma_desc(sG + ks * KP * 32u, KP * 32u, 128u),
+                 idesc, ks > 0);
+}
+
 }  // namespace
 
 // D: embedding dimension (UMMA M of the dN^T product: 128); KP: shared
@@ -177,9 +207,6 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
     const float lr = p.lr;
     const uint64_t nbatch = (p.count + kBatch - 1) / kBatch;
     const uint32_t i = tid;  // batch row of this thread
-    constexpr uint32_t idesc1 = idesc_tf32(kBatch, KP, false, false);  // S = V N^T
-    constexpr uint32_t idesc2 = idesc_tf32(kBatch, D, false, true);    // dV = G N
-    constexpr uint32_t idesc3 = idesc_tf32(D, KP, true, true);         // dN^T = V^T G
     double loss = 0.0;
     uint32_t phase = 0;
 
@@ -220,15 +247,10 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         fence_async_smem();
         __syncthreads();
-        // ---- MMA1: S = V N^T (K = D, 8 per instruction = 2 chunks = 256 B)
+        // ---- MMA1: S = V N^T
         if (tid == 0) {
             fence_after();
-#pragma unroll
-            for (uint32_t ks = 0; ks < D / 8; ++ks) {
-                const uint64_t a = umma_desc(smem_u32(sV) + ks * 256u, 128u, D * 32u);
-                const uint64_t bb = umma_desc(smem_u32(sN) + ks * 256u, 128u, D * 32u);
-                mma_tf32(t_S, a, bb, idesc1, ks > 0);
-            }
+            issue_S<D, KP>(smem_u32(sV), smem_u32(sN), t_S);
             mma_commit(&bar[0]);
         }
         // ---- positive term of row i (CUDA cores, overlapping MMA1)
@@ -271,21 +293,11 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         fence_async_smem();
         fence_before();
         __syncthreads();
-        // ---- MMA2: dV = G N (K = KP); MMA3: dN^T = V^T G (K = B)
+        // ---- MMA2: dV = G N; MMA3: dN^T = V^T G
         if (tid == 0) {
             fence_after();
-#pragma unroll
-            for (uint32_t ks = 0; ks < (uint32_t)KP / 8; ++ks) {
-                const uint64_t a = umma_desc(smem_u32(sG) + ks * 256u, 128u, KP * 32u);       // G, K-major
-                const uint64_t bb = umma_desc(smem_u32(sN) + ks * D * 32u, D * 32u, 128u);    // N, MN-major
-                mma_tf32(t_dV, a, bb, idesc2, ks > 0);
-            }
-#pragma unroll
-            for (uint32_t ks = 0; ks < (uint32_t)kBatch / 8; ++ks) {
-                const uint64_t a = umma_desc(smem_u32(sV) + ks * D * 32u, D * 32u, 128u);     // V^T, MN-major
-                const uint64_t bb = umma_desc(smem_u32(sG) + ks * KP * 32u, KP * 32u, 128u);  // G, MN-major
-                mma_tf32(t_dNt, a, bb, idesc3, ks > 0);
-            }
+            issue_dV<D, KP>(smem_u32(sG), smem_u32(sN), t_dV);
+            issue_dNt<D, KP>(smem_u32(sV), smem_u32(sG), t_dNt);
             mma_commit(&bar[1]);
         }
         mbar_wait(&bar[1], phase);
@@ -343,6 +355,79 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols) : "memory");
+}
+
+// Test hook (ne_umma_products): the three products above on dense row-major
+// inputs V[128][D], N[KP][D], G[128][KP] through the same tiles, descriptors
+// and TMEM read-back; outputs S[128][KP], dV[128][D], dNt[D][KP] row-major.
+template <int D, int KP>
+__global__ void __launch_bounds__(kBatch, 1) umma_products_kernel(const float* __restrict__ V,
+                                                                  const float* __restrict__ N,
+                                                                  const float* __restrict__ G, float* __restrict__ S,
+                                                                  float* __restrict__ dV, float* __restrict__ dNt) {
+    constexpr uint32_t kTileV = kBatch * D * 4, kTileN = KP * D * 4, kTileG = kBatch * KP * 4;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char *sV = smem, *sN = sV + kTileV, *sG = sN + kTileN;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sG + kTileG);
+    uint32_t* tmem_base = reinterpret_cast<uint32_t*>(bar + 2);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_base)),
+                     "n"(256) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (uint32_t r = 0; r < kBatch; ++r)
+        for (uint32_t c = tid; c < D / 4; c += kBatch)
+            *reinterpret_cast<float4*>(sV + tile_off(r, c, D)) = reinterpret_cast<const float4*>(V + r * D)[c];
+    for (uint32_t r = 0; r < (uint32_t)KP; ++r)
+        for (uint32_t c = tid; c < D / 4; c += kBatch)
+            *reinterpret_cast<float4*>(sN + tile_off(r, c, D)) = reinterpret_cast<const float4*>(N + r * D)[c];
+    for (uint32_t r = 0; r < kBatch; ++r)
+        for (uint32_t c = tid; c < KP / 4; c += kBatch)
+            *reinterpret_cast<float4*>(sG + tile_off(r, c, KP)) = reinterpret_cast<const float4*>(G + r * KP)[c];
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_base, t_S = tmem, t_dV = tmem + KP, t_dNt = tmem + KP + D;
+    if (tid == 0) {
+        issue_S<D, KP>(smem_u32(sV), smem_u32(sN), t_S);
+        issue_dV<D, KP>(smem_u32(sG), smem_u32(sN), t_dV);
+        issue_dNt<D, KP>(smem_u32(sV), smem_u32(sG), t_dNt);
+        mma_commit(&bar[0]);
+    }
+    mbar_wait(&bar[0], 0);
+    fence_after();
+    const uint32_t lane_base = (warp * 32u) << 16;
+    float v[32];
+    for (uint32_t j0 = 0; j0 < (uint32_t)KP; j0 += 32) {
+        tmem_ld32(t_S + lane_base + j0, v);
+        for (uint32_t e = 0; e < 32; ++e) S[tid * KP + j0 + e] = v[e];
+        tmem_ld32(t_dNt + lane_base + j0, v);
+        for (uint32_t e = 0; e < 32; ++e) dNt[tid * KP + j0 + e] = v[e];
+    }
+    for (uint32_t d0 = 0; d0 < (uint32_t)D; d0 += 32) {
+        tmem_ld32(t_dV + lane_base + d0, v);
+        for (uint32_t e = 0; e < 32; ++e) dV[tid * D + d0 + e] = v[e];
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(256) : "memory");
+}
+
+cudaError_t launch_umma_products(const float* V, const float* N, const float* G, float* S, float* dV, float* dNt,
+                                 cudaStream_t s) {
+    constexpr size_t smem = 128ull * 128 * 4 + 64ull * 128 * 4 + 128ull * 64 * 4 + 64;
+    auto kern = umma_products_kernel<128, 64>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<1, kBatch, smem, s>>>(V, N, G, S, dV, dNt);
+    return cudaGetLastError();
 }
 
 template <int D, int KP>

@@ -149,6 +149,11 @@ cudaError_t launch_sgns_bf16(const SgnsParams& p, const Device& dev, cudaStream_
 // NEXT-4 shared-negative mini-batch rule (p.accumulate == 2; kernels_sgns_batch.cu):
 // batches of 128 samples share p.K negatives; tcgen05 tf32 products.  d == 128.
 cudaError_t launch_sgns_batch(const SgnsParams& p, const Device& dev, cudaStream_t s);
+// Test hook: the batch kernel's three tcgen05 products (d = 128, K' = 64) on dense
+// row-major device inputs V[128][128], N[64][128], G[128][64] ->
+// S = V N^T [128][64], dV = G N [128][128], dNt = V^T G [128][64].
+cudaError_t launch_umma_products(const float* V, const float* N, const float* G, float* S, float* dV, float* dNt,
+                                 cudaStream_t s);
 cudaError_t launch_export_negatives(const SgnsParams& p, uint64_t pos_begin, uint64_t count,
                                     uint32_t* out, const Device& dev, cudaStream_t s);
 

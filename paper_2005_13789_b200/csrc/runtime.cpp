@@ -1591,6 +1591,26 @@ int ne_capture_block(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vsub,
     return NE_OK;
 }
 
+int ne_umma_products(const float* V, const float* N, const float* G, float* S, float* dV, float* dNt) {
+    if (!V || !N || !G || !S || !dV || !dNt) return NE_EINVAL;
+    float* d = nullptr;
+    const size_t nV = 128 * 128, nN = 64 * 128, nG = 128 * 64, nS = 128 * 64, ndV = 128 * 128, ndN = 128 * 64;
+    if (cudaMalloc(&d, (nV + nN + nG + nS + ndV + ndN) * sizeof(float)) != cudaSuccess) return NE_ECUDA;
+    float *dV_in = d, *dN_in = dV_in + nV, *dG_in = dN_in + nN, *dS = dG_in + nG, *ddV = dS + nS, *ddN = ddV + ndV;
+    int rc = NE_OK;
+    if (cudaMemcpy(dV_in, V, nV * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(dN_in, N, nN * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(dG_in, G, nG * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        ne::launch_umma_products(dV_in, dN_in, dG_in, dS, ddV, ddN, 0) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(S, dS, nS * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(dV, ddV, ndV * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(dNt, ddN, ndN * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+        rc = NE_ECUDA;
+    cudaGetLastError();
+    cudaFree(d);
+    return rc;
+}
+
 int ne_train_samples_local_ring(ne_ctx* const* ctxs, uint32_t world, uint32_t epoch,
                                 uint32_t episode, float lr, ne_stats* stats) {
     if (!ctxs || world == 0) return NE_EINVAL;

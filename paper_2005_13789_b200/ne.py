@@ -80,6 +80,7 @@ _sig = {
     "ne_ipc_blob_size": (C.c_size_t, []),
     "ne_ipc_export": (C.c_int, [_P, _P, C.c_size_t]),
     "ne_ipc_connect": (C.c_int, [_P, _P, C.c_size_t]),
+    "ne_umma_products": (C.c_int, [_P] * 6),
     "ne_train_samples_local_ring": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
                                              C.POINTER(ne_stats)]),
     "ne_plan_vsub": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
@@ -249,6 +250,17 @@ def ne_ipc_connect(ctx, blobs: list[bytes]) -> None:
     assert all(len(b) == n for b in blobs)
     buf = (C.c_uint8 * (n * len(blobs))).from_buffer_copy(b"".join(blobs))
     _check(ctx, _lib.ne_ipc_connect(ctx, buf, n))
+
+
+def ne_umma_products(V, N, G):
+    """Test hook: the tcgen05 products of the batch kernel; returns (S, dV, dNt)."""
+    V, N, G = (np.ascontiguousarray(x, np.float32) for x in (V, N, G))
+    assert V.shape == (128, 128) and N.shape == (64, 128) and G.shape == (128, 64)
+    S, dV, dNt = np.zeros((128, 64), np.float32), np.zeros((128, 128), np.float32), np.zeros((128, 64), np.float32)
+    rc = _lib.ne_umma_products(_ptr(V), _ptr(N), _ptr(G), _ptr(S), _ptr(dV), _ptr(dNt))
+    if rc != NE_OK:
+        raise NEError(rc, "ne_umma_products failed")
+    return S, dV, dNt
 
 
 def ne_train_samples_local_ring(ctxs, epoch: int, episode: int, lr: float) -> ne_stats:

@@ -103,3 +103,22 @@ def test_batch_rule_rejects_unsupported_shapes():
     for kw in (dict(dim=96), dict(negatives=5), dict(negatives=128)):
         with pytest.raises(ne.NEError, match="update_rule=2"):
             _engine(**kw)
+
+
+def test_umma_products_match_numpy():
+    """The batch kernel's three tcgen05 tf32 products (tiles, descriptors, TMEM
+    read-back) against fp64 numpy products of the same inputs: tf32 keeps 10
+    mantissa bits of each factor, so |error| <= 2^-10 * sum |a_k b_k| bounds
+    each entry."""
+    from paper_2005_13789_b200 import ne
+    rng = np.random.default_rng(3)
+    V = rng.normal(0, 1, (128, 128)).astype(np.float32)
+    N = rng.normal(0, 1, (64, 128)).astype(np.float32)
+    G = rng.normal(0, 1, (128, 64)).astype(np.float32)
+    S, dV, dNt = ne.ne_umma_products(V, N, G)
+    V64, N64, G64 = V.astype(np.float64), N.astype(np.float64), G.astype(np.float64)
+    for got, ref, bound in ((S, V64 @ N64.T, np.abs(V64) @ np.abs(N64.T)),
+                            (dV, G64 @ N64, np.abs(G64) @ np.abs(N64)),
+                            (dNt, V64.T @ G64, np.abs(V64.T) @ np.abs(G64))):
+        err = np.abs(got - ref)
+        assert (err <= 2.0 ** -10 * bound + 1e-5).all(), float((err / (bound + 1e-30)).max())
