@@ -59,14 +59,16 @@ def test_batch_rule_deterministic_matches_oracle(kp, epochs):
 
 def test_batch_rule_ragged_and_tiny_blocks():
     """Blocks smaller than one batch and ragged last batches (padding rows)."""
+    # (a small lr: on a 300-node graph a batch sums the gradients of many
+    # repeated hub rows, and lr = 0.05 makes the exact rule itself diverge)
     off, tgt = synth.rmat_graph(300, 1200, 22)
     n = len(off) - 1
     eng = _engine(subparts=3, walk_len=4, window=2)
     eng.load_graph(off, tgt)
-    st = eng.train_epoch(0, 0.05)
+    st = eng.train_epoch(0, 0.005)
     V = oracle.init_vertex(n, 128, 42)
     Cm = np.zeros_like(V)
-    ns, _ = oracle.train_epoch(_ocfg(subparts=3, walk_len=4, window=2), off, tgt, V, Cm, 0, 0.05)
+    ns, _ = oracle.train_epoch(_ocfg(subparts=3, walk_len=4, window=2), off, tgt, V, Cm, 0, 0.005)
     assert st["samples"] == ns and ns % 128 != 0
     assert np.abs(eng.embeddings(0) - V).max() <= TOL_ABS
     assert np.abs(eng.embeddings(1) - Cm).max() <= TOL_ABS
