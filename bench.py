@@ -236,6 +236,9 @@ def main():
     ap.add_argument("--rule", default="sequential", choices=["sequential", "accumulated", "batch"],
                     help="update rule: Alg. 1 sequential (the headline), accumulated (word2vec), or batch "
                          "(NEXT-4 shared negatives: 128-sample batches share 64 negatives, tcgen05 tf32)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="ring transport at N > 1: NCCL send/recv kernels, or copy-engine pushes over CUDA IPC")
+    ap.add_argument("--groups", type=int, default=1, help="NEXT-3 two-level ring: groups of N/groups ranks")
     ap.add_argument("--storage", default="f32", choices=["f32", "bf16"],
                     help="row storage: f32 (the paper's, the headline) or bf16 (NEXT-4 option, reading D16)")
     args = ap.parse_args()
@@ -277,10 +280,16 @@ def main():
     eng = Engine(dim=w.dim, negatives=negatives, walk_len=w.walk_len, window=w.window,
                  walks_per_node=1, episodes=episodes, subparts=args.subparts, deterministic=False, seed=42,
                  update_rule=rule, staging=ne.NE_STAGE_HOST if args.staging == "host" else ne.NE_STAGE_DEVICE,
+                 transport=ne.NE_TRANSPORT_IPC if args.transport == "ipc" else ne.NE_TRANSPORT_NCCL, groups=args.groups,
                  p=w.p, q=w.q, storage=ne.NE_STORE_BF16 if args.storage == "bf16" else ne.NE_STORE_F32,
                  device=local, rank=rank, world=world, nccl_id=nccl_id, torch_allocator=True,
                  stream=stream.cuda_stream)
-    eng.load_graph(off, tgt)
+    def all_gather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    eng.load_graph(off, tgt, all_gather=all_gather if world > 1 else None)
 
     def barrier():
         torch.cuda.synchronize()
@@ -392,7 +401,9 @@ def main():
                        "update_rule": args.rule + (" (K'=64 negatives shared per 128-sample batch)"
                                                    if args.rule == "batch" else ""),
                        "staging": args.staging,
-                       "mode": "hogwild", "parallelism": f"2D ring x{world}",
+                       "mode": "hogwild",
+                       "parallelism": f"2D ring x{world}" + (f" in {args.groups} groups" if args.groups > 1 else "")
+                                      + (" (copy-engine IPC ring)" if args.transport == "ipc" and world > 1 else ""),
                        "l2": "inputs larger than L2 (embeddings %.2f GB vs 126 MB L2)" % (2 * n * w.dim * esz / 1e9),
                        "graph_generator": "numpy Philox (host)" if w.m <= 200_000_000 else "torch CUDA generator"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
