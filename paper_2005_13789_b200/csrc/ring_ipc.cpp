@@ -138,7 +138,6 @@ int ipc_reset_on_load(ne_ctx* c) {
 }
 
 int ipc_wait_arrival(ne_ctx* c, uint32_t t) {
-    if (!c->ipc.started) return NE_OK;
     return wait_ge(c, c->stream, c->ipc.flags + t, ++c->ipc.waited[t]);
 }
 

@@ -793,6 +793,7 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
     const uint32_t P = (uint32_t)c->world, k = c->cfg.subparts, g = (uint32_t)c->rank, G = groups_of(c);
     const uint64_t d = c->cfg.dim;
     const bool ipc = ipc_ring(c);
+    const bool ipc_resumed = ipc && c->ipc.started;  // arrivals owed from an earlier call (not this one's pushes)
     if (P > 1 && !c->comm && !ipc)
         return ne_fail(c, NE_ESTATE, "world=%u context has no NCCL communicator (layout-only)", P);
     std::vector<cudaEvent_t> recv(k, nullptr);
@@ -801,7 +802,7 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
         for (uint32_t t = 0; t < k; ++t) {
             const uint32_t vs = (uint32_t)plan_vsub(P, G, k, r, t, g);
             float* V = c->vslot[c->cur * k + t];
-            if (ipc && (r > 0 || c->ipc.started)) {  // the sub-part of this slot has landed
+            if (ipc && (r > 0 || ipc_resumed)) {  // the sub-part of this slot has landed
                 cudaEvent_t w0 = next_event(c), w1 = next_event(c);
                 NE_CUDA(c, cudaEventRecord(w0, c->stream));
                 NE_TRY(ipc_wait_arrival(c, t));
