@@ -33,6 +33,7 @@
 // transposed: MMA1 reads V and N K-major, MMA2 reads G K-major and N MN-major,
 // MMA3 reads V and G MN-major.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ne_device.cuh"
 #include "ne_internal.h"
@@ -57,6 +58,17 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes
     d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
     d |= (uint64_t)1 << 46;  // version = 1 (sm_100)
     return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE
+}
+
+// MN-major operand descriptor: kg = byte stride between groups of 8 K values,
+// mg = byte stride between groups of 4 MN elements (16 B).  g_mn_variant
+// (diagnostics only, set by ne_umma_products) selects alternative encodings.
+__device__ int g_mn_variant = 0;
+__device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t kg, uint32_t mg) {
+    const int v = g_mn_variant;
+    uint64_t d = (v & 1) ? umma_desc(saddr, mg, kg) : umma_desc(saddr, kg, mg);
+    if (v & 2) d |= (uint64_t)1 << 52;  // lbo mode
+    return d;
 }
 
 // Instruction descriptor of kind::tf32: D fp32, A/B tf32, M x N, majors.
@@ -150,7 +162,7 @@ __device__ __forceinline__ void issue_dV(uint32_t sG, uint32_t sN, uint32_t t_dV
     constexpr uint32_t idesc = idesc_tf32(kBatch, D, false, true);
 #pragma unroll
     for (uint32_t ks = 0; ks < (uint32_t)KP / 8; ++ks)
-        mma_tf32(t_dV, umma_desc(sG + ks * 256u, 128u, KP * 32u), umma_desc(sN + ks * D * 32u, D * 32u, 128u), idesc,
+        mma_tf32(t_dV, umma_desc(sG + ks * 256u, 128u, KP * 32u), mn_desc(sN + ks * D * 32u, D * 32u, 128u), idesc,
                  ks > 0);
 }
 template <int D, int KP>
@@ -158,7 +170,7 @@ __device__ __forceinline__ void issue_dNt(uint32_t sV, uint32_t sG, uint32_t t_d
     constexpr uint32_t idesc = idesc_tf32(D, KP, true, true);
 #pragma unroll
     for (uint32_t ks = 0; ks < (uint32_t)kBatch / 8; ++ks)
-        mma_tf32(t_dNt, umma_desc(sV + ks * D * 32u, D * 32u, 128u), umma_desc(sG + ks * KP * 32u, KP * 32u, 128u),
+        mma_tf32(t_dNt, mn_desc(sV + ks * D * 32u, D * 32u, 128u), mn_desc(sG + ks * KP * 32u, KP * 32u, 128u),
                  idesc, ks > 0);
 }
 
@@ -422,6 +434,10 @@ __global__ void __launch_bounds__(kBatch, 1) umma_products_kernel(const float* _
 
 cudaError_t launch_umma_products(const float* V, const float* N, const float* G, float* S, float* dV, float* dNt,
                                  cudaStream_t s) {
+    if (const char* e = std::getenv("NE_UMMA_VARIANT")) {  // diagnostics
+        const int v = std::atoi(e);
+        cudaMemcpyToSymbol(g_mn_variant, &v, sizeof v);
+    }
     constexpr size_t smem = 128ull * 128 * 4 + 64ull * 128 * 4 + 128ull * 64 * 4 + 64;
     auto kern = umma_products_kernel<128, 64>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

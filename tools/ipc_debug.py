@@ -28,8 +28,9 @@ def all_gather(b):
 
 
 off, tgt = synth.rmat_graph(500, 3000, 11)
+groups = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 eng = Engine(dim=32, walk_len=6, window=2, episodes=1, subparts=2, deterministic=True, device=dev, rank=rank,
-             world=world, nccl_id=None, transport=ne.NE_TRANSPORT_IPC)
+             world=world, nccl_id=None, transport=ne.NE_TRANSPORT_IPC, groups=groups)
 log("created")
 eng.load_graph(off, tgt, all_gather=all_gather)
 log("loaded + connected")
