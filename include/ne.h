@@ -337,6 +337,15 @@ int ne_capture_block(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint32_t vsu
  * [128][64].  Errors: NE_EINVAL, NE_ECUDA. */
 int ne_umma_products(const float *V, const float *N, const float *G, float *S, float *dV, float *dNt);
 
+/* Diagnostics hook: one tcgen05 tf32 product D[128][N] from raw shared-memory
+ * images of A and B (img_bytes each, <= 64 KB), shared-memory descriptors
+ * (lbo, sbo in bytes; a_hi / b_hi OR-ed into the upper descriptor bits, e.g.
+ * the layout type), start addresses advancing a_step / b_step bytes over
+ * `ksteps` instructions, and instruction descriptor idesc. */
+int ne_umma_raw(const void *a_img, const void *b_img, uint32_t img_bytes, uint64_t a_hi, uint64_t b_hi,
+                uint32_t a_lbo, uint32_t a_sbo, uint32_t b_lbo, uint32_t b_sbo, uint32_t a_step, uint32_t b_step,
+                uint32_t ksteps, uint32_t idesc, uint32_t N, float *D);
+
 /* Single-GPU emulation of the P-rank ring for parity tests: ctxs[g] are
  * layout-only contexts (ne_init_dist(ctx, g, world, NULL)) on ONE device, each
  * with the pool of `episode` built.  Runs the same plan as ne_train_samples

@@ -432,6 +432,74 @@ __global__ void __launch_bounds__(kBatch, 1) umma_products_kernel(const float* _
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(256) : "memory");
 }
 
+// Diagnostics hook (ne_umma_raw): one product D[M][N] (M = 128) from raw
+// shared-memory images of A and B (each up to 64 KB, copied verbatim),
+// descriptors built from (lbo, sbo, layout type) with start advancing by
+// a_step / b_step bytes per instruction, `ksteps` instructions, a given
+// instruction descriptor.
+__global__ void __launch_bounds__(kBatch, 1) umma_raw_kernel(const uint4* __restrict__ a_img,
+                                                             const uint4* __restrict__ b_img, uint32_t img_u4,
+                                                             uint64_t a_hi, uint64_t b_hi, uint32_t a_lbo, uint32_t a_sbo,
+                                                             uint32_t b_lbo, uint32_t b_sbo, uint32_t a_step,
+                                                             uint32_t b_step, uint32_t ksteps, uint32_t idesc,
+                                                             uint32_t N, float* __restrict__ D) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint4* sA = reinterpret_cast<uint4*>(smem);
+    uint4* sB = sA + img_u4;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + img_u4);
+    uint32_t* tmem_base = reinterpret_cast<uint32_t*>(bar + 2);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_base)),
+                     "n"(256) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (uint32_t i = tid; i < img_u4; i += kBatch) {
+        sA[i] = a_img[i];
+        sB[i] = b_img[i];
+    }
+    fence_async_smem();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_base;
+    if (tid == 0) {
+        for (uint32_t ks = 0; ks < ksteps; ++ks) {
+            const uint64_t a = umma_desc(smem_u32(sA) + ks * a_step, a_lbo, a_sbo) | a_hi;
+            const uint64_t b = umma_desc(smem_u32(sB) + ks * b_step, b_lbo, b_sbo) | b_hi;
+            mma_tf32(tmem, a, b, idesc, ks > 0);
+        }
+        mma_commit(&bar[0]);
+    }
+    mbar_wait(&bar[0], 0);
+    fence_after();
+    float v[32];
+    for (uint32_t j0 = 0; j0 < N; j0 += 32) {
+        tmem_ld32(tmem + ((warp * 32u) << 16) + j0, v);
+        for (uint32_t e = 0; e < 32 && j0 + e < N; ++e) D[tid * N + j0 + e] = v[e];
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(256) : "memory");
+}
+
+cudaError_t launch_umma_raw(const void* a_img, const void* b_img, uint32_t img_bytes, uint64_t a_hi, uint64_t b_hi,
+                            uint32_t a_lbo, uint32_t a_sbo, uint32_t b_lbo, uint32_t b_sbo, uint32_t a_step,
+                            uint32_t b_step, uint32_t ksteps, uint32_t idesc, uint32_t N, float* D, cudaStream_t s) {
+    const size_t smem = 2ull * img_bytes + 64;
+    cudaError_t e = cudaFuncSetAttribute(umma_raw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    umma_raw_kernel<<<1, kBatch, smem, s>>>(static_cast<const uint4*>(a_img), static_cast<const uint4*>(b_img),
+                                             img_bytes / 16, a_hi, b_hi, a_lbo, a_sbo, b_lbo, b_sbo, a_step, b_step,
+                                             ksteps, idesc, N, D);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_umma_products(const float* V, const float* N, const float* G, float* S, float* dV, float* dNt,
                                  cudaStream_t s) {
     if (const char* e = std::getenv("NE_UMMA_VARIANT")) {  // diagnostics

@@ -1612,6 +1612,26 @@ int ne_umma_products(const float* V, const float* N, const float* G, float* S, f
     return rc;
 }
 
+int ne_umma_raw(const void* a_img, const void* b_img, uint32_t img_bytes, uint64_t a_hi, uint64_t b_hi,
+                uint32_t a_lbo, uint32_t a_sbo, uint32_t b_lbo, uint32_t b_sbo, uint32_t a_step, uint32_t b_step,
+                uint32_t ksteps, uint32_t idesc, uint32_t N, float* D) {
+    void* d = nullptr;
+    const size_t out = 128ull * N * sizeof(float);
+    if (cudaMalloc(&d, 2ull * img_bytes + out) != cudaSuccess) return NE_ECUDA;
+    char* base = static_cast<char*>(d);
+    int rc = NE_OK;
+    if (cudaMemcpy(base, a_img, img_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(base + img_bytes, b_img, img_bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        ne::launch_umma_raw(base, base + img_bytes, img_bytes, a_hi, b_hi, a_lbo, a_sbo, b_lbo, b_sbo, a_step, b_step,
+                            ksteps, idesc, N, reinterpret_cast<float*>(base + 2ull * img_bytes), 0) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess ||
+        cudaMemcpy(D, base + 2ull * img_bytes, out, cudaMemcpyDeviceToHost) != cudaSuccess)
+        rc = NE_ECUDA;
+    cudaGetLastError();
+    cudaFree(d);
+    return rc;
+}
+
 int ne_train_samples_local_ring(ne_ctx* const* ctxs, uint32_t world, uint32_t epoch,
                                 uint32_t episode, float lr, ne_stats* stats) {
     if (!ctxs || world == 0) return NE_EINVAL;

@@ -81,6 +81,7 @@ _sig = {
     "ne_ipc_export": (C.c_int, [_P, _P, C.c_size_t]),
     "ne_ipc_connect": (C.c_int, [_P, _P, C.c_size_t]),
     "ne_umma_products": (C.c_int, [_P] * 6),
+    "ne_umma_raw": (C.c_int, [_P, _P, C.c_uint32, C.c_uint64, C.c_uint64] + [C.c_uint32] * 9 + [_P]),
     "ne_train_samples_local_ring": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_float,
                                              C.POINTER(ne_stats)]),
     "ne_plan_vsub": (C.c_int, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
@@ -261,6 +262,19 @@ def ne_umma_products(V, N, G):
     if rc != NE_OK:
         raise NEError(rc, "ne_umma_products failed")
     return S, dV, dNt
+
+
+def ne_umma_raw(a_img: bytes, b_img: bytes, a_hi: int, b_hi: int, a_lbo: int, a_sbo: int, b_lbo: int, b_sbo: int,
+                a_step: int, b_step: int, ksteps: int, idesc: int, N: int) -> np.ndarray:
+    """Diagnostics hook: one tcgen05 tf32 product from raw smem images."""
+    assert len(a_img) == len(b_img) and len(a_img) % 16 == 0
+    D = np.zeros((128, N), np.float32)
+    ab, bb = (C.c_char * len(a_img)).from_buffer_copy(a_img), (C.c_char * len(b_img)).from_buffer_copy(b_img)
+    rc = _lib.ne_umma_raw(C.cast(ab, _P), C.cast(bb, _P), len(a_img), a_hi, b_hi, a_lbo, a_sbo, b_lbo, b_sbo, a_step,
+                          b_step, ksteps, idesc, N, _ptr(D))
+    if rc != NE_OK:
+        raise NEError(rc, "ne_umma_raw failed")
+    return D
 
 
 def ne_train_samples_local_ring(ctxs, epoch: int, episode: int, lr: float) -> ne_stats:
