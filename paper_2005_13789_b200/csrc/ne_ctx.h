@@ -119,11 +119,11 @@ struct ne_ctx {
     struct Ipc {
         void* region = nullptr;          // this rank's 2k vertex slots + flags, one exportable cudaMalloc
         size_t region_bytes = 0, slot_bytes = 0;
-        uint32_t* flags = nullptr;       // arrived[k] (written by rank - 1), credit[k] (written by rank + 1)
+        uint32_t* flags = nullptr;       // arrived[2][k], credit[2][k] (per hop kind; ring_ipc.cpp)
         std::vector<void*> peer;         // regions of the ranks this one pushes to / credits, opened handles
         bool connected = false;
         bool started = false;            // a ring call ran since the last load (arrivals to wait for)
-        std::vector<uint32_t> pushed, waited;  // per slot t: pushes issued / arrivals awaited (monotonic)
+        std::vector<uint32_t> pushed[2], waited[2];  // per hop kind and slot: pushes issued / arrivals awaited
     } ipc;
 };
 
@@ -146,10 +146,16 @@ inline uint32_t ring_src(uint32_t P, uint32_t G, uint32_t rho, uint32_t g) {
 bool ipc_ring(const ne_ctx* c);                      // world > 1 and transport == NE_TRANSPORT_IPC
 int ipc_alloc_slots(ne_ctx* c, size_t slot_bytes, size_t nslots);  // the 2k vertex slots, exportable
 int ipc_reset_on_load(ne_ctx* c);                    // home sub-parts re-initialised: no arrivals owed
-int ipc_wait_arrival(ne_ctx* c, uint32_t t);         // compute stream waits for the sub-part of slot t
-// push slot t's sub-part into rank `dest`; `credit_to` = the rank that pushes into this one next round
-int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after, uint32_t dest,
-             uint32_t credit_to);
+// hop kind after global round rho: 0 = along the group's ring, 1 = to the next group
+inline uint32_t ring_kind(uint32_t P, uint32_t G, uint32_t rho) {
+    const uint32_t L = P / G;
+    return (rho % P) % L + 1 < L ? 0u : 1u;
+}
+int ipc_wait_arrival(ne_ctx* c, uint32_t t, uint32_t kind);  // compute stream waits for slot t's sub-part
+// push slot t's sub-part into rank `dest` (a hop of `kind`); `credit_to` = the
+// rank that pushes into this one next round, with a hop of `next_kind`
+int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after, uint32_t kind, uint32_t dest,
+             uint32_t credit_to, uint32_t next_kind);
 int ipc_drain(ne_ctx* c, bool host_sync);            // every push into / out of this rank has landed
 void ipc_release(ne_ctx* c);
 

@@ -10,20 +10,22 @@
 // After training (round rho, slot t) rank g pushes the sub-part with one
 // cudaMemcpyAsync on its comm stream straight into the other half of slot t of
 // D = ring_dest(rho) -- a copy-engine transfer over NVLink between GPUs (a
-// plain device copy when two processes share a GPU), no SM involved.  Every
-// rank pushes every slot once per round, so push i of slot t is global round
-// i - 1 on every rank, and ordering uses these monotonic per-slot counters in
-// the flag words, waited on and written by the GPU front end
-// (cuStreamWaitValue32 / cuStreamWriteValue32, no kernel, no host round trip):
-//   * push i first waits credit[t] >= i - 1 at g: D's own push i-1 of slot t
-//     -- the sub-part that occupied the target half -- has left;
-//   * after the copy, g writes arrived[t] = i at D and credit[t] = i at the
-//     rank that pushes into g in the next round (g's push i freed the half
-//     that push lands in);
+// plain device copy when two processes share a GPU), no SM involved.
+// Ordering uses monotonic counters in flag words, waited on and written by the
+// GPU front end (cuStreamWaitValue32 / cuStreamWriteValue32: no kernel, no
+// host round trip).  A hop is of kind 0 (along the group's ring) or 1 (to the
+// next group, NEXT-3; with one group, the last round's hop); every rank makes
+// the same hop kind in the same round, so per-kind, per-slot push counts agree
+// on all ranks, and every flag word has exactly one writer (its value never
+// goes down -- a flag shared by two writers could be overwritten with an older
+// count):
+//   * push c of kind k first waits credit[k][t] >= c (D's previous push --
+//     the sub-part that occupied the target half -- has left), except the very
+//     first push after the ring was set up;
+//   * after the copy g writes arrived[k][t] = c at D, and credit[k'][t] =
+//     (its next kind-k' push index) at the rank that pushes into g next round;
 //   * before training slot t in every round but the first after a load, g
-//     waits arrived[t] >= (its next expected arrival).
-// The counters never reset while the region lives, so a rank can never clear
-// a flag a fast peer has already advanced.
+//     waits arrived[k][t] >= (its next expected kind-k arrival).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -73,6 +75,9 @@ constexpr uint32_t kMagic = 0x4E455250u;  // "NERP"
 uint32_t* flags_of(const ne_ctx* c, void* region) {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(region) + 2ull * c->cfg.subparts * c->ipc.slot_bytes);
 }
+// flag words: arrived[kind][t] at [kind * k + t], credit[kind][t] at [2k + kind * k + t]
+uint32_t arrived_idx(const ne_ctx* c, uint32_t kind, uint32_t t) { return kind * c->cfg.subparts + t; }
+uint32_t credit_idx(const ne_ctx* c, uint32_t kind, uint32_t t) { return (2 + kind) * c->cfg.subparts + t; }
 
 bool ipc_debug() {
     static const bool on = std::getenv("NE_IPC_DEBUG") != nullptr;
@@ -107,7 +112,7 @@ bool ipc_ring(const ne_ctx* c) { return c->world > 1 && c->cfg.transport == NE_T
 int ipc_alloc_slots(ne_ctx* c, size_t slot_bytes, size_t nslots) {
     const uint32_t k = c->cfg.subparts;
     slot_bytes = (slot_bytes + 255) & ~(size_t)255;
-    const size_t bytes = nslots * slot_bytes + 2ull * k * sizeof(uint32_t);
+    const size_t bytes = nslots * slot_bytes + 4ull * k * sizeof(uint32_t);
     if (!ops().ok) return ne_fail(c, NE_ECUDA, "stream memory operations (cuStreamWaitValue32) unavailable");
     if (c->ipc.region && c->ipc.region_bytes == bytes) {  // same shape: keep region, flags and counters
         for (size_t i = 0; i < nslots; ++i) c->vslot[i] = reinterpret_cast<float*>(static_cast<char*>(c->ipc.region) + i * slot_bytes);
@@ -120,10 +125,12 @@ int ipc_alloc_slots(ne_ctx* c, size_t slot_bytes, size_t nslots) {
     c->ipc.flags = flags_of(c, c->ipc.region);
     // on the compute stream and waited for: the flags must be zero before any
     // peer can write them (the handles are exported after the load returns)
-    NE_CUDA(c, cudaMemsetAsync(c->ipc.flags, 0, 2ull * k * sizeof(uint32_t), c->stream));
+    NE_CUDA(c, cudaMemsetAsync(c->ipc.flags, 0, 4ull * k * sizeof(uint32_t), c->stream));
     NE_CUDA(c, cudaStreamSynchronize(c->stream));
-    c->ipc.pushed.assign(k, 0);
-    c->ipc.waited.assign(k, 0);
+    for (int kind = 0; kind < 2; ++kind) {
+        c->ipc.pushed[kind].assign(k, 0);
+        c->ipc.waited[kind].assign(k, 0);
+    }
     c->ipc.started = false;
     for (size_t i = 0; i < nslots; ++i) c->vslot[i] = reinterpret_cast<float*>(static_cast<char*>(c->ipc.region) + i * slot_bytes);
     return NE_OK;
@@ -132,30 +139,32 @@ int ipc_alloc_slots(ne_ctx* c, size_t slot_bytes, size_t nslots) {
 int ipc_reset_on_load(ne_ctx* c) {
     // the previous calls' return-home pushes into this rank were drained; the
     // re-initialised home sub-parts need no arrival
-    c->ipc.waited = c->ipc.pushed;
+    for (int kind = 0; kind < 2; ++kind) c->ipc.waited[kind] = c->ipc.pushed[kind];
     c->ipc.started = false;
     return NE_OK;
 }
 
-int ipc_wait_arrival(ne_ctx* c, uint32_t t) {
-    return wait_ge(c, c->stream, c->ipc.flags + t, ++c->ipc.waited[t]);
+int ipc_wait_arrival(ne_ctx* c, uint32_t t, uint32_t kind) {
+    return wait_ge(c, c->stream, c->ipc.flags + arrived_idx(c, kind, t), ++c->ipc.waited[kind][t]);
 }
 
-int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after, uint32_t dest,
-             uint32_t credit_to) {
+int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after, uint32_t kind, uint32_t dest,
+             uint32_t credit_to, uint32_t next_kind) {
     if (!c->ipc.connected || dest >= c->ipc.peer.size() || credit_to >= c->ipc.peer.size() || !c->ipc.peer[dest] ||
         !c->ipc.peer[credit_to])
         return ne_fail(c, NE_ESTATE, "IPC ring not connected to ranks %u / %u (ne_ipc_export / ne_ipc_connect)", dest,
                        credit_to);
     const uint32_t k = c->cfg.subparts;
-    const uint32_t i = ++c->ipc.pushed[t];
+    const bool first = c->ipc.pushed[0][t] + c->ipc.pushed[1][t] == 0;
+    const uint32_t cnt = ++c->ipc.pushed[kind][t];
     NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, after, 0));
-    if (i > 1) NE_TRY(wait_ge(c, c->comm_stream, c->ipc.flags + k + t, i - 1));  // credit: the target half is free
-    const size_t half = (size_t)(1 - c->cur) * k + t;                            // the other half of dest
+    if (!first) NE_TRY(wait_ge(c, c->comm_stream, c->ipc.flags + credit_idx(c, kind, t), cnt));  // target half free
+    const size_t half = (size_t)(1 - c->cur) * k + t;                                         // the other half of dest
     char* dst = static_cast<char*>(c->ipc.peer[dest]) + half * c->ipc.slot_bytes;
     NE_CUDA(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->comm_stream));
-    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.peer[dest]) + t, i));              // arrived at dest
-    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.peer[credit_to]) + k + t, i));     // credit
+    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.peer[dest]) + arrived_idx(c, kind, t), cnt));
+    NE_TRY(write_flag(c, c->comm_stream, flags_of(c, c->ipc.peer[credit_to]) + credit_idx(c, next_kind, t),
+                      c->ipc.pushed[next_kind][t] + 1));
     c->ipc.started = true;
     return NE_OK;
 }
@@ -163,11 +172,15 @@ int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t a
 int ipc_drain(ne_ctx* c, bool host_sync) {
     if (!c->ipc.region || !c->ipc.connected) return NE_OK;
     const uint32_t k = c->cfg.subparts;
+    const uint32_t G = c->cfg.groups > 1 ? c->cfg.groups : 1, L = (uint32_t)c->world / G;
+    const uint32_t k0 = L > 1 ? 0u : 1u;  // kind of the round-0 hop's credit (the next call's first push)
     for (uint32_t t = 0; t < k; ++t) {
-        if (!c->ipc.pushed[t]) continue;
-        NE_TRY(wait_ge(c, c->stream, c->ipc.flags + t, c->ipc.pushed[t]));      // every push into me landed
-        NE_TRY(wait_ge(c, c->stream, c->ipc.flags + k + t, c->ipc.pushed[t]));  // rank + 1 is done with mine
-        c->ipc.waited[t] = c->ipc.pushed[t];
+        if (c->ipc.pushed[0][t] + c->ipc.pushed[1][t] == 0) continue;
+        for (uint32_t kind = 0; kind < 2; ++kind)  // every push into me landed
+            NE_TRY(wait_ge(c, c->stream, c->ipc.flags + arrived_idx(c, kind, t), c->ipc.pushed[kind][t]));
+        // the last credit write into me (after the final round) landed
+        NE_TRY(wait_ge(c, c->stream, c->ipc.flags + credit_idx(c, k0, t), c->ipc.pushed[k0][t] + 1));
+        for (uint32_t kind = 0; kind < 2; ++kind) c->ipc.waited[kind][t] = c->ipc.pushed[kind][t];
     }
     c->ipc.started = false;
     if (host_sync) {

@@ -805,7 +805,7 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
             if (ipc && (r > 0 || ipc_resumed)) {  // the sub-part of this slot has landed
                 cudaEvent_t w0 = next_event(c), w1 = next_event(c);
                 NE_CUDA(c, cudaEventRecord(w0, c->stream));
-                NE_TRY(ipc_wait_arrival(c, t));
+                NE_TRY(ipc_wait_arrival(c, t, ring_kind(P, G, r + P - 1)));
                 NE_CUDA(c, cudaEventRecord(w1, c->stream));
                 tp.waits.push_back({w0, w1});
             } else if (recv[t]) {
@@ -825,8 +825,8 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
             tp.samples += sp.count;
             if (P > 1 && ipc) {  // copy-engine push into rank + 1 (ring_ipc.cpp)
                 const uint64_t send_rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
-                NE_TRY(ipc_push(c, t, V, send_rows * d * elem_bytes(c), e1, ring_dest(P, G, r, g),
-                                ring_src(P, G, r + 1, g)));
+                NE_TRY(ipc_push(c, t, V, send_rows * d * elem_bytes(c), e1, ring_kind(P, G, r), ring_dest(P, G, r, g),
+                                ring_src(P, G, r + 1, g), ring_kind(P, G, r + 1)));
             } else if (P > 1) {
                 const uint32_t vs_next = (uint32_t)plan_vsub(P, G, k, r + 1, t, g);
                 const uint64_t send_rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
