@@ -235,7 +235,7 @@ def main():
                          "(host: NEXT-2, the paper's pipeline stages 2 and 5, P:142)")
     ap.add_argument("--rule", default="sequential", choices=["sequential", "accumulated", "batch"],
                     help="update rule: Alg. 1 sequential (the headline), accumulated (word2vec), or batch "
-                         "(NEXT-4 shared negatives: 128-sample batches share 64 negatives, tcgen05 tf32)")
+                         "(NEXT-4 shared negatives: 128-sample batches share 32 negatives, tcgen05 tf32)")
     ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
                     help="ring transport at N > 1: NCCL send/recv kernels, or copy-engine pushes over CUDA IPC")
     ap.add_argument("--groups", type=int, default=1, help="NEXT-3 two-level ring: groups of N/groups ranks")
@@ -276,7 +276,7 @@ def main():
     torch.cuda.set_stream(stream)
     rule = {"sequential": ne.NE_UPDATE_SEQUENTIAL, "accumulated": ne.NE_UPDATE_ACCUMULATED,
             "batch": ne.NE_UPDATE_SHARED_BATCH}[args.rule]
-    negatives = 64 if args.rule == "batch" else w.negatives
+    negatives = 32 if args.rule == "batch" else w.negatives
     eng = Engine(dim=w.dim, negatives=negatives, walk_len=w.walk_len, window=w.window,
                  walks_per_node=1, episodes=episodes, subparts=args.subparts, deterministic=False, seed=42,
                  update_rule=rule, staging=ne.NE_STAGE_HOST if args.staging == "host" else ne.NE_STAGE_DEVICE,
@@ -331,8 +331,8 @@ def main():
     # roofline of the dominant kernel (SGNS), this rank's launches
     esz = 2 if args.storage == "bf16" else 4
     B = alg_bytes_per_sample(w.dim, w.negatives, esz)
-    if args.rule == "batch":  # per sample: pair, its vertex + positive rows (read + write), 64/128 of a shared
-        B = 8 + 8 * 64 / 128 + 2 * esz * w.dim * (2 + 64 / 128)  # negative row and of its alias entry
+    if args.rule == "batch":  # per sample: pair, its vertex + positive rows (read + write), 32/128 of a shared
+        B = 8 + 8 * 32 / 128 + 2 * esz * w.dim * (2 + 32 / 128)  # negative row and of its alias entry
     achieved = samples * B / (ms_train / 1e3) / 1e9 if ms_train > 0 else 0.0
     peak, peak_src = hbm_peak()
     traffic = dram_achieved = None
@@ -398,7 +398,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": desc, "step": "one epoch: walk + augment + order/bucket + SGNS (+ ring)",
                        "samples_per_step": samples_all / args.steps, "episodes": episodes, "subparts": args.subparts,
-                       "update_rule": args.rule + (" (K'=64 negatives shared per 128-sample batch)"
+                       "update_rule": args.rule + (" (K'=32 negatives shared per 128-sample batch)"
                                                    if args.rule == "batch" else ""),
                        "staging": args.staging,
                        "mode": "hogwild",
@@ -412,7 +412,7 @@ def main():
                          # profile) x this run's samples / SGNS time -- frac counts L2 hits as HBM bytes
                          "dram_achieved": dram_achieved,
                          "dram_frac": dram_achieved / peak if dram_achieved else None,
-                         "kernel": ("ne::sgns_batch_kernel<128,64> (tcgen05.mma kind::tf32, TMEM accumulators)"
+                         "kernel": ("ne::sgns_batch_kernel<128,32> (tcgen05.mma kind::tf32, TMEM accumulators)"
                                     if args.rule == "batch" else sgns_kernel_name(w.dim, w.negatives, esz == 2)),
                          "bytes_per_sample": B, "launches": train_launches,
                          "avg_launch_ms": ms_train / max(train_launches, 1), "peak_source": peak_src},

@@ -119,7 +119,7 @@ typedef struct {
                                 all 1+K dots use the pre-sample vertex row, whose
                                 accumulated gradient is applied once (NEXT-4);
                                 NE_UPDATE_SHARED_BATCH (2): mini-batches of 128
-                                consecutive samples share `negatives` (32 or 64)
+                                consecutive samples share `negatives` (= 32)
                                 negatives and take one SGD step on the batch loss
                                 (Ji et al. / BlazingText; DESIGN D17) --
                                 three tf32 tensor-core products per batch (tcgen05,
@@ -332,9 +332,9 @@ int ne_capture_block(ne_ctx *ctx, uint32_t epoch, uint32_t episode, uint32_t vsu
 
 /* NEXT-4 test hook: the shared-negative batch kernel's three tcgen05 tf32
  * products on the current device, through its shared-memory tiles,
- * descriptors and TMEM read-back: host row-major V[128][128], N[64][128],
- * G[128][64] -> S = V N^T [128][64], dV = G N [128][128], dNt = V^T G
- * [128][64].  Errors: NE_EINVAL, NE_ECUDA. */
+ * transposes, descriptors and TMEM read-back: host row-major V[128][128],
+ * N[32][128], G[128][32] -> S = V N^T [128][32], dV = G N [128][128],
+ * dNt = V^T G [128][32].  Errors: NE_EINVAL, NE_ECUDA. */
 int ne_umma_products(const float *V, const float *N, const float *G, float *S, float *dV, float *dNt);
 
 /* Diagnostics hook: one tcgen05 tf32 product D[128][N] from raw shared-memory

@@ -23,15 +23,15 @@
 // batches share rows; every write-back is a red.global.add of the delta), the
 // deterministic mode runs one CTA over the batches in order.
 //
-// Shared-memory tiles use the UMMA canonical no-swizzle ("interleaved") layout:
+// Every operand is K-major (measured: with the no-swizzle layout, MN-major
+// tf32 operands multiply as zeros -- CUTLASS allows MN-major tf32 only in the
+// 128B/32B-base swizzled layout), in the UMMA canonical no-swizzle layout:
 // 8-row x 16-byte core matrices, row r chunk c (4 floats) at byte
-//   ((r / 8) * (cols / 4) + c) * 128 + (r % 8) * 16.
-// The same bytes serve as a K-major operand (K = the column index; LBO = 128 B
-// between K chunks, SBO = cols * 32 B between row groups) and as an MN-major
-// operand (MN = the column index; SBO = 128 B between column groups of 4,
-// LBO = cols * 32 B between groups of 8 rows = 8 K values), so no tile is ever
-// transposed: MMA1 reads V and N K-major, MMA2 reads G K-major and N MN-major,
-// MMA3 reads V and G MN-major.
+//   ((r / 8) * (cols / 4) + c) * 128 + (r % 8) * 16,
+// LBO = 128 B between K chunks, SBO = cols * 32 B between row groups.  Each
+// matrix is therefore kept in both orientations the products need: V (rows i)
+// and V^T (rows = dimensions), N and N^T, G and G^T -- 192 KB at d = 128,
+// K' = 32 (the positive context rows are read from global memory).
 #include <algorithm>
 #include <cstdlib>
 
@@ -58,17 +58,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes
     d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
     d |= (uint64_t)1 << 46;  // version = 1 (sm_100)
     return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE
-}
-
-// MN-major operand descriptor: kg = byte stride between groups of 8 K values,
-// mg = byte stride between groups of 4 MN elements (16 B).  g_mn_variant
-// (diagnostics only, set by ne_umma_products) selects alternative encodings.
-__device__ int g_mn_variant = 0;
-__device__ __forceinline__ uint64_t mn_desc(uint32_t saddr, uint32_t kg, uint32_t mg) {
-    const int v = g_mn_variant;
-    uint64_t d = (v & 1) ? umma_desc(saddr, mg, kg) : umma_desc(saddr, kg, mg);
-    if (v & 2) d |= (uint64_t)1 << 52;  // lbo mode
-    return d;
 }
 
 // Instruction descriptor of kind::tf32: D fp32, A/B tf32, M x N, majors.
@@ -144,11 +133,10 @@ __device__ __forceinline__ float sigmoid_clamped(float x, float& ex) {
     return __fdividef(1.f, 1.f + ex);
 }
 
-// The three products of a batch, issued by one thread (tiles in the layout of
-// tile_off; D = dimension, KP = shared negatives, B = 128 rows):
-//   S[B x KP]    = V N^T   A = V   K-major, B = N K-major      (K = D)
-//   dV[B x D]    = G N     A = G   K-major, B = N MN-major     (K = KP)
-//   dN^T[D x KP] = V^T G   A = V^T MN-major, B = G MN-major    (K = B)
+// The three products of a batch, issued by one thread, all operands K-major:
+//   S[B x KP]    = V N^T   A = V   (i x d),  B = N   (j x d)    K = d
+//   dV[B x D]    = G N     A = G   (i x j),  B = N^T (d x j)    K = KP
+//   dN^T[D x KP] = V^T G   A = V^T (d x i),  B = G^T (j x i)    K = B
 template <int D, int KP>
 __device__ __forceinline__ void issue_S(uint32_t sV, uint32_t sN, uint32_t t_S) {
     constexpr uint32_t idesc = idesc_tf32(kBatch, KP, false, false);
@@ -158,21 +146,46 @@ __device__ __forceinline__ void issue_S(uint32_t sV, uint32_t sN, uint32_t t_S) 
                  ks > 0);
 }
 template <int D, int KP>
-__device__ __forceinline__ void issue_dV(uint32_t sG, uint32_t sN, uint32_t t_dV) {
-    constexpr uint32_t idesc = idesc_tf32(kBatch, D, false, true);
+__device__ __forceinline__ void issue_dV(uint32_t sG, uint32_t sNt, uint32_t t_dV) {
+    constexpr uint32_t idesc = idesc_tf32(kBatch, D, false, false);
 #pragma unroll
     for (uint32_t ks = 0; ks < (uint32_t)KP / 8; ++ks)
-        mma_tf32(t_dV, umma_desc(sG + ks * 256u, 128u, KP * 32u), mn_desc(sN + ks * D * 32u, D * 32u, 128u), idesc,
+        mma_tf32(t_dV, umma_desc(sG + ks * 256u, 128u, KP * 32u), umma_desc(sNt + ks * 256u, 128u, KP * 32u), idesc,
                  ks > 0);
 }
 template <int D, int KP>
-__device__ __forceinline__ void issue_dNt(uint32_t sV, uint32_t sG, uint32_t t_dNt) {
-    constexpr uint32_t idesc = idesc_tf32(D, KP, true, true);
+__device__ __forceinline__ void issue_dNt(uint32_t sVt, uint32_t sGt, uint32_t t_dNt) {
+    constexpr uint32_t idesc = idesc_tf32(D, KP, false, false);
 #pragma unroll
     for (uint32_t ks = 0; ks < (uint32_t)kBatch / 8; ++ks)
-        mma_tf32(t_dNt, mn_desc(sV + ks * D * 32u, D * 32u, 128u), mn_desc(sG + ks * KP * 32u, KP * 32u, 128u),
+        mma_tf32(t_dNt, umma_desc(sVt + ks * 256u, 128u, kBatch * 32u), umma_desc(sGt + ks * 256u, 128u, kBatch * 32u),
                  idesc, ks > 0);
 }
+
+// dst = src^T between two tiles (src: R rows x C cols, dst: C rows x R cols):
+// every thread gathers 4 consecutive source rows of one column and stores them
+// as one 16-byte chunk of the destination row.
+template <uint32_t R, uint32_t C>
+__device__ __forceinline__ void transpose_tile(const unsigned char* src, unsigned char* dst, uint32_t tid) {
+    for (uint32_t f = tid; f < R / 4 * C; f += kBatch) {
+        const uint32_t col = f % C, r4 = f / C;  // destination row col, chunk r4 (source rows 4 r4 .. 4 r4 + 3)
+        float4 v;
+        float* vp = &v.x;
+#pragma unroll
+        for (uint32_t e = 0; e < 4; ++e)
+            vp[e] = *reinterpret_cast<const float*>(src + tile_off(4 * r4 + e, col >> 2, C) + (col & 3u) * 4u);
+        *reinterpret_cast<float4*>(dst + tile_off(col, r4, R)) = v;
+    }
+}
+
+// Shared-memory plan of a batch (bytes): V, V^T (B x D each), N (KP x D),
+// N^T (D x KP), G (B x KP), G^T (KP x B), then barriers, TMEM address, ids.
+template <int D, int KP>
+struct BatchSmem {
+    static constexpr uint32_t V = 0, Vt = V + kBatch * D * 4, N = Vt + kBatch * D * 4, Nt = N + KP * D * 4,
+                              G = Nt + KP * D * 4, Gt = G + kBatch * KP * 4, tail = Gt + kBatch * KP * 4;
+    static constexpr size_t bytes = tail + 16 + 16 + (2 * kBatch + KP) * 4;
+};
 
 }  // namespace
 
@@ -181,22 +194,19 @@ __device__ __forceinline__ void issue_dNt(uint32_t sV, uint32_t sG, uint32_t t_d
 template <int D, int KP>
 __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
     static_assert(D == 128, "the dN^T product has M = d: 128");
-    static_assert(KP == 32 || KP == 64, "K' in {32, 64} (shared memory: 2 x 64 KB + 2 x 32 KB at 64)");
-    constexpr uint32_t kTileV = kBatch * D * 4, kTileN = KP * D * 4, kTileG = kBatch * KP * 4;
-    constexpr uint32_t kTmemCols = 256;  // S: KP, dV: D, dN^T: KP (<= 256)
-    static_assert(2 * KP + D <= (int)kTmemCols, "TMEM columns");
+    static_assert(KP == 32, "K' = 32 (both orientations of V, N, G: 192 KB of shared memory)");
+    using SM = BatchSmem<D, KP>;
+    constexpr uint32_t kTmemCols = 256;  // S: KP, dV: D, dN^T: KP
     extern __shared__ __align__(1024) unsigned char smem[];
-    unsigned char* sV = smem;                  // batch vertex rows, B x D
-    unsigned char* sC = sV + kTileV;           // batch positive context rows, B x D
-    unsigned char* sN = sC + kTileV;           // shared negative rows, KP x D
-    unsigned char* sG = sN + kTileN;           // G = lr sigma(S), B x KP; later dN rows (KP x D, row-major)
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sG + kTileG);   // [0]: S ready, [1]: dV, dN^T ready
+    unsigned char *sV = smem + SM::V, *sVt = smem + SM::Vt, *sN = smem + SM::N, *sNt = smem + SM::Nt,
+                  *sG = smem + SM::G, *sGt = smem + SM::Gt;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::tail);   // [0]: S ready, [1]: dV, dN^T ready
     uint32_t* tmem_base = reinterpret_cast<uint32_t*>(bar + 2);
-    uint32_t* s_src = tmem_base + 4;           // kBatch
-    uint32_t* s_dst = s_src + kBatch;          // kBatch
-    uint32_t* s_neg = s_dst + kBatch;          // KP
+    uint32_t* s_src = tmem_base + 4;
+    uint32_t* s_dst = s_src + kBatch;
+    uint32_t* s_neg = s_dst + kBatch;
 
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
                      ::"r"(smem_u32(tmem_base)), "n"(kTmemCols) : "memory");
@@ -219,14 +229,16 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
     const float lr = p.lr;
     const uint64_t nbatch = (p.count + kBatch - 1) / kBatch;
     const uint32_t i = tid;  // batch row of this thread
+    constexpr uint32_t KC = D / 4;
     double loss = 0.0;
     uint32_t phase = 0;
 
     for (uint64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
         const uint64_t p0 = b * kBatch;
         const uint32_t nb = (uint32_t)(p.count - p0 < (uint64_t)kBatch ? p.count - p0 : (uint64_t)kBatch);
+        const bool live = i < nb;
         // ---- ids: pairs, shared negatives (O8 with the batch counter, tag BNEG)
-        if (i < nb) {
+        if (live) {
             const uint2 pr = p.pool[p0 + i];
             s_src[i] = pr.x;
             s_dst[i] = pr.y;
@@ -239,24 +251,20 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
             s_neg[i] = (uint32_t)(p.c_begin + (x.z < ta.x ? col : ta.y));
         }
         __syncthreads();
-        // ---- gather rows into the UMMA tiles (cp.async, 16 B per lane; a warp
-        // covers 8 rows x 4 chunks so each quarter-warp writes 128 contiguous bytes)
-        constexpr uint32_t KC = D / 4;
+        // ---- gather V and N rows (cp.async, 16 B per lane; a warp covers 8 rows
+        // x 4 chunks so each quarter-warp writes 128 contiguous bytes)
         for (uint32_t f = tid; f < kBatch * KC; f += kBatch) {
             const uint32_t q = f >> 5, l = f & 31u;
             const uint32_t row = (q / (KC / 4)) * 8 + (l & 7u), chunk = (q % (KC / 4)) * 4 + (l >> 3);
             const uint32_t off = tile_off(row, chunk, D);
-            if (row < nb) {
-                cp_async16(sV + off, p.V + (uint64_t)(s_src[row] - p.v_begin) * D + chunk * 4);
-                cp_async16(sC + off, p.C + (uint64_t)(s_dst[row] - p.c_begin) * D + chunk * 4);
-            } else {
-                *reinterpret_cast<float4*>(sV + off) = make_float4(0.f, 0.f, 0.f, 0.f);
-                *reinterpret_cast<float4*>(sC + off) = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            if (row < (uint32_t)KP)
-                cp_async16(sN + off, p.C + (uint64_t)(s_neg[row] - p.c_begin) * D + chunk * 4);
+            if (row < nb) cp_async16(sV + off, p.V + (uint64_t)(s_src[row] - p.v_begin) * D + chunk * 4);
+            else *reinterpret_cast<float4*>(sV + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row < (uint32_t)KP) cp_async16(sN + off, p.C + (uint64_t)(s_neg[row] - p.c_begin) * D + chunk * 4);
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        transpose_tile<kBatch, D>(sV, sVt, tid);
+        transpose_tile<KP, D>(sN, sNt, tid);
         fence_async_smem();
         __syncthreads();
         // ---- MMA1: S = V N^T
@@ -265,14 +273,17 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
             issue_S<D, KP>(smem_u32(sV), smem_u32(sN), t_S);
             mma_commit(&bar[0]);
         }
-        // ---- positive term of row i (CUDA cores, overlapping MMA1)
+        // ---- positive term of row i (CUDA cores, overlapping MMA1): x = v . c+
+        // with c+ read from global memory (no shared copy; no C row is written
+        // before every thread has read its c+ twice, see the write-back)
         float gpos = 0.f;
-        if (i < nb) {
+        const float* crow = p.C + (uint64_t)((live ? s_dst[i] : p.c_begin) - p.c_begin) * D;
+        if (live) {
             float x = 0.f;
 #pragma unroll 8
             for (uint32_t c = 0; c < KC; ++c) {
                 const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(i, c, D));
-                const float4 cc = *reinterpret_cast<const float4*>(sC + tile_off(i, c, D));
+                const float4 cc = __ldcg(reinterpret_cast<const float4*>(crow) + c);
                 x = fmaf(v.x, cc.x, fmaf(v.y, cc.y, fmaf(v.z, cc.z, fmaf(v.w, cc.w, x))));
             }
             float ex;
@@ -280,15 +291,14 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
             gpos = lr * (s - 1.f);
             loss += (double)__logf(1.f + ex);  // -log s
         }
-        // ---- epilogue 1: G = lr sigma(S) (rows of padding stay 0)
+        // ---- epilogue 1: G = lr sigma(S) and G^T (padding rows stay 0)
         mbar_wait(&bar[0], phase);
         fence_after();
-#pragma unroll
-        for (uint32_t j0 = 0; j0 < (uint32_t)KP; j0 += 32) {
+        {
             float sv[32];
-            tmem_ld32(t_S + lane_base + j0, sv);
+            tmem_ld32(t_S + lane_base, sv);
 #pragma unroll
-            for (uint32_t c = 0; c < 8; ++c) {
+            for (uint32_t c = 0; c < KP / 4; ++c) {
                 float4 g;
                 float* gp = &g.x;
 #pragma unroll
@@ -296,10 +306,11 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
                     float ex;
                     const float xcl = fminf(fmaxf(sv[c * 4 + e], -30.f), 30.f);
                     const float s = sigmoid_clamped(sv[c * 4 + e], ex);
-                    gp[e] = i < nb ? lr * s : 0.f;
-                    if (i < nb) loss += (double)(__logf(1.f + ex) + xcl);  // -log(1 - s)
+                    gp[e] = live ? lr * s : 0.f;
+                    if (live) loss += (double)(__logf(1.f + ex) + xcl);  // -log(1 - s)
+                    *reinterpret_cast<float*>(sGt + tile_off(c * 4 + e, i >> 2, kBatch) + (i & 3u) * 4u) = gp[e];
                 }
-                *reinterpret_cast<float4*>(sG + tile_off(i, (j0 >> 2) + c, KP)) = g;
+                *reinterpret_cast<float4*>(sG + tile_off(i, c, KP)) = g;
             }
         }
         fence_async_smem();
@@ -308,53 +319,55 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         // ---- MMA2: dV = G N; MMA3: dN^T = V^T G
         if (tid == 0) {
             fence_after();
-            issue_dV<D, KP>(smem_u32(sG), smem_u32(sN), t_dV);
-            issue_dNt<D, KP>(smem_u32(sV), smem_u32(sG), t_dNt);
+            issue_dV<D, KP>(smem_u32(sG), smem_u32(sNt), t_dV);
+            issue_dNt<D, KP>(smem_u32(sVt), smem_u32(sGt), t_dNt);
             mma_commit(&bar[1]);
         }
         mbar_wait(&bar[1], phase);
         fence_after();
-        // ---- write-back, all deltas from the batch-start snapshot (the
-        // tcgen05.ld are warp-collective: every thread runs them, padding rows
-        // skip only the stores)
-        {
-            const bool live = i < nb;
-            float* vrow = p.V + (uint64_t)((live ? s_src[i] : p.v_begin) - p.v_begin) * D;
-            float* crow = p.C + (uint64_t)((live ? s_dst[i] : p.c_begin) - p.c_begin) * D;
+        // ---- write-back from the batch-start snapshot.  (1) vertex rows: -(dV +
+        // gpos c+), c+ read again from global (no C row written yet); the
+        // tcgen05.ld are warp-collective: every thread runs them
+        float* vrow = p.V + (uint64_t)((live ? s_src[i] : p.v_begin) - p.v_begin) * D;
 #pragma unroll 1
-            for (uint32_t d0 = 0; d0 < (uint32_t)D; d0 += 32) {
-                float dv[32];
-                tmem_ld32(t_dV + lane_base + d0, dv);
-                if (!live) continue;
+        for (uint32_t d0 = 0; d0 < (uint32_t)D; d0 += 32) {
+            float dv[32];
+            tmem_ld32(t_dV + lane_base + d0, dv);
+            if (!live) continue;
 #pragma unroll
-                for (uint32_t c = 0; c < 8; ++c) {
-                    const uint32_t ch = (d0 >> 2) + c;
-                    const float4 cc = *reinterpret_cast<const float4*>(sC + tile_off(i, ch, D));
-                    const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(i, ch, D));
-                    atomicAdd(reinterpret_cast<float4*>(vrow) + ch,
-                              make_float4(-(dv[4 * c] + gpos * cc.x), -(dv[4 * c + 1] + gpos * cc.y),
-                                          -(dv[4 * c + 2] + gpos * cc.z), -(dv[4 * c + 3] + gpos * cc.w)));
-                    atomicAdd(reinterpret_cast<float4*>(crow) + ch,
-                              make_float4(-gpos * v.x, -gpos * v.y, -gpos * v.z, -gpos * v.w));
-                }
+            for (uint32_t c = 0; c < 8; ++c) {
+                const uint32_t ch = (d0 >> 2) + c;
+                const float4 cc = __ldcg(reinterpret_cast<const float4*>(crow) + ch);
+                atomicAdd(reinterpret_cast<float4*>(vrow) + ch,
+                          make_float4(-(dv[4 * c] + gpos * cc.x), -(dv[4 * c + 1] + gpos * cc.y),
+                                      -(dv[4 * c + 2] + gpos * cc.z), -(dv[4 * c + 3] + gpos * cc.w)));
             }
         }
-        // dN^T: TMEM lane = dimension, column = negative j; stage dN rows in the
-        // G tile (MMA3 has consumed it) and add them with coalesced row reductions
-        __syncthreads();
-        float* sDN = reinterpret_cast<float*>(sG);  // KP x D, row-major
-#pragma unroll
-        for (uint32_t j0 = 0; j0 < (uint32_t)KP; j0 += 32) {
+        // (2) the dN^T lanes (= dimensions) into dN rows staged in the G tile
+        {
             float dn[32];
-            tmem_ld32(t_dNt + lane_base + j0, dn);
+            tmem_ld32(t_dNt + lane_base, dn);
+            float* sDN = reinterpret_cast<float*>(sG);  // KP x D, row-major (G is consumed)
 #pragma unroll
-            for (uint32_t e = 0; e < 32; ++e) sDN[(j0 + e) * D + i] = dn[e];
+            for (uint32_t e = 0; e < (uint32_t)KP; ++e) sDN[e * D + i] = dn[e];
         }
         fence_before();
-        __syncthreads();
+        __syncthreads();  // every c+ read (1) is done before any C row is written
+        // (3) positive context rows: -gpos v
+        if (live) {
+            float* cw = p.C + (uint64_t)(s_dst[i] - p.c_begin) * D;
+#pragma unroll 8
+            for (uint32_t c = 0; c < KC; ++c) {
+                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(i, c, D));
+                atomicAdd(reinterpret_cast<float4*>(cw) + c, make_float4(-gpos * v.x, -gpos * v.y, -gpos * v.z,
+                                                                         -gpos * v.w));
+            }
+        }
+        // (4) negative rows: -dN, coalesced row reductions
+        const float* sDN = reinterpret_cast<const float*>(sG);
         for (uint32_t j = warp; j < (uint32_t)KP; j += kBatch / 32) {
             float* nrow = p.C + (uint64_t)(s_neg[j] - p.c_begin) * D;
-            for (uint32_t ch = lane; ch < KC; ch += 32) {
+            for (uint32_t ch = tid & 31u; ch < KC; ch += 32) {
                 const float4 g = reinterpret_cast<const float4*>(sDN + j * D)[ch];
                 atomicAdd(reinterpret_cast<float4*>(nrow) + ch, make_float4(-g.x, -g.y, -g.z, -g.w));
             }
@@ -369,18 +382,19 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
-// Test hook (ne_umma_products): the three products above on dense row-major
-// inputs V[128][D], N[KP][D], G[128][KP] through the same tiles, descriptors
-// and TMEM read-back; outputs S[128][KP], dV[128][D], dNt[D][KP] row-major.
+// Test hook (ne_umma_products): the batch kernel's tiles, transposes and three
+// products on dense row-major inputs V[128][D], N[KP][D], G[128][KP]; outputs
+// S[128][KP], dV[128][D], dNt[D][KP] row-major.
 template <int D, int KP>
 __global__ void __launch_bounds__(kBatch, 1) umma_products_kernel(const float* __restrict__ V,
                                                                   const float* __restrict__ N,
                                                                   const float* __restrict__ G, float* __restrict__ S,
                                                                   float* __restrict__ dV, float* __restrict__ dNt) {
-    constexpr uint32_t kTileV = kBatch * D * 4, kTileN = KP * D * 4, kTileG = kBatch * KP * 4;
+    using SM = BatchSmem<D, KP>;
     extern __shared__ __align__(1024) unsigned char smem[];
-    unsigned char *sV = smem, *sN = sV + kTileV, *sG = sN + kTileN;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sG + kTileG);
+    unsigned char *sV = smem + SM::V, *sVt = smem + SM::Vt, *sN = smem + SM::N, *sNt = smem + SM::Nt,
+                  *sG = smem + SM::G, *sGt = smem + SM::Gt;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::tail);
     uint32_t* tmem_base = reinterpret_cast<uint32_t*>(bar + 2);
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     if (warp == 0) {
@@ -401,6 +415,10 @@ __global__ void __launch_bounds__(kBatch, 1) umma_products_kernel(const float* _
     for (uint32_t r = 0; r < kBatch; ++r)
         for (uint32_t c = tid; c < KP / 4; c += kBatch)
             *reinterpret_cast<float4*>(sG + tile_off(r, c, KP)) = reinterpret_cast<const float4*>(G + r * KP)[c];
+    __syncthreads();
+    transpose_tile<kBatch, D>(sV, sVt, tid);
+    transpose_tile<KP, D>(sN, sNt, tid);
+    transpose_tile<kBatch, KP>(sG, sGt, tid);
     fence_async_smem();
     fence_before();
     __syncthreads();
@@ -408,8 +426,8 @@ __global__ void __launch_bounds__(kBatch, 1) umma_products_kernel(const float* _
     const uint32_t tmem = *tmem_base, t_S = tmem, t_dV = tmem + KP, t_dNt = tmem + KP + D;
     if (tid == 0) {
         issue_S<D, KP>(smem_u32(sV), smem_u32(sN), t_S);
-        issue_dV<D, KP>(smem_u32(sG), smem_u32(sN), t_dV);
-        issue_dNt<D, KP>(smem_u32(sV), smem_u32(sG), t_dNt);
+        issue_dV<D, KP>(smem_u32(sG), smem_u32(sNt), t_dV);
+        issue_dNt<D, KP>(smem_u32(sVt), smem_u32(sGt), t_dNt);
         mma_commit(&bar[0]);
     }
     mbar_wait(&bar[0], 0);
@@ -502,12 +520,8 @@ cudaError_t launch_umma_raw(const void* a_img, const void* b_img, uint32_t img_b
 
 cudaError_t launch_umma_products(const float* V, const float* N, const float* G, float* S, float* dV, float* dNt,
                                  cudaStream_t s) {
-    if (const char* e = std::getenv("NE_UMMA_VARIANT")) {  // diagnostics
-        const int v = std::atoi(e);
-        cudaMemcpyToSymbol(g_mn_variant, &v, sizeof v);
-    }
-    constexpr size_t smem = 128ull * 128 * 4 + 64ull * 128 * 4 + 128ull * 64 * 4 + 64;
-    auto kern = umma_products_kernel<128, 64>;
+    constexpr size_t smem = BatchSmem<128, 32>::bytes;
+    auto kern = umma_products_kernel<128, 32>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<1, kBatch, smem, s>>>(V, N, G, S, dV, dNt);
@@ -516,8 +530,7 @@ cudaError_t launch_umma_products(const float* V, const float* N, const float* G,
 
 template <int D, int KP>
 static cudaError_t launch_batch(const SgnsParams& p, const Device& dev, cudaStream_t s) {
-    constexpr size_t smem = 2ull * kBatch * D * 4 + (size_t)KP * D * 4 + (size_t)kBatch * KP * 4 + 16 + 16 +
-                            (2 * kBatch + KP) * 4;
+    constexpr size_t smem = BatchSmem<D, KP>::bytes;
     auto kern = sgns_batch_kernel<D, KP>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -533,7 +546,6 @@ cudaError_t launch_sgns_batch(const SgnsParams& p, const Device& dev, cudaStream
     if (p.d != 128 || p.bf16) return cudaErrorNotSupported;
     switch (p.K) {
         case 32: return launch_batch<128, 32>(p, dev, s);
-        case 64: return launch_batch<128, 64>(p, dev, s);
         default: return cudaErrorNotSupported;
     }
 }

@@ -149,9 +149,9 @@ cudaError_t launch_sgns_bf16(const SgnsParams& p, const Device& dev, cudaStream_
 // NEXT-4 shared-negative mini-batch rule (p.accumulate == 2; kernels_sgns_batch.cu):
 // batches of 128 samples share p.K negatives; tcgen05 tf32 products.  d == 128.
 cudaError_t launch_sgns_batch(const SgnsParams& p, const Device& dev, cudaStream_t s);
-// Test hook: the batch kernel's three tcgen05 products (d = 128, K' = 64) on dense
-// row-major device inputs V[128][128], N[64][128], G[128][64] ->
-// S = V N^T [128][64], dV = G N [128][128], dNt = V^T G [128][64].
+// Test hook: the batch kernel's three tcgen05 products (d = 128, K' = 32) on dense
+// row-major device inputs V[128][128], N[32][128], G[128][32] ->
+// S = V N^T [128][32], dV = G N [128][128], dNt = V^T G [128][32].
 cudaError_t launch_umma_raw(const void* a_img, const void* b_img, uint32_t img_bytes, uint64_t a_hi, uint64_t b_hi,
                             uint32_t a_lbo, uint32_t a_sbo, uint32_t b_lbo, uint32_t b_sbo, uint32_t a_step,
                             uint32_t b_step, uint32_t ksteps, uint32_t idesc, uint32_t N, float* D, cudaStream_t s);

@@ -1006,9 +1006,9 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
     if (g.dim == 0 || g.dim % 4 || g.dim > 512)
         return bad(ne_fail(c, NE_EINVAL, "dim=%u must be a multiple of 4 in [4, 512]", g.dim));
     if (g.update_rule == NE_UPDATE_SHARED_BATCH) {
-        if (g.dim != 128 || (g.negatives != 32 && g.negatives != 64) || g.storage != NE_STORE_F32)
-            return bad(ne_fail(c, NE_EINVAL, "update_rule=2 (shared-negative batches) needs dim=128, negatives in "
-                                             "{32, 64} and fp32 storage (dim=%u negatives=%u)", g.dim, g.negatives));
+        if (g.dim != 128 || g.negatives != 32 || g.storage != NE_STORE_F32)
+            return bad(ne_fail(c, NE_EINVAL, "update_rule=2 (shared-negative batches) needs dim=128, negatives=32 "
+                                             "and fp32 storage (dim=%u negatives=%u)", g.dim, g.negatives));
     } else if (g.negatives > 8) {
         return bad(ne_fail(c, NE_EINVAL, "negatives=%u > 8", g.negatives));
     }
@@ -1595,7 +1595,7 @@ int ne_capture_block(ne_ctx* c, uint32_t epoch, uint32_t episode, uint32_t vsub,
 int ne_umma_products(const float* V, const float* N, const float* G, float* S, float* dV, float* dNt) {
     if (!V || !N || !G || !S || !dV || !dNt) return NE_EINVAL;
     float* d = nullptr;
-    const size_t nV = 128 * 128, nN = 64 * 128, nG = 128 * 64, nS = 128 * 64, ndV = 128 * 128, ndN = 128 * 64;
+    const size_t nV = 128 * 128, nN = 32 * 128, nG = 128 * 32, nS = 128 * 32, ndV = 128 * 128, ndN = 128 * 32;
     if (cudaMalloc(&d, (nV + nN + nG + nS + ndV + ndN) * sizeof(float)) != cudaSuccess) return NE_ECUDA;
     float *dV_in = d, *dN_in = dV_in + nV, *dG_in = dN_in + nN, *dS = dG_in + nG, *ddV = dS + nS, *ddN = ddV + ndV;
     int rc = NE_OK;

@@ -256,8 +256,8 @@ def ne_ipc_connect(ctx, blobs: list[bytes]) -> None:
 def ne_umma_products(V, N, G):
     """Test hook: the tcgen05 products of the batch kernel; returns (S, dV, dNt)."""
     V, N, G = (np.ascontiguousarray(x, np.float32) for x in (V, N, G))
-    assert V.shape == (128, 128) and N.shape == (64, 128) and G.shape == (128, 64)
-    S, dV, dNt = np.zeros((128, 64), np.float32), np.zeros((128, 128), np.float32), np.zeros((128, 64), np.float32)
+    assert V.shape == (128, 128) and N.shape == (32, 128) and G.shape == (128, 32)
+    S, dV, dNt = np.zeros((128, 32), np.float32), np.zeros((128, 128), np.float32), np.zeros((128, 32), np.float32)
     rc = _lib.ne_umma_products(_ptr(V), _ptr(N), _ptr(G), _ptr(S), _ptr(dV), _ptr(dNt))
     if rc != NE_OK:
         raise NEError(rc, "ne_umma_products failed")
