@@ -12,7 +12,6 @@
 #   launches[:ARGS]       ncu launch list (gpu__time_duration) of a short bench with ARGS
 #   ncu:WORKLOAD[:ARGS]   ncu --set full of the first SGNS launch of tools/probe.py WORKLOAD ARGS
 #   ncuk:REGEX:WORKLOAD   ncu --set full of the first launch matching REGEX in tools/probe.py WORKLOAD
-#   sanitize              compute-sanitizer memcheck + racecheck of a deterministic C1 epoch
 #   py:SCRIPT[:ARGS]      python SCRIPT ARGS
 #   env:VAR=VALUE         export VAR=VALUE for the following steps (env:VAR= unsets it)
 # Every step has its own timeout; logs land in gpurun_out/OUT/.
@@ -65,12 +64,6 @@ for step in "$@"; do
       ncu -i /tmp/ncu_$i.ncu-rep --page raw --csv > "$OUT/ncu_${W}_${i}_raw.csv" 2>/dev/null
       ncu -i /tmp/ncu_$i.ncu-rep --page details --csv > "$OUT/ncu_${W}_${i}_details.csv" 2>/dev/null
       ncu -i /tmp/ncu_$i.ncu-rep --page source --csv --print-source sass > "$OUT/ncu_${W}_${i}_source.csv" 2>/dev/null ;;
-    sanitize)
-      for tool in memcheck racecheck; do
-        timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_epoch.py \
-          > "$OUT/sanitize_$tool.log" 2>&1
-        echo "$tool rc=$?"; tail -3 "$OUT/sanitize_$tool.log"
-      done ;;
     env)
       v=${rest%%=*}; val=${rest#*=}
       if [ -n "$val" ]; then export "$v=$val"; else unset "$v"; fi
