@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "ne.h"
 #include "ne_internal.h"
@@ -158,6 +159,14 @@ int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t a
              uint32_t credit_to, uint32_t next_kind);
 int ipc_drain(ne_ctx* c, bool host_sync);            // every push into / out of this rank has landed
 void ipc_release(ne_ctx* c);
+
+// NVTX range for profilers (nsys / ncu --nvtx): walk, build, train, ring phases.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Sets ctx->err to "NE_<CODE>: <message>" and returns code.
 int ne_fail(ne_ctx* c, int code, const char* fmt, ...) __attribute__((format(printf, 3, 4)));

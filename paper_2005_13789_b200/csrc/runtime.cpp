@@ -11,6 +11,7 @@
 //   slots         u64[N]   pi-indexed pairs (one episode, ~0 = hole)
 //   pool          u64[N]   (src, dst) grouped by vertex sub-part, pi order
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <memory>
 #include <cstdarg>
@@ -42,6 +43,46 @@ int ne_fail(ne_ctx* c, int code, const char* fmt, ...) {
 
 
 namespace {
+
+// Host wait for a stream that may hold NCCL work (ring, pool exchange): poll it
+// and the communicators' asynchronous errors, so a failed or vanished peer
+// returns NE_ENCCL (communicators aborted) instead of hanging; a stall longer
+// than NE_NCCL_TIMEOUT_S (default 900 s) is treated the same way.
+int wait_stream(ne_ctx* c, cudaStream_t s) {
+    if (!(c->world > 1 && c->comm)) {
+        NE_CUDA(c, cudaStreamSynchronize(s));
+        return NE_OK;
+    }
+    static const double limit_s = [] {
+        const char* e = std::getenv("NE_NCCL_TIMEOUT_S");
+        return e ? std::atof(e) : 900.0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return NE_OK;
+        if (q != cudaErrorNotReady) NE_CUDA(c, q);
+        for (ncclComm_t comm : {c->comm, c->comm_walk}) {
+            ncclResult_t async = ncclSuccess;
+            if (comm && ncclCommGetAsyncError(comm, &async) == ncclSuccess && async != ncclSuccess) {
+                ncclCommAbort(c->comm_walk);
+                ncclCommAbort(c->comm);
+                c->comm_walk = c->comm = nullptr;
+                return ne_fail(c, NE_ENCCL, "NCCL asynchronous error on rank %d: %s (communicators aborted)", c->rank,
+                               ncclGetErrorString(async));
+            }
+        }
+        const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (waited > limit_s) {
+            ncclCommAbort(c->comm_walk);
+            ncclCommAbort(c->comm);
+            c->comm_walk = c->comm = nullptr;
+            return ne_fail(c, NE_ENCCL, "rank %d: ring / exchange stalled for %.0f s (a peer is gone?); communicators "
+                                        "aborted", c->rank, waited);
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
 
 thread_local std::string g_create_error;  // ne_last_error(NULL) after a failed ne_create
 
@@ -300,6 +341,7 @@ void shard_range(uint64_t units, uint32_t P, uint32_t s, uint64_t* b, uint64_t* 
 }
 
 int do_walk(ne_ctx* c, uint32_t epoch, uint32_t episode) {
+    NvtxRange range("ne walk");
     uint64_t u0, units;
     episode_range(c, episode, &u0, &units);
     if (c->world > 1 && c->comm) {
@@ -420,7 +462,7 @@ int finish_pool(ne_ctx* c, uint64_t N, bool keyed) {
     c->boff.assign(nb_local(c) + 1, 0);
     NE_CUDA(c, cudaMemcpyAsync(c->boff.data(), c->d_boff, c->boff.size() * sizeof(uint64_t),
                                cudaMemcpyDeviceToHost, c->ws));
-    NE_CUDA(c, cudaStreamSynchronize(c->ws));
+    NE_TRY(wait_stream(c, c->ws));
     return NE_OK;
 }
 
@@ -488,7 +530,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     }
     NE_CUDA(c, cudaMemcpyAsync(c->tmat.data(), c->d_tmat, c->tmat.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                c->ws));
-    NE_CUDA(c, cudaStreamSynchronize(c->ws));
+    NE_TRY(wait_stream(c, c->ws));
     auto M = [&](uint32_t s, uint32_t g) { return c->tmat[(size_t)s * P + g]; };
     uint64_t N = 0, send_max = 0;
     std::vector<uint64_t> recv_off(P + 1, 0);
@@ -561,6 +603,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
 }
 
 int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
+    NvtxRange range("ne pool build");
     if (c->world > 1 && c->cfg.walk_len > 0) return do_build_sharded(c, epoch, episode);
     uint64_t u0, units;
     episode_range(c, episode, &u0, &units);
@@ -786,6 +829,7 @@ int launch_train_staged_ring(ne_ctx* c, uint32_t epoch, uint32_t episode, float 
 // from rank-1 into the other half of the ping-pong buffers.  Everything is
 // enqueued (compute stream + comm stream); finish_train waits for it.
 int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPending& tp) {
+    NvtxRange range("ne train (SGNS + ring)");
     NE_TRY(wait_alias(c));
     NE_CUDA(c, cudaMemsetAsync(c->d_loss, 0, sizeof(double), c->stream));
     if (c->cfg.staging == NE_STAGE_HOST && c->world > 1) return launch_train_staged_ring(c, epoch, episode, lr, tp);
@@ -862,7 +906,7 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
 int finish_train(ne_ctx* c, TrainPending& tp, ne_stats* st) {
     double loss = 0.0;
     NE_CUDA(c, cudaMemcpyAsync(&loss, c->d_loss, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    NE_CUDA(c, cudaStreamSynchronize(c->stream));
+    NE_TRY(wait_stream(c, c->stream));
     if (st) {
         st->samples += tp.samples;
         st->loss_sum += loss;
@@ -912,6 +956,7 @@ int walk_build(ne_ctx* c, uint32_t epoch, uint32_t episode, cudaStream_t s, floa
 // (pool_at) trains on the compute stream: the build uses the two pair buffers
 // the training pool does not occupy and the alternate block-offset array.
 int prebuild_next(ne_ctx* c, uint32_t epoch, uint32_t episode) {
+    NvtxRange range("ne next-episode build (side stream)");
     // stash the current pool
     uint64_t* at = c->pool_at;
     std::vector<uint64_t> boff;
