@@ -535,8 +535,11 @@ static cudaError_t launch_batch(const SgnsParams& p, const Device& dev, cudaStre
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const uint64_t nbatch = (p.count + kBatch - 1) / kBatch;
-    const unsigned grid = p.deterministic ? 1u : (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(
-                                                     nbatch, (uint64_t)std::max(1, dev.sm_count - p.reserve_sms)));
+    // Hogwild: one batch per CTA, at most p.max_warps concurrent batches (the
+    // conflict cap, counted in batches for this rule)
+    const uint64_t full = (uint64_t)std::max(1, dev.sm_count - p.reserve_sms);
+    const unsigned grid = p.deterministic ? 1u : (unsigned)std::max<uint64_t>(
+                                                     1, std::min<uint64_t>({nbatch, full, p.max_warps}));
     kern<<<grid, kBatch, smem, s>>>(p);
     return cudaGetLastError();
 }

@@ -670,6 +670,13 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
     const double cr = (double)std::max<uint64_t>(1, c->c_count);
     const double cap = eps / (kk / cr + 1.0 / vr);
     p.max_warps = cap >= 1e15 ? ~0ull : std::max<uint64_t>(1, (uint64_t)cap);
+    if (c->cfg.update_rule == NE_UPDATE_SHARED_BATCH) {
+        // shared-negative batches: at most eps of the rows touched by concurrent
+        // batches (2B + K' rows each); the cap is counted in batches (CTAs)
+        const double rows = std::min(cr, vr), per = 2.0 * 128 + c->cfg.negatives;
+        const double bcap = eps * rows / per;
+        p.max_warps = bcap >= 1e15 ? ~0ull : std::max<uint64_t>(1, (uint64_t)bcap);
+    }
     p.atomic_writeback = c->cfg.writeback == NE_WB_ATOMIC_DELTA ? 1 : 0;
     p.accumulate = (int)c->cfg.update_rule;
     p.bf16 = c->cfg.storage == NE_STORE_BF16 ? 1 : 0;

@@ -47,7 +47,8 @@ def test_batch_rule_deterministic_matches_oracle(kp, epochs):
         st = eng.train_epoch(ep, 0.025)
         ns, loss = oracle.train_epoch(cfg, off, tgt, V, Cm, ep, 0.025)
         assert st["samples"] == ns
-        assert abs(st["loss_sum"] - loss) <= 1e-4 * abs(loss), (st["loss_sum"], loss)
+        # the loss sums sigma of tf32 logits: each logit is off by up to 2^-10 of its term magnitudes
+        assert abs(st["loss_sum"] - loss) <= 2e-3 * abs(loss), (st["loss_sum"], loss)
     Vg, Cg = eng.embeddings(0), eng.embeddings(1)
     eng.close()
     for got, ref in ((Vg, V), (Cg, Cm)):
