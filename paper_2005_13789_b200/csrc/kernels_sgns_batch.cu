@@ -184,7 +184,7 @@ template <int D, int KP>
 struct BatchSmem {
     static constexpr uint32_t V = 0, Vt = V + kBatch * D * 4, N = Vt + kBatch * D * 4, Nt = N + KP * D * 4,
                               G = Nt + KP * D * 4, Gt = G + kBatch * KP * 4, tail = Gt + kBatch * KP * 4;
-    static constexpr size_t bytes = tail + 16 + 16 + (2 * kBatch + KP) * 4;
+    static constexpr size_t bytes = tail + 16 + 16 + (3 * kBatch + KP) * 4;
 };
 
 }  // namespace
@@ -205,8 +205,9 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
     uint32_t* s_src = tmem_base + 4;
     uint32_t* s_dst = s_src + kBatch;
     uint32_t* s_neg = s_dst + kBatch;
+    float* s_gpos = reinterpret_cast<float*>(s_neg + KP);  // kBatch: x_r, then lr (sigma(x_r) - 1)
 
-    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
                      ::"r"(smem_u32(tmem_base)), "n"(kTmemCols) : "memory");
@@ -273,22 +274,27 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
             issue_S<D, KP>(smem_u32(sV), smem_u32(sN), t_S);
             mma_commit(&bar[0]);
         }
-        // ---- positive term of row i (CUDA cores, overlapping MMA1): x = v . c+
-        // with c+ read from global memory (no shared copy; no C row is written
-        // before every thread has read its c+ twice, see the write-back)
-        float gpos = 0.f;
-        const float* crow = p.C + (uint64_t)((live ? s_dst[i] : p.c_begin) - p.c_begin) * D;
-        if (live) {
+        // ---- positive terms (CUDA cores, overlapping MMA1): x_r = v_r . c+_r,
+        // warp per row, the context row read coalesced from global memory (no
+        // shared copy; no C row is written before every read of it, below)
+        for (uint32_t r = warp; r < nb; r += kBatch / 32) {
+            const float4* crow = reinterpret_cast<const float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D);
             float x = 0.f;
-#pragma unroll 8
-            for (uint32_t c = 0; c < KC; ++c) {
-                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(i, c, D));
-                const float4 cc = __ldcg(reinterpret_cast<const float4*>(crow) + c);
+            for (uint32_t c = lane; c < KC; c += 32) {
+                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, c, D));
+                const float4 cc = __ldcg(crow + c);
                 x = fmaf(v.x, cc.x, fmaf(v.y, cc.y, fmaf(v.z, cc.z, fmaf(v.w, cc.w, x))));
             }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+            if (lane == 0) s_gpos[r] = x;
+        }
+        __syncthreads();
+        float gpos = 0.f;  // lr (sigma(x_i) - 1) of this thread's row
+        if (live) {
             float ex;
-            const float s = sigmoid_clamped(x, ex);
-            gpos = lr * (s - 1.f);
+            const float sp = sigmoid_clamped(s_gpos[i], ex);
+            gpos = lr * (sp - 1.f);
             loss += (double)__logf(1.f + ex);  // -log s
         }
         // ---- epilogue 1: G = lr sigma(S) and G^T (padding rows stay 0)
@@ -325,51 +331,67 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         }
         mbar_wait(&bar[1], phase);
         fence_after();
-        // ---- write-back from the batch-start snapshot.  (1) vertex rows: -(dV +
-        // gpos c+), c+ read again from global (no C row written yet); the
-        // tcgen05.ld are warp-collective: every thread runs them
-        float* vrow = p.V + (uint64_t)((live ? s_src[i] : p.v_begin) - p.v_begin) * D;
+        __syncthreads();
+        s_gpos[i] = gpos;
+        // ---- write-back from the batch-start snapshot; every row update is a
+        // coalesced red.global.add of the delta by a warp.  (1) vertex rows,
+        // -(dV + gpos c+), two halves of 64 rows staged through the G / G^T
+        // tiles (consumed by the products); c+ is read again from global memory
+        // (no C row has been written yet).  tcgen05.ld is warp-collective: a
+        // warp loads its own 32 lanes (rows) or none.
+        float* stage = reinterpret_cast<float*>(sG);  // 64 x D floats (G and G^T are adjacent)
 #pragma unroll 1
-        for (uint32_t d0 = 0; d0 < (uint32_t)D; d0 += 32) {
-            float dv[32];
-            tmem_ld32(t_dV + lane_base + d0, dv);
-            if (!live) continue;
+        for (uint32_t half = 0; half < 2; ++half) {
+            if ((warp >> 1) == half) {
+#pragma unroll 1
+                for (uint32_t d0 = 0; d0 < (uint32_t)D; d0 += 32) {
+                    float dv[32];
+                    tmem_ld32(t_dV + lane_base + d0, dv);
+                    float4* dst = reinterpret_cast<float4*>(stage + (i - 64 * half) * D + d0);
 #pragma unroll
-            for (uint32_t c = 0; c < 8; ++c) {
-                const uint32_t ch = (d0 >> 2) + c;
-                const float4 cc = __ldcg(reinterpret_cast<const float4*>(crow) + ch);
-                atomicAdd(reinterpret_cast<float4*>(vrow) + ch,
-                          make_float4(-(dv[4 * c] + gpos * cc.x), -(dv[4 * c + 1] + gpos * cc.y),
-                                      -(dv[4 * c + 2] + gpos * cc.z), -(dv[4 * c + 3] + gpos * cc.w)));
+                    for (uint32_t c = 0; c < 8; ++c)
+                        dst[c] = make_float4(dv[4 * c], dv[4 * c + 1], dv[4 * c + 2], dv[4 * c + 3]);
+                }
             }
+            fence_before();
+            __syncthreads();
+            for (uint32_t r = 64 * half + warp; r < 64 * half + 64 && r < nb; r += kBatch / 32) {
+                const float g = s_gpos[r];
+                float4* vrow = reinterpret_cast<float4*>(p.V + (uint64_t)(s_src[r] - p.v_begin) * D);
+                const float4* crow = reinterpret_cast<const float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D);
+                for (uint32_t c = lane; c < KC; c += 32) {
+                    const float4 dv = reinterpret_cast<const float4*>(stage + (r - 64 * half) * D)[c];
+                    const float4 cc = __ldcg(crow + c);
+                    atomicAdd(vrow + c, make_float4(-(dv.x + g * cc.x), -(dv.y + g * cc.y), -(dv.z + g * cc.z),
+                                                    -(dv.w + g * cc.w)));
+                }
+            }
+            __syncthreads();
         }
         // (2) the dN^T lanes (= dimensions) into dN rows staged in the G tile
         {
             float dn[32];
             tmem_ld32(t_dNt + lane_base, dn);
-            float* sDN = reinterpret_cast<float*>(sG);  // KP x D, row-major (G is consumed)
 #pragma unroll
-            for (uint32_t e = 0; e < (uint32_t)KP; ++e) sDN[e * D + i] = dn[e];
+            for (uint32_t e = 0; e < (uint32_t)KP; ++e) stage[e * D + i] = dn[e];
         }
         fence_before();
         __syncthreads();  // every c+ read (1) is done before any C row is written
         // (3) positive context rows: -gpos v
-        if (live) {
-            float* cw = p.C + (uint64_t)(s_dst[i] - p.c_begin) * D;
-#pragma unroll 8
-            for (uint32_t c = 0; c < KC; ++c) {
-                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(i, c, D));
-                atomicAdd(reinterpret_cast<float4*>(cw) + c, make_float4(-gpos * v.x, -gpos * v.y, -gpos * v.z,
-                                                                         -gpos * v.w));
+        for (uint32_t r = warp; r < nb; r += kBatch / 32) {
+            const float g = s_gpos[r];
+            float4* cw = reinterpret_cast<float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D);
+            for (uint32_t c = lane; c < KC; c += 32) {
+                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, c, D));
+                atomicAdd(cw + c, make_float4(-g * v.x, -g * v.y, -g * v.z, -g * v.w));
             }
         }
-        // (4) negative rows: -dN, coalesced row reductions
-        const float* sDN = reinterpret_cast<const float*>(sG);
+        // (4) negative rows: -dN
         for (uint32_t j = warp; j < (uint32_t)KP; j += kBatch / 32) {
-            float* nrow = p.C + (uint64_t)(s_neg[j] - p.c_begin) * D;
-            for (uint32_t ch = tid & 31u; ch < KC; ch += 32) {
-                const float4 g = reinterpret_cast<const float4*>(sDN + j * D)[ch];
-                atomicAdd(reinterpret_cast<float4*>(nrow) + ch, make_float4(-g.x, -g.y, -g.z, -g.w));
+            float4* nrow = reinterpret_cast<float4*>(p.C + (uint64_t)(s_neg[j] - p.c_begin) * D);
+            for (uint32_t c = lane; c < KC; c += 32) {
+                const float4 g = reinterpret_cast<const float4*>(stage + j * D)[c];
+                atomicAdd(nrow + c, make_float4(-g.x, -g.y, -g.z, -g.w));
             }
         }
         __syncthreads();
