@@ -11,7 +11,7 @@
 #   ref[:ARGS]            python bench.py --impl reference ARGS
 #   launches[:ARGS]       ncu launch list (gpu__time_duration) of a short bench with ARGS
 #   ncu:WORKLOAD[:ARGS]   ncu --set full of the first SGNS launch of tools/probe.py WORKLOAD ARGS
-#   ncuk:REGEX:WORKLOAD   ncu --set full of the first launch matching REGEX in tools/probe.py WORKLOAD
+#   ncuk:REGEX:WORKLOAD[:ARGS]  ncu --set full of the first launch matching REGEX in tools/probe.py WORKLOAD
 #   py:SCRIPT[:ARGS]      python SCRIPT ARGS
 #   env:VAR=VALUE         export VAR=VALUE for the following steps (env:VAR= unsets it)
 # Every step has its own timeout; logs land in gpurun_out/OUT/.
@@ -54,7 +54,7 @@ for step in "$@"; do
       echo "launches rc=$?" ;;
     ncu|ncuk)
       if [ "$kind" = ncu ]; then RX=sgns; W=${rest%%:*}; a=${rest#*:}; [ "$a" = "$rest" ] && a="";
-      else RX=${rest%%:*}; W=${rest#*:}; a=""; fi
+      else RX=${rest%%:*}; r2=${rest#*:}; W=${r2%%:*}; a=${r2#*:}; [ "$a" = "$r2" ] && a=""; fi
       a=${a//,/ }
       PCMD="python tools/probe.py $W 1 $a"
       timeout 900 $PCMD > "$OUT/probe_${W}_$i.log" 2>&1 && \
