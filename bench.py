@@ -39,7 +39,7 @@ def sgns_kernel_name(d: int, K: int, bf16: bool) -> str:
     red = "bf16x4 red" if bf16 else "red.v4.f32"
     kt = 5 if K == 5 else 0
     if 16 < q <= 24 and K == 5:
-        g, r, shape = 8, 3, "64x5"
+        g, r, shape = 8, 3, "256x1"
     elif q <= 32:
         g, r, shape = 16, (1 if q <= 16 else 2), "256x2"
     else:

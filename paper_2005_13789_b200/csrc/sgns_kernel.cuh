@@ -370,20 +370,20 @@ static cudaError_t launch_sgns_v(const SgnsParams& p, const Device& dev, cudaStr
 // Launch shapes (measured; registers per thread from -Xptxas -v):
 //  * 16 lanes x 2 float4 (d <= 128) and 32 lanes x 2 (d <= 256): 256 threads,
 //    2 CTAs/SM -> <= 128 registers, 16 warps/SM, spill-free;
-//  * 8 lanes x 3 float4 (64 < d <= 96, K = 5): ~187 registers unconstrained;
-//    with 256-thread CTAs only one CTA fits (8 warps, a quarter of the register
-//    file idle), 64-thread CTAs pack 10 warps per SM with no spills (knob
-//    NE_SGNS_G8SHAPE: 0 = 64 x 5, 1 = 128 x 3 (<= 168 registers), 2 = 256 x 1);
+//  * 8 lanes x 3 float4 (64 < d <= 96, K = 5): ~189 registers unconstrained,
+//    256-thread CTAs, one per SM (8 warps).  Packing more warps per SM with
+//    smaller CTAs (knob NE_SGNS_G8SHAPE: 1 = 64 x 5 -> 160 registers, 12
+//    warps; 2 = 128 x 3) measured slower on C4: 902 / 906 vs 970 M samples/s;
 //  * 32 lanes x 3-4 float4 (d > 256): 200-245 registers, 64-thread CTAs.
 template <int G, int R, int KT, bool BF>
 static cudaError_t launch_sgns_k(const SgnsParams& p, const Device& dev, cudaStream_t s) {
     if constexpr (G == 8) {
         static const int shape = env_int("NE_SGNS_G8SHAPE", 0);
         if constexpr (!BF) {
-            if (shape == 1) return launch_sgns_v<G, R, KT, Shape<128, 3>, BF>(p, dev, s);
-            if (shape == 2) return launch_sgns_v<G, R, KT, Shape<256, 1>, BF>(p, dev, s);
+            if (shape == 1) return launch_sgns_v<G, R, KT, Shape<64, 5>, BF>(p, dev, s);
+            if (shape == 2) return launch_sgns_v<G, R, KT, Shape<128, 3>, BF>(p, dev, s);
         }
-        return launch_sgns_v<G, R, KT, Shape<64, 5>, BF>(p, dev, s);
+        return launch_sgns_v<G, R, KT, Shape<256, 1>, BF>(p, dev, s);
     } else if constexpr (R > 2) {
         return launch_sgns_v<G, R, KT, Shape<64, 1>, BF>(p, dev, s);
     } else {
