@@ -1,8 +1,10 @@
-"""Multi-process (world size 2 and 3, gloo, CPU) check of the ring's host
-logic: every rank follows the library's schedule (ne_plan_vsub,
-ne_partition_bounds from libne_b200.so, no GPU needed), trains its block with
-the oracle's single-sample update, and ships the trained vertex sub-part to
-rank g+1 while receiving the next from rank g-1 (torch.distributed send/recv).
+"""Multi-process (world size 2, 3 and 4 with two groups, gloo, CPU) check of
+the ring's host logic: every rank follows the library's schedule
+(ne_plan_vsub2, ne_ring_peers, ne_partition_bounds from libne_b200.so, no GPU
+needed), trains its block with the oracle's single-sample update, and ships
+the trained vertex sub-part to the library's ring destination while receiving
+the next from its ring source (torch.distributed send/recv) -- g+1 / g-1 on
+one ring, the group ring or the next group with NEXT-3 groups.
 The gathered result must be bit-identical to the oracle's sequential replay of
 the P-part plan (P:89 orthogonality, S:383 sequential equivalence)."""
 import os
@@ -23,7 +25,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, groups, port, q):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import oracle
@@ -37,7 +39,7 @@ def _worker(rank, world, port, q):
         n, d, k = 260, 8, 2
         off, tgt = synth.rmat_graph(n, 1500, 13)
         cfg = oracle.Config(dim=d, negatives=3, walk_len=6, window=2, walks_per_node=1, episodes=2,
-                            subparts=k, parts=world, seed=42)
+                            subparts=k, parts=world, seed=42, groups=groups)
         # NCCL-id bootstrap path of bench.py / the harness, over gloo
         obj = [bytes(range(128)) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -56,7 +58,7 @@ def _worker(rank, world, port, q):
             pairs, boff = oracle.build_episode(cfg, off, tgt, 0, e)
             for r in range(world):
                 for t in range(k):
-                    vs = ne.ne_plan_vsub(world, k, r, t, rank)
+                    vs = ne.ne_plan_vsub2(world, groups, k, r, t, rank)
                     have, rows = slots[t]
                     assert have == vs, (rank, r, t, have, vs)
                     Vfull = np.zeros((n, d), np.float32)
@@ -67,11 +69,12 @@ def _worker(rank, world, port, q):
                         negs = oracle.negatives(cfg, thr, al, cb, cn, 0, e, B, p)
                         oracle.train_sample(Vfull, Cm, int(s), int(dd), negs, 0.05)
                     rows = Vfull[sb[vs]:sb[vs + 1]].copy()
-                    # ring: send to g+1, receive the next sub-part from g-1
-                    nxt = ne.ne_plan_vsub(world, k, r + 1, t, rank)
+                    # ring: send to the library's destination, receive from its source
+                    nxt = ne.ne_plan_vsub2(world, groups, k, r + 1, t, rank)
+                    dest, src = ne.ne_ring_peers(world, groups, r, rank)
                     out = torch.from_numpy(rows)
                     inc = torch.zeros((int(sb[nxt + 1] - sb[nxt]), d), dtype=torch.float32)
-                    reqs = [dist.isend(out, (rank + 1) % world), dist.irecv(inc, (rank - 1) % world)]
+                    reqs = [dist.isend(out, dest), dist.irecv(inc, src)]
                     for rq in reqs:
                         rq.wait()
                     slots[t] = (nxt, inc.numpy().copy())
@@ -81,13 +84,13 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_ring_host_logic_matches_oracle(world, orc):
+@pytest.mark.parametrize("world,groups", [(2, 1), (3, 1), (4, 2)])
+def test_ring_host_logic_matches_oracle(world, groups, orc):
     import synth
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, groups, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=300) for _ in range(world)]
@@ -97,7 +100,7 @@ def test_ring_host_logic_matches_oracle(world, orc):
     n, d, k = 260, 8, 2
     off, tgt = synth.rmat_graph(n, 1500, 13)
     cfg = orc.Config(dim=d, negatives=3, walk_len=6, window=2, walks_per_node=1, episodes=2,
-                     subparts=k, parts=world, seed=42)
+                     subparts=k, parts=world, seed=42, groups=groups)
     V = orc.init_vertex(n, d, 42)
     Cm = np.zeros_like(V)
     orc.train_epoch(cfg, off, tgt, V, Cm, 0, 0.05)
