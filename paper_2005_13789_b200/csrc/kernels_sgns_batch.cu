@@ -277,17 +277,26 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         // ---- positive terms (CUDA cores, overlapping MMA1): x_r = v_r . c+_r,
         // warp per row, the context row read coalesced from global memory (no
         // shared copy; no C row is written before every read of it, below)
-        for (uint32_t r = warp; r < nb; r += kBatch / 32) {
-            const float4* crow = reinterpret_cast<const float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D);
-            float x = 0.f;
-            for (uint32_t c = lane; c < KC; c += 32) {
-                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, c, D));
-                const float4 cc = __ldcg(crow + c);
-                x = fmaf(v.x, cc.x, fmaf(v.y, cc.y, fmaf(v.z, cc.z, fmaf(v.w, cc.w, x))));
+        // (rows in groups of 8 per warp: 8 independent row loads in flight per lane)
+        static_assert(KC == 32, "one float4 of a row per lane");
+        for (uint32_t r0 = warp * 8; r0 < nb; r0 += kBatch / 4) {
+            float4 cc[8];
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                const uint32_t r = r0 + u;
+                cc[u] = r < nb ? __ldcg(reinterpret_cast<const float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D) +
+                                        lane)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
-            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
-            if (lane == 0) s_gpos[r] = x;
+            for (uint32_t u = 0; u < 8; ++u) {
+                const uint32_t r = r0 + u;
+                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, lane, D));
+                float x = fmaf(v.x, cc[u].x, fmaf(v.y, cc[u].y, fmaf(v.z, cc[u].z, v.w * cc[u].w)));
+#pragma unroll
+                for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+                if (lane == 0 && r < nb) s_gpos[r] = x;
+            }
         }
         __syncthreads();
         float gpos = 0.f;  // lr (sigma(x_i) - 1) of this thread's row
@@ -355,15 +364,24 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
             }
             fence_before();
             __syncthreads();
-            for (uint32_t r = 64 * half + warp; r < 64 * half + 64 && r < nb; r += kBatch / 32) {
-                const float g = s_gpos[r];
-                float4* vrow = reinterpret_cast<float4*>(p.V + (uint64_t)(s_src[r] - p.v_begin) * D);
-                const float4* crow = reinterpret_cast<const float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D);
-                for (uint32_t c = lane; c < KC; c += 32) {
-                    const float4 dv = reinterpret_cast<const float4*>(stage + (r - 64 * half) * D)[c];
-                    const float4 cc = __ldcg(crow + c);
-                    atomicAdd(vrow + c, make_float4(-(dv.x + g * cc.x), -(dv.y + g * cc.y), -(dv.z + g * cc.z),
-                                                    -(dv.w + g * cc.w)));
+            for (uint32_t r0 = 64 * half + warp * 8; r0 < 64 * half + 64 && r0 < nb; r0 += kBatch / 4) {
+                float4 cc[8];
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) {
+                    const uint32_t r = r0 + u;
+                    cc[u] = r < nb ? __ldcg(reinterpret_cast<const float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D) +
+                                            lane)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < 8; ++u) {
+                    const uint32_t r = r0 + u;
+                    if (r >= nb) break;
+                    const float g = s_gpos[r];
+                    const float4 dv = reinterpret_cast<const float4*>(stage + (r - 64 * half) * D)[lane];
+                    atomicAdd(reinterpret_cast<float4*>(p.V + (uint64_t)(s_src[r] - p.v_begin) * D) + lane,
+                              make_float4(-(dv.x + g * cc[u].x), -(dv.y + g * cc[u].y), -(dv.z + g * cc[u].z),
+                                          -(dv.w + g * cc[u].w)));
                 }
             }
             __syncthreads();
