@@ -233,24 +233,35 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
     constexpr uint32_t KC = D / 4;
     double loss = 0.0;
     uint32_t phase = 0;
+    // ids of batch b: this thread's pair; threads j < KP draw shared negative j
+    // (Philox + the alias entry; the coin is taken when the id is stored)
+    uint2 nx_pr = make_uint2(0, 0), nx_ta = make_uint2(0, 0);
+    uint32_t nx_col = 0, nx_coin = 0;
+    auto fetch_ids = [&](uint64_t b) {
+        if (b >= nbatch) return;
+        const uint64_t q = b * kBatch + i;
+        if (q < p.count) nx_pr = p.pool[q];
+        if (i < (uint32_t)KP) {
+            const uint4 x = philox(make_uint4((uint32_t)b, (uint32_t)(b >> 32), (p.episode << 20) | (p.block << 8) | i,
+                                              tagw), key);
+            nx_col = (uint32_t)uniform_index(x.x, x.y, p.c_count);
+            nx_coin = x.z;
+            nx_ta = __ldg(p.alias + nx_col);
+        }
+    };
+    fetch_ids(blockIdx.x);
 
     for (uint64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
         const uint64_t p0 = b * kBatch;
         const uint32_t nb = (uint32_t)(p.count - p0 < (uint64_t)kBatch ? p.count - p0 : (uint64_t)kBatch);
         const bool live = i < nb;
-        // ---- ids: pairs, shared negatives (O8 with the batch counter, tag BNEG)
+        // ---- ids: pairs, shared negatives (O8 with the batch counter, tag BNEG),
+        // fetched during the previous batch's write-back (fetch_ids below)
         if (live) {
-            const uint2 pr = p.pool[p0 + i];
-            s_src[i] = pr.x;
-            s_dst[i] = pr.y;
+            s_src[i] = nx_pr.x;
+            s_dst[i] = nx_pr.y;
         }
-        if (i < (uint32_t)KP) {
-            const uint4 x = philox(make_uint4((uint32_t)b, (uint32_t)(b >> 32), (p.episode << 20) | (p.block << 8) | i,
-                                              tagw), key);
-            const uint32_t col = (uint32_t)uniform_index(x.x, x.y, p.c_count);
-            const uint2 ta = __ldg(p.alias + col);
-            s_neg[i] = (uint32_t)(p.c_begin + (x.z < ta.x ? col : ta.y));
-        }
+        if (i < (uint32_t)KP) s_neg[i] = (uint32_t)(p.c_begin + (nx_coin < nx_ta.x ? nx_col : nx_ta.y));
         __syncthreads();
         // ---- gather V and N rows (cp.async, 16 B per lane; a warp covers 8 rows
         // x 4 chunks so each quarter-warp writes 128 contiguous bytes)
@@ -342,6 +353,7 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         fence_after();
         __syncthreads();
         s_gpos[i] = gpos;
+        fetch_ids(b + gridDim.x);  // the next batch's ids load while this one is written back
         // ---- write-back from the batch-start snapshot; every row update is a
         // coalesced red.global.add of the delta by a warp.  (1) vertex rows,
         // -(dV + gpos c+), two halves of 64 rows staged through the G / G^T
