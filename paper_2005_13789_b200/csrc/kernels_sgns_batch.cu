@@ -167,8 +167,12 @@ __device__ __forceinline__ void issue_dNt(uint32_t sVt, uint32_t sGt, uint32_t t
 // as one 16-byte chunk of the destination row.
 template <uint32_t R, uint32_t C>
 __device__ __forceinline__ void transpose_tile(const unsigned char* src, unsigned char* dst, uint32_t tid) {
+    static_assert(R % 16 == 0 && C % 8 == 0, "a warp covers 8 columns x 4 row chunks");
     for (uint32_t f = tid; f < R / 4 * C; f += kBatch) {
-        const uint32_t col = f % C, r4 = f / C;  // destination row col, chunk r4 (source rows 4 r4 .. 4 r4 + 3)
+        // a warp covers 8 consecutive columns x 4 consecutive row chunks: 4-way
+        // bank conflicts on the gathers (32 lanes in one column would be 8-way)
+        const uint32_t l = f & 31u, grp = f >> 5, cgroups = C / 8;
+        const uint32_t col = (grp % cgroups) * 8 + (l & 7u), r4 = (grp / cgroups) * 4 + (l >> 3);
         float4 v;
         float* vp = &v.x;
 #pragma unroll
