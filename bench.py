@@ -340,7 +340,9 @@ def main():
     if os.path.exists(prof):
         with open(prof) as f:
             tr = json.load(f).get(args.workload)
-        per_sample = (tr or {}).get("dram_bytes_per_sample" if esz == 4 else "bf16_dram_bytes_per_sample")
+        key = ("batch_dram_bytes_per_sample" if args.rule == "batch" else
+               "dram_bytes_per_sample" if esz == 4 else "bf16_dram_bytes_per_sample")
+        per_sample = (tr or {}).get(key)
         if per_sample and train_launches:
             # captured DRAM bytes per sample x this run's samples per SGNS launch (this rank)
             traffic = per_sample * samples / train_launches
