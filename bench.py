@@ -236,8 +236,10 @@ def main():
     ap.add_argument("--rule", default="sequential", choices=["sequential", "accumulated", "batch"],
                     help="update rule: Alg. 1 sequential (the headline), accumulated (word2vec), or batch "
                          "(NEXT-4 shared negatives: 128-sample batches share 32 negatives, tcgen05 tf32)")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
-                    help="ring transport at N > 1: NCCL send/recv kernels, or copy-engine pushes over CUDA IPC")
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "ipc"],
+                    help="ring transport at N > 1: NCCL send/recv kernels, or copy-engine pushes over CUDA IPC; "
+                         "auto = ipc (measured faster at every N and workload, profiles/r02_bench_*_ipc_*), "
+                         "nccl with --staging host (the staged ring runs over NCCL)")
     ap.add_argument("--groups", type=int, default=1, help="NEXT-3 two-level ring: groups of N/groups ranks")
     ap.add_argument("--storage", default="f32", choices=["f32", "bf16"],
                     help="row storage: f32 (the paper's, the headline) or bf16 (NEXT-4 option, reading D16)")
@@ -274,6 +276,8 @@ def main():
     # transfers, left on the library's comm stream, into it)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
+    if args.transport == "auto":
+        args.transport = "nccl" if args.staging == "host" else "ipc"
     rule = {"sequential": ne.NE_UPDATE_SEQUENTIAL, "accumulated": ne.NE_UPDATE_ACCUMULATED,
             "batch": ne.NE_UPDATE_SHARED_BATCH}[args.rule]
     negatives = 32 if args.rule == "batch" else w.negatives

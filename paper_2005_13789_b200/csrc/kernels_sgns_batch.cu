@@ -118,13 +118,33 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 consecutive TMEM columns of this thread's lane (32x32b shape, x16).
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
 // Byte offset of (row, 4-float chunk) in a no-swizzle tile with `cols` columns.
-__device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t chunk, uint32_t cols) {
-    return ((row >> 3) * (cols >> 2) + chunk) * 128u + (row & 7u) * 16u;
+// Byte offset of (row, 4-float chunk) in a no-swizzle tile with `cols` columns
+// whose K-adjacent core matrices are `lbo` bytes apart (LBO; SBO = cols / 4 *
+// lbo).  lbo = 128 packs the core matrices; kLboPad = 144 leaves 16 bytes
+// after each, so the 32 chunks of one row fall in 32 different banks (a warp
+// reading a row, lane = chunk, is conflict-free instead of 8-way).
+constexpr uint32_t kLboPad = 144;
+__device__ __forceinline__ uint32_t tile_off(uint32_t row, uint32_t chunk, uint32_t cols, uint32_t lbo = 128u) {
+    return ((row >> 3) * (cols >> 2) + chunk) * lbo + (row & 7u) * 16u;
 }
 
 __device__ __forceinline__ float sigmoid_clamped(float x, float& ex) {
@@ -142,7 +162,8 @@ __device__ __forceinline__ void issue_S(uint32_t sV, uint32_t sN, uint32_t t_S) 
     constexpr uint32_t idesc = idesc_tf32(kBatch, KP, false, false);
 #pragma unroll
     for (uint32_t ks = 0; ks < D / 8; ++ks)
-        mma_tf32(t_S, umma_desc(sV + ks * 256u, 128u, D * 32u), umma_desc(sN + ks * 256u, 128u, D * 32u), idesc,
+        mma_tf32(t_S, umma_desc(sV + ks * 2u * kLboPad, kLboPad, D / 4 * kLboPad),
+                 umma_desc(sN + ks * 2u * kLboPad, kLboPad, D / 4 * kLboPad), idesc,
                  ks > 0);
 }
 template <int D, int KP>
@@ -158,17 +179,18 @@ __device__ __forceinline__ void issue_dNt(uint32_t sVt, uint32_t sGt, uint32_t t
     constexpr uint32_t idesc = idesc_tf32(D, KP, false, false);
 #pragma unroll
     for (uint32_t ks = 0; ks < (uint32_t)kBatch / 8; ++ks)
-        mma_tf32(t_dNt, umma_desc(sVt + ks * 256u, 128u, kBatch * 32u), umma_desc(sGt + ks * 256u, 128u, kBatch * 32u),
+        mma_tf32(t_dNt, umma_desc(sVt + ks * 256u, 128u, kBatch * 32u),
+                 umma_desc(sGt + ks * 2u * kLboPad, kLboPad, kBatch / 4 * kLboPad),
                  idesc, ks > 0);
 }
 
 // dst = src^T between two tiles (src: R rows x C cols, dst: C rows x R cols):
 // every thread gathers 4 consecutive source rows of one column and stores them
 // as one 16-byte chunk of the destination row.
-template <uint32_t R, uint32_t C>
+template <uint32_t R, uint32_t C, uint32_t NT = kBatch, uint32_t SL = kLboPad, uint32_t DL = 128u>
 __device__ __forceinline__ void transpose_tile(const unsigned char* src, unsigned char* dst, uint32_t tid) {
     static_assert(R % 16 == 0 && C % 8 == 0, "a warp covers 8 columns x 4 row chunks");
-    for (uint32_t f = tid; f < R / 4 * C; f += kBatch) {
+    for (uint32_t f = tid; f < R / 4 * C; f += NT) {
         // a warp covers 8 consecutive columns x 4 consecutive row chunks: 4-way
         // bank conflicts on the gathers (32 lanes in one column would be 8-way)
         const uint32_t l = f & 31u, grp = f >> 5, cgroups = C / 8;
@@ -177,8 +199,8 @@ __device__ __forceinline__ void transpose_tile(const unsigned char* src, unsigne
         float* vp = &v.x;
 #pragma unroll
         for (uint32_t e = 0; e < 4; ++e)
-            vp[e] = *reinterpret_cast<const float*>(src + tile_off(4 * r4 + e, col >> 2, C) + (col & 3u) * 4u);
-        *reinterpret_cast<float4*>(dst + tile_off(col, r4, R)) = v;
+            vp[e] = *reinterpret_cast<const float*>(src + tile_off(4 * r4 + e, col >> 2, C, SL) + (col & 3u) * 4u);
+        *reinterpret_cast<float4*>(dst + tile_off(col, r4, R, DL)) = v;
     }
 }
 
@@ -186,20 +208,28 @@ __device__ __forceinline__ void transpose_tile(const unsigned char* src, unsigne
 // N^T (D x KP), G (B x KP), G^T (KP x B), then barriers, TMEM address, ids.
 template <int D, int KP>
 struct BatchSmem {
-    static constexpr uint32_t V = 0, Vt = V + kBatch * D * 4, N = Vt + kBatch * D * 4, Nt = N + KP * D * 4,
-                              G = Nt + KP * D * 4, Gt = G + kBatch * KP * 4, tail = Gt + kBatch * KP * 4;
+    // V, N and G^T with padded core matrices (kLboPad): rows read by a warp
+    static constexpr uint32_t V = 0, Vt = V + kBatch / 8 * (D / 4) * kLboPad, N = Vt + kBatch * D * 4,
+                              Nt = N + KP / 8 * (D / 4) * kLboPad, G = Nt + KP * D * 4, Gt = G + kBatch * KP * 4,
+                              tail = Gt + KP / 8 * (kBatch / 4) * kLboPad;
+    static_assert(tail - G >= 64 * D * 4, "the dV write-back stages 64 rows in G, G^T");
     static constexpr size_t bytes = tail + 16 + 16 + (3 * kBatch + KP) * 4;
 };
 
 }  // namespace
 
 // D: embedding dimension (UMMA M of the dN^T product: 128); KP: shared
-// negatives per batch (UMMA N of S and dN^T).
+// negatives per batch (UMMA N of S and dN^T).  256 threads: batch row i is
+// TMEM lane i of warps i / 32 and 4 + i / 32 (a warp reaches only its own
+// 32-lane quarter of TMEM), which split the columns of every TMEM read; the
+// gathers, transposes, dot products and write-backs stride over all 8 warps.
+constexpr uint32_t kBatchThreads = 256;
 template <int D, int KP>
-__global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
+__global__ void __launch_bounds__(kBatchThreads, 1) sgns_batch_kernel(SgnsParams p) {
     static_assert(D == 128, "the dN^T product has M = d: 128");
     static_assert(KP == 32, "K' = 32 (both orientations of V, N, G: 192 KB of shared memory)");
     using SM = BatchSmem<D, KP>;
+    constexpr uint32_t NT = kBatchThreads, NW = NT / 32;
     constexpr uint32_t kTmemCols = 256;  // S: KP, dV: D, dN^T: KP
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char *sV = smem + SM::V, *sVt = smem + SM::Vt, *sN = smem + SM::N, *sNt = smem + SM::Nt,
@@ -227,22 +257,23 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
     fence_after();
     const uint32_t tmem = *tmem_base;
     const uint32_t t_S = tmem, t_dV = tmem + KP, t_dNt = tmem + KP + D;
-    const uint32_t lane_base = (warp * 32u) << 16;  // this warp's TMEM lanes
+    const uint32_t i = tid & (kBatch - 1u);     // batch row (TMEM lane) of this thread
+    const uint32_t hi = tid / kBatch;           // 0: warps 0-3, 1: warps 4-7 (column half)
+    const uint32_t lane_base = ((warp & 3u) * 32u) << 16;  // this warp's TMEM lanes
 
     const uint2 key = key_of(p.seed);
     const uint32_t tagw = tag_word(kTagBNeg, p.epoch);
     const float lr = p.lr;
     const uint64_t nbatch = (p.count + kBatch - 1) / kBatch;
-    const uint32_t i = tid;  // batch row of this thread
     constexpr uint32_t KC = D / 4;
     double loss = 0.0;
     uint32_t phase = 0;
-    // ids of batch b: this thread's pair; threads j < KP draw shared negative j
-    // (Philox + the alias entry; the coin is taken when the id is stored)
+    // ids of batch b: thread i < 128 holds pair i; threads j < KP draw shared
+    // negative j (Philox + the alias entry; the coin is taken when the id is stored)
     uint2 nx_pr = make_uint2(0, 0), nx_ta = make_uint2(0, 0);
     uint32_t nx_col = 0, nx_coin = 0;
     auto fetch_ids = [&](uint64_t b) {
-        if (b >= nbatch) return;
+        if (b >= nbatch || hi) return;
         const uint64_t q = b * kBatch + i;
         if (q < p.count) nx_pr = p.pool[q];
         if (i < (uint32_t)KP) {
@@ -261,26 +292,28 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         const bool live = i < nb;
         // ---- ids: pairs, shared negatives (O8 with the batch counter, tag BNEG),
         // fetched during the previous batch's write-back (fetch_ids below)
-        if (live) {
-            s_src[i] = nx_pr.x;
-            s_dst[i] = nx_pr.y;
+        if (!hi) {
+            if (live) {
+                s_src[i] = nx_pr.x;
+                s_dst[i] = nx_pr.y;
+            }
+            if (i < (uint32_t)KP) s_neg[i] = (uint32_t)(p.c_begin + (nx_coin < nx_ta.x ? nx_col : nx_ta.y));
         }
-        if (i < (uint32_t)KP) s_neg[i] = (uint32_t)(p.c_begin + (nx_coin < nx_ta.x ? nx_col : nx_ta.y));
         __syncthreads();
         // ---- gather V and N rows (cp.async, 16 B per lane; a warp covers 8 rows
         // x 4 chunks so each quarter-warp writes 128 contiguous bytes)
-        for (uint32_t f = tid; f < kBatch * KC; f += kBatch) {
+        for (uint32_t f = tid; f < kBatch * KC; f += NT) {
             const uint32_t q = f >> 5, l = f & 31u;
             const uint32_t row = (q / (KC / 4)) * 8 + (l & 7u), chunk = (q % (KC / 4)) * 4 + (l >> 3);
-            const uint32_t off = tile_off(row, chunk, D);
+            const uint32_t off = tile_off(row, chunk, D, kLboPad);
             if (row < nb) cp_async16(sV + off, p.V + (uint64_t)(s_src[row] - p.v_begin) * D + chunk * 4);
             else *reinterpret_cast<float4*>(sV + off) = make_float4(0.f, 0.f, 0.f, 0.f);
             if (row < (uint32_t)KP) cp_async16(sN + off, p.C + (uint64_t)(s_neg[row] - p.c_begin) * D + chunk * 4);
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
-        transpose_tile<kBatch, D>(sV, sVt, tid);
-        transpose_tile<KP, D>(sN, sNt, tid);
+        transpose_tile<kBatch, D, NT>(sV, sVt, tid);
+        transpose_tile<KP, D, NT>(sN, sNt, tid);
         fence_async_smem();
         __syncthreads();
         // ---- MMA1: S = V N^T
@@ -294,7 +327,7 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         // shared copy; no C row is written before every read of it, below)
         // (rows in groups of 8 per warp: 8 independent row loads in flight per lane)
         static_assert(KC == 32, "one float4 of a row per lane");
-        for (uint32_t r0 = warp * 8; r0 < nb; r0 += kBatch / 4) {
+        for (uint32_t r0 = warp * 8; r0 < nb; r0 += NW * 8) {
             float4 cc[8];
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
@@ -306,7 +339,7 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
                 const uint32_t r = r0 + u;
-                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, lane, D));
+                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, lane, D, kLboPad));
                 float x = fmaf(v.x, cc[u].x, fmaf(v.y, cc[u].y, fmaf(v.z, cc[u].z, v.w * cc[u].w)));
 #pragma unroll
                 for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
@@ -319,16 +352,19 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
             float ex;
             const float sp = sigmoid_clamped(s_gpos[i], ex);
             gpos = lr * (sp - 1.f);
-            loss += (double)__logf(1.f + ex);  // -log s
+            if (!hi) loss += (double)__logf(1.f + ex);  // -log s
         }
-        // ---- epilogue 1: G = lr sigma(S) and G^T (padding rows stay 0)
+        // ---- epilogue 1: G = lr sigma(S) and G^T (padding rows stay 0); the
+        // two warps of a lane quarter take 16 columns each
         mbar_wait(&bar[0], phase);
         fence_after();
         {
-            float sv[32];
-            tmem_ld32(t_S + lane_base, sv);
+            constexpr uint32_t HC = KP / 2;
+            float sv[HC];
+            tmem_ld16(t_S + lane_base + hi * HC, sv);
+            float part = 0.f;
 #pragma unroll
-            for (uint32_t c = 0; c < KP / 4; ++c) {
+            for (uint32_t c = 0; c < HC / 4; ++c) {
                 float4 g;
                 float* gp = &g.x;
 #pragma unroll
@@ -337,11 +373,14 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
                     const float xcl = fminf(fmaxf(sv[c * 4 + e], -30.f), 30.f);
                     const float s = sigmoid_clamped(sv[c * 4 + e], ex);
                     gp[e] = live ? lr * s : 0.f;
-                    if (live) loss += (double)(__logf(1.f + ex) + xcl);  // -log(1 - s)
-                    *reinterpret_cast<float*>(sGt + tile_off(c * 4 + e, i >> 2, kBatch) + (i & 3u) * 4u) = gp[e];
+                    if (live) part += __logf(1.f + ex) + xcl;  // -log(1 - s)
+                    *reinterpret_cast<float*>(sGt + tile_off(hi * HC + c * 4 + e, i >> 2, kBatch, kLboPad) +
+                                              (i & 3u) * 4u) =
+                        gp[e];
                 }
-                *reinterpret_cast<float4*>(sG + tile_off(i, c, KP)) = g;
+                *reinterpret_cast<float4*>(sG + tile_off(i, hi * (HC / 4) + c, KP)) = g;
             }
+            loss += (double)part;
         }
         fence_async_smem();
         fence_before();
@@ -356,31 +395,35 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         mbar_wait(&bar[1], phase);
         fence_after();
         __syncthreads();
-        s_gpos[i] = gpos;
+        if (!hi) s_gpos[i] = gpos;
         fetch_ids(b + gridDim.x);  // the next batch's ids load while this one is written back
         // ---- write-back from the batch-start snapshot; every row update is a
         // coalesced red.global.add of the delta by a warp.  (1) vertex rows,
         // -(dV + gpos c+), two halves of 64 rows staged through the G / G^T
         // tiles (consumed by the products); c+ is read again from global memory
-        // (no C row has been written yet).  tcgen05.ld is warp-collective: a
-        // warp loads its own 32 lanes (rows) or none.
+        // (no C row has been written yet).  tcgen05.ld is warp-collective: the
+        // two warps of a lane quarter load 64 columns each of their 32 rows.
         float* stage = reinterpret_cast<float*>(sG);  // 64 x D floats (G and G^T are adjacent)
 #pragma unroll 1
         for (uint32_t half = 0; half < 2; ++half) {
-            if ((warp >> 1) == half) {
+            if (((warp & 3u) >> 1) == half) {
 #pragma unroll 1
-                for (uint32_t d0 = 0; d0 < (uint32_t)D; d0 += 32) {
+                for (uint32_t d0 = hi * (D / 2); d0 < (hi + 1) * (D / 2); d0 += 32) {
                     float dv[32];
                     tmem_ld32(t_dV + lane_base + d0, dv);
-                    float4* dst = reinterpret_cast<float4*>(stage + (i - 64 * half) * D + d0);
+                    // chunk ch of staged row sr at ch ^ (sr % 8): the 8 rows of a
+                    // quarter-warp store to 8 different bank groups
+                    const uint32_t sr = i - 64 * half;
+                    float4* dst = reinterpret_cast<float4*>(stage + sr * D);
 #pragma unroll
                     for (uint32_t c = 0; c < 8; ++c)
-                        dst[c] = make_float4(dv[4 * c], dv[4 * c + 1], dv[4 * c + 2], dv[4 * c + 3]);
+                        dst[(d0 / 4 + c) ^ (sr & 7u)] = make_float4(dv[4 * c], dv[4 * c + 1], dv[4 * c + 2], dv[4 * c + 3]);
                 }
             }
             fence_before();
             __syncthreads();
-            for (uint32_t r0 = 64 * half + warp * 8; r0 < 64 * half + 64 && r0 < nb; r0 += kBatch / 4) {
+            {
+                const uint32_t r0 = 64 * half + warp * 8;  // 8 warps x 8 rows = the half
                 float4 cc[8];
 #pragma unroll
                 for (uint32_t u = 0; u < 8; ++u) {
@@ -394,7 +437,7 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
                     const uint32_t r = r0 + u;
                     if (r >= nb) break;
                     const float g = s_gpos[r];
-                    const float4 dv = reinterpret_cast<const float4*>(stage + (r - 64 * half) * D)[lane];
+                    const float4 dv = reinterpret_cast<const float4*>(stage + (r - 64 * half) * D)[lane ^ (r & 7u)];
                     atomicAdd(reinterpret_cast<float4*>(p.V + (uint64_t)(s_src[r] - p.v_begin) * D) + lane,
                               make_float4(-(dv.x + g * cc[u].x), -(dv.y + g * cc[u].y), -(dv.z + g * cc[u].z),
                                           -(dv.w + g * cc[u].w)));
@@ -404,24 +447,24 @@ __global__ void __launch_bounds__(kBatch, 1) sgns_batch_kernel(SgnsParams p) {
         }
         // (2) the dN^T lanes (= dimensions) into dN rows staged in the G tile
         {
-            float dn[32];
-            tmem_ld32(t_dNt + lane_base, dn);
+            float dn[16];
+            tmem_ld16(t_dNt + lane_base + hi * (KP / 2), dn);
 #pragma unroll
-            for (uint32_t e = 0; e < (uint32_t)KP; ++e) stage[e * D + i] = dn[e];
+            for (uint32_t e = 0; e < (uint32_t)KP / 2; ++e) stage[(hi * (KP / 2) + e) * D + i] = dn[e];
         }
         fence_before();
         __syncthreads();  // every c+ read (1) is done before any C row is written
         // (3) positive context rows: -gpos v
-        for (uint32_t r = warp; r < nb; r += kBatch / 32) {
+        for (uint32_t r = warp; r < nb; r += NW) {
             const float g = s_gpos[r];
             float4* cw = reinterpret_cast<float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D);
             for (uint32_t c = lane; c < KC; c += 32) {
-                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, c, D));
+                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, c, D, kLboPad));
                 atomicAdd(cw + c, make_float4(-g * v.x, -g * v.y, -g * v.z, -g * v.w));
             }
         }
         // (4) negative rows: -dN
-        for (uint32_t j = warp; j < (uint32_t)KP; j += kBatch / 32) {
+        for (uint32_t j = warp; j < (uint32_t)KP; j += NW) {
             float4* nrow = reinterpret_cast<float4*>(p.C + (uint64_t)(s_neg[j] - p.c_begin) * D);
             for (uint32_t c = lane; c < KC; c += 32) {
                 const float4 g = reinterpret_cast<const float4*>(stage + j * D)[c];
@@ -464,17 +507,17 @@ __global__ void __launch_bounds__(kBatch, 1) umma_products_kernel(const float* _
     }
     for (uint32_t r = 0; r < kBatch; ++r)
         for (uint32_t c = tid; c < D / 4; c += kBatch)
-            *reinterpret_cast<float4*>(sV + tile_off(r, c, D)) = reinterpret_cast<const float4*>(V + r * D)[c];
+            *reinterpret_cast<float4*>(sV + tile_off(r, c, D, kLboPad)) = reinterpret_cast<const float4*>(V + r * D)[c];
     for (uint32_t r = 0; r < (uint32_t)KP; ++r)
         for (uint32_t c = tid; c < D / 4; c += kBatch)
-            *reinterpret_cast<float4*>(sN + tile_off(r, c, D)) = reinterpret_cast<const float4*>(N + r * D)[c];
+            *reinterpret_cast<float4*>(sN + tile_off(r, c, D, kLboPad)) = reinterpret_cast<const float4*>(N + r * D)[c];
     for (uint32_t r = 0; r < kBatch; ++r)
         for (uint32_t c = tid; c < KP / 4; c += kBatch)
             *reinterpret_cast<float4*>(sG + tile_off(r, c, KP)) = reinterpret_cast<const float4*>(G + r * KP)[c];
     __syncthreads();
     transpose_tile<kBatch, D>(sV, sVt, tid);
     transpose_tile<KP, D>(sN, sNt, tid);
-    transpose_tile<kBatch, KP>(sG, sGt, tid);
+    transpose_tile<kBatch, KP, kBatch, 128u, kLboPad>(sG, sGt, tid);
     fence_async_smem();
     fence_before();
     __syncthreads();
@@ -596,7 +639,7 @@ static cudaError_t launch_batch(const SgnsParams& p, const Device& dev, cudaStre
     const uint64_t full = (uint64_t)std::max(1, dev.sm_count - p.reserve_sms);
     const unsigned grid = p.deterministic ? 1u : (unsigned)std::max<uint64_t>(
                                                      1, std::min<uint64_t>({nbatch, full, p.max_warps}));
-    kern<<<grid, kBatch, smem, s>>>(p);
+    kern<<<grid, kBatchThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -51,6 +51,9 @@ struct ne_ctx {
     cudaStream_t copy_stream = nullptr;  // host staging H2D (D2H uses comm_stream)
     cudaEvent_t stage_done = nullptr;    // last D2H of a call (deferred like ring_done)
     bool stage_pending = false;
+    cudaEvent_t stage_pre_ev = nullptr;  // one GPU: the next episode's sub-part 0, prefetched into slot 0
+    bool stage_pre = false;
+    uint32_t stage_base = 0;             // one GPU: sub-part t of this episode uses slot (t + base) % 3
     int cur = 0;                // half [cur*k, cur*k+k) holds the current sub-parts
     uint64_t max_sub_rows = 0;
 
@@ -123,6 +126,7 @@ struct ne_ctx {
         uint32_t* flags = nullptr;       // arrived[2][k], credit[2][k] (per hop kind; ring_ipc.cpp)
         std::vector<void*> peer;         // regions of the ranks this one pushes to / credits, opened handles
         bool connected = false;
+        std::string blobs;               // the handles the open peers came from (a reload reuses them)
         bool started = false;            // a ring call ran since the last load (arrivals to wait for)
         std::vector<uint32_t> pushed[2], waited[2];  // per hop kind and slot: pushes issued / arrivals awaited
     } ipc;

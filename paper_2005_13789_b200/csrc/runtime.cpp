@@ -162,7 +162,7 @@ void free_all(ne_ctx* c) {
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     if (c->build_stream) cudaStreamSynchronize(c->build_stream);
-    c->stage_pending = false;
+    c->stage_pending = c->stage_pre = false;
     for (auto& a : c->allocs) {
         if (c->free_fn) c->free_fn(a.p, a.bytes, c->device, (void*)c->stream, c->user);
         else cudaFree(a.p);
@@ -497,6 +497,16 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     const uint64_t row = c->cfg.walk_len + 1;
     const bool real = c->comm != nullptr;
     c->tmat.assign((size_t)P * P, 0);
+    // developer knob NE_BUILD_TIMING=1: per-stage times of this build on stderr
+    static const bool timing = [] { const char* e = std::getenv("NE_BUILD_TIMING"); return e && std::atoi(e); }();
+    std::vector<std::pair<const char*, cudaEvent_t>> marks;
+    auto mark = [&](const char* name) {
+        if (!timing) return;
+        cudaEvent_t e = next_event(c);
+        cudaEventRecord(e, c->ws);
+        marks.push_back({name, e});
+    };
+    mark("start");
     // this rank's shard (real) or shard s (emulation): counts -> scan -> part totals
     auto count_shard = [&](uint32_t s, const uint32_t* walks, uint64_t su, uint64_t* tot_dev) -> int {
         ne::PoolParams pp = pool_params(c, epoch, episode, u0, su);
@@ -528,6 +538,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
             NE_TRY(count_shard(s, w, su, c->d_tmat + (uint64_t)s * P));
         }
     }
+    mark("count+scan+allgather");
     NE_CUDA(c, cudaMemcpyAsync(c->tmat.data(), c->d_tmat, c->tmat.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                c->ws));
     NE_TRY(wait_stream(c, c->ws));
@@ -562,8 +573,10 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         (void)s;
         return NE_OK;
     };
+    mark("host");
     if (real) {
         NE_TRY(gen_shard(me, c->d_walks, c->shard_units));
+        mark("pairs_parts");
         NE_NCCL(c, ncclGroupStart());
         for (uint32_t q = 0; q < P; ++q) {
             if (M(me, q)) NE_NCCL(c, ncclSend(c->d_pool + send_off(me, q), M(me, q), ncclUint64, (int)q, c->comm_walk,
@@ -583,6 +596,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
                                        cudaMemcpyDeviceToDevice, c->ws));
         }
     }
+    mark("exchange");
     // O6: pi over the gathered pool, then order + bucketing
     ne::PoolParams pp = pool_params(c, epoch, episode, u0, units);
     pp.N = N;
@@ -596,7 +610,21 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         }
         c->launches += 1;
     }
+    mark("feistel_keys");
     NE_TRY(finish_pool(c, N, keyed));
+    mark("order+bucket");
+    if (timing && !marks.empty()) {
+        cudaEventSynchronize(marks.back().second);
+        std::string line;
+        for (size_t m = 1; m < marks.size(); ++m) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[m - 1].second, marks[m].second);
+            char buf[96];
+            std::snprintf(buf, sizeof buf, " %s=%.2f", marks[m].first, ms);
+            line += buf;
+        }
+        std::fprintf(stderr, "[ne build rank %u ep %u N=%llu]%s\n", me, episode, (unsigned long long)N, line.c_str());
+    }
     c->built_epoch = epoch;
     c->built_episode = episode;
     return NE_OK;
@@ -705,21 +733,25 @@ int launch_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, T
     const uint32_t k = c->cfg.subparts, S = (uint32_t)c->vslot.size();
     const uint64_t d = c->cfg.dim;
     std::vector<cudaEvent_t> loaded(k), stored(k);
+    const uint32_t base = c->stage_base;
+    auto slot = [&](uint32_t t) { return c->vslot[(t + base) % S]; };
     auto h2d = [&](uint32_t t) -> int {
         if (t >= S) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, stored[t - S], 0));
         else if (c->stage_pending) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->stage_done, 0));
         const uint64_t sb = c->sub_bounds[t], rows = c->sub_bounds[t + 1] - sb;
-        NE_CUDA(c, cudaMemcpyAsync(c->vslot[t % S], host_row(c, sb), rows * d * elem_bytes(c),
+        NE_CUDA(c, cudaMemcpyAsync(slot(t), host_row(c, sb), rows * d * elem_bytes(c),
                                    cudaMemcpyHostToDevice, c->copy_stream));
         loaded[t] = next_event(c);
         NE_CUDA(c, cudaEventRecord(loaded[t], c->copy_stream));
         return NE_OK;
     };
-    if (k) NE_TRY(h2d(0));
+    if (k && c->stage_pre) loaded[0] = c->stage_pre_ev;  // prefetched by the previous episode
+    else if (k) NE_TRY(h2d(0));
+    c->stage_pre = false;
     for (uint32_t t = 0; t < k; ++t) {
         if (t + 1 < k) NE_TRY(h2d(t + 1));
         NE_CUDA(c, cudaStreamWaitEvent(c->stream, loaded[t], 0));
-        const ne::SgnsParams sp = sgns_params(c, t, c->vslot[t % S], epoch, episode, lr);
+        const ne::SgnsParams sp = sgns_params(c, t, slot(t), epoch, episode, lr);
         cudaEvent_t e0 = next_event(c), e1 = next_event(c);
         NE_CUDA(c, cudaEventRecord(e0, c->stream));
         NE_CUDA(c, ne::launch_sgns(sp, c->dev, c->stream));
@@ -729,7 +761,7 @@ int launch_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, T
         tp.samples += sp.count;
         const uint64_t sb = c->sub_bounds[t], rows = c->sub_bounds[t + 1] - sb;
         NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, e1, 0));
-        NE_CUDA(c, cudaMemcpyAsync(host_row(c, sb), c->vslot[t % S], rows * d * elem_bytes(c),
+        NE_CUDA(c, cudaMemcpyAsync(host_row(c, sb), slot(t), rows * d * elem_bytes(c),
                                    cudaMemcpyDeviceToHost, c->comm_stream));
         stored[t] = next_event(c);
         NE_CUDA(c, cudaEventRecord(stored[t], c->comm_stream));
@@ -739,6 +771,22 @@ int launch_train_staged(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, T
     if (!c->stage_done) NE_CUDA(c, cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
     NE_CUDA(c, cudaEventRecord(c->stage_done, c->comm_stream));
     c->stage_pending = true;
+    // Prefetch the next episode's sub-part 0 while sub-part k-1 still trains, so
+    // an episode does not start behind a full-part H2D: slots rotate across
+    // episodes (sub-part 0 of the next episode takes slot (base + k) % 3), and
+    // that slot is free once sub-part k-3, its last user, is copied back
+    // (comm-stream order also puts sub-part 0's own copy-back, the rows loaded
+    // here, before it).  Host writers (rows_op, load_graph) drop the prefetch.
+    c->stage_base = (base + k) % S;
+    if (k) {
+        if (!c->stage_pre_ev) NE_CUDA(c, cudaEventCreateWithFlags(&c->stage_pre_ev, cudaEventDisableTiming));
+        NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, k >= S ? stored[k - S] : c->stage_done, 0));
+        NE_CUDA(c, cudaMemcpyAsync(c->vslot[c->stage_base], host_row(c, c->sub_bounds[0]),
+                                   (c->sub_bounds[1] - c->sub_bounds[0]) * d * elem_bytes(c),
+                                   cudaMemcpyHostToDevice, c->copy_stream));
+        NE_CUDA(c, cudaEventRecord(c->stage_pre_ev, c->copy_stream));
+        c->stage_pre = true;
+    }
     return NE_OK;
 }
 
@@ -1175,7 +1223,7 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));  // ring transfers into the vertex slots
     NE_CUDA(c, cudaStreamSynchronize(c->copy_stream));
     c->ring_pending = false;
-    c->stage_pending = false;
+    c->stage_pending = c->stage_pre = false;
     if (c->alias_thread.joinable()) c->alias_thread.join();
     c->alias_pending = false;
     const bool reuse = c->loaded && c->n == n && c->nnz == nnz;
@@ -1537,7 +1585,7 @@ static int rows_op(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, f
     if (which == NE_CONTEXT) return copy(c->d_C, c->c_begin, row_begin, row_end);
     if (c->cfg.staging == NE_STAGE_HOST) {
         NE_CUDA(c, cudaStreamSynchronize(c->copy_stream));
-        c->stage_pending = false;
+        c->stage_pending = c->stage_pre = false;
         // pinned host rows (device-accessible under UVA: the bf16 conversion kernel reads them in place)
         return copy(static_cast<float*>(host_row(c, row_begin)), row_begin, row_begin, row_end);
     }
@@ -1792,6 +1840,7 @@ void ne_destroy(ne_ctx* c) {
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->ring_done) cudaEventDestroy(c->ring_done);
     if (c->stage_done) cudaEventDestroy(c->stage_done);
+    if (c->stage_pre_ev) cudaEventDestroy(c->stage_pre_ev);
     if (c->h_V) cudaFreeHost(c->h_V);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->build_stream) cudaStreamDestroy(c->build_stream);

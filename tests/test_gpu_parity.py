@@ -578,14 +578,38 @@ def test_accumulated_rule_hogwild_auc():
 
 
 # ---------------------------------------------------------------- NEXT-2 host staging
-@pytest.mark.parametrize("subparts", [2, 7])
+@pytest.mark.parametrize("subparts", [2, 3, 7])
 def test_host_staged_vertex_matrix_matches_oracle(subparts):
     """NE_STAGE_HOST: the vertex matrix lives in pinned host memory and streams
-    through 3 device slots (P:142 stages 2, 5); results equal the in-HBM path."""
+    through 3 device slots (P:142 stages 2, 5); results equal the in-HBM path.
+    k = 2, 3, 7 cover the next-episode prefetch of sub-part 0 with k < 3,
+    k = 3 and a slot rotation that moves every episode (7 % 3 = 1)."""
     off, tgt = synth.rmat_graph(3000, 20000, 41)
     dv, dc = _det_epoch(off, tgt, epochs=2, dim=64, walk_len=12, window=3, subparts=subparts,
                         episodes=2, staging=1)
     assert dv <= TOL and dc <= TOL, (dv, dc)
+
+
+def test_host_staged_write_drops_prefetch():
+    """A host write between epochs lands after the next episode's sub-part 0
+    was prefetched: the write must win (the prefetch is dropped), so the run
+    still equals the oracle fed the same write."""
+    off, tgt = synth.rmat_graph(3000, 20000, 43)
+    kw = dict(dim=64, walk_len=10, window=3, subparts=7, episodes=2)
+    cfg = ocfg(**kw)
+    eng = engine(staging=1, **kw)
+    eng.load_graph(off, tgt)
+    V = oracle.init_vertex(3000, 64, 42)
+    Cm = np.zeros_like(V)
+    mark = np.random.default_rng(3).normal(0, 0.1, (40, 64)).astype(np.float32)
+    for ep in range(2):
+        eng.train_epoch(ep, 0.025)
+        oracle.train_epoch(cfg, off, tgt, V, Cm, ep, 0.025)
+        eng.set_embeddings(0, 10, mark)   # rows of sub-part 0
+        V[10:50] = mark
+    assert np.abs(eng.embeddings(0) - V).max() <= TOL
+    assert np.abs(eng.embeddings(1) - Cm).max() <= TOL
+    eng.close()
 
 
 def test_host_staged_set_get_and_hogwild():
