@@ -18,10 +18,13 @@
 // accumulation in TMEM) by one thread.  The positive term of each sample is a
 // d-long dot (CUDA cores, from shared memory).
 //
-// One CTA of 128 threads (thread i <-> batch row i <-> TMEM lane i) per batch;
-// the persistent grid strides over the block's batches (Hogwild: concurrent
-// batches share rows; every write-back is a red.global.add of the delta), the
-// deterministic mode runs one CTA over the batches in order.
+// One CTA of 256 threads per batch (batch row i <-> TMEM lane i, read by the
+// two warps of its lane quarter); the persistent grid strides over the block's
+// batches (Hogwild: concurrent batches share rows; every write-back is a
+// red.global.add of the delta), and each CTA gathers its next batch's rows
+// while it writes the current one back.  The deterministic mode runs one CTA
+// over the batches in order, gathering each batch after the previous one's
+// write-back.
 //
 // Every operand is K-major (measured: with the no-swizzle layout, MN-major
 // tf32 operands multiply as zeros -- CUTLASS allows MN-major tf32 only in the
@@ -213,7 +216,7 @@ struct BatchSmem {
                               Nt = N + KP / 8 * (D / 4) * kLboPad, G = Nt + KP * D * 4, Gt = G + kBatch * KP * 4,
                               tail = Gt + KP / 8 * (kBatch / 4) * kLboPad;
     static_assert(tail - G >= 64 * D * 4, "the dV write-back stages 64 rows in G, G^T");
-    static constexpr size_t bytes = tail + 16 + 16 + (3 * kBatch + KP) * 4;
+    static constexpr size_t bytes = tail + 16 + 16 + (2 * (2 * kBatch + KP) + kBatch) * 4;
 };
 
 }  // namespace
@@ -236,10 +239,9 @@ __global__ void __launch_bounds__(kBatchThreads, 1) sgns_batch_kernel(SgnsParams
                   *sG = smem + SM::G, *sGt = smem + SM::Gt;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::tail);   // [0]: S ready, [1]: dV, dN^T ready
     uint32_t* tmem_base = reinterpret_cast<uint32_t*>(bar + 2);
-    uint32_t* s_src = tmem_base + 4;
-    uint32_t* s_dst = s_src + kBatch;
-    uint32_t* s_neg = s_dst + kBatch;
-    float* s_gpos = reinterpret_cast<float*>(s_neg + KP);  // kBatch: x_r, then lr (sigma(x_r) - 1)
+    constexpr uint32_t kIds = 2 * kBatch + KP;  // one id buffer: src[B], dst[B], neg[K']
+    uint32_t* s_ids = tmem_base + 4;             // two buffers: this batch's and the next one's
+    float* s_gpos = reinterpret_cast<float*>(s_ids + 2 * kIds);  // kBatch: x_r, then lr (sigma(x_r) - 1)
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     if (warp == 0) {
@@ -284,34 +286,81 @@ __global__ void __launch_bounds__(kBatchThreads, 1) sgns_batch_kernel(SgnsParams
             nx_ta = __ldg(p.alias + nx_col);
         }
     };
+    auto rows_of = [&](uint64_t bb) -> uint32_t {
+        const uint64_t q0 = bb * kBatch;
+        return (uint32_t)(p.count - q0 < (uint64_t)kBatch ? p.count - q0 : (uint64_t)kBatch);
+    };
+    // ids of a batch (O8 with the batch counter, tag BNEG) from the registers
+    // fetch_ids filled into id buffer `buf`
+    auto publish_ids = [&](uint32_t buf, uint32_t nbx) {
+        if (hi) return;
+        uint32_t* ids = s_ids + buf * kIds;
+        if (i < nbx) {
+            ids[i] = nx_pr.x;
+            ids[kBatch + i] = nx_pr.y;
+        }
+        if (i < (uint32_t)KP) ids[2 * kBatch + i] = (uint32_t)(p.c_begin + (nx_coin < nx_ta.x ? nx_col : nx_ta.y));
+    };
+    // gather V and N rows of a batch (cp.async, 16 B per lane; a warp covers 8
+    // rows x 4 chunks so each quarter-warp writes 128 contiguous bytes)
+    // Lane l of warp w copies chunk 4w + l / 8 of rows 8k + l % 8 (k < B / 8);
+    // the row ids are read from shared memory first, all at once.
+    static_assert(NW * 4 == KC, "8 warps x 4 chunks cover a row");
+    auto gather = [&](uint32_t buf, uint32_t nbx) {
+        const uint32_t* src = s_ids + buf * kIds;
+        const uint32_t* neg = src + 2 * kBatch;
+        const uint32_t chunk = warp * 4 + (lane >> 3), r8 = lane & 7u;
+        uint32_t vid[kBatch / 8], nid[KP / 8];
+#pragma unroll
+        for (uint32_t k = 0; k < kBatch / 8; ++k) vid[k] = src[8 * k + r8];
+#pragma unroll
+        for (uint32_t k = 0; k < (uint32_t)KP / 8; ++k) nid[k] = neg[8 * k + r8];
+#pragma unroll
+        for (uint32_t k = 0; k < kBatch / 8; ++k) {
+            const uint32_t row = 8 * k + r8;
+            const uint32_t off = tile_off(row, chunk, D, kLboPad);
+            if (row < nbx) cp_async16(sV + off, p.V + (uint64_t)(vid[k] - p.v_begin) * D + chunk * 4);
+            else *reinterpret_cast<float4*>(sV + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (k < (uint32_t)KP / 8) cp_async16(sN + off, p.C + (uint64_t)(nid[k] - p.c_begin) * D + chunk * 4);
+        }
+    };
+    // the next batch's ids and rows: published and gathered while this batch
+    // is written back (Hogwild: it reads rows as concurrent CTAs do, without
+    // this batch's updates); the deterministic mode fetches after them
+    auto prepare = [&](uint32_t buf, uint64_t bn) {
+        publish_ids(buf, rows_of(bn));
+        fetch_ids(bn + gridDim.x);
+        __syncthreads();
+        gather(buf, rows_of(bn));
+    };
+    uint32_t buf = 0;
     fetch_ids(blockIdx.x);
+    if (blockIdx.x < nbatch) prepare(0, blockIdx.x);
 
     for (uint64_t b = blockIdx.x; b < nbatch; b += gridDim.x) {
-        const uint64_t p0 = b * kBatch;
-        const uint32_t nb = (uint32_t)(p.count - p0 < (uint64_t)kBatch ? p.count - p0 : (uint64_t)kBatch);
+        const uint32_t nb = rows_of(b);
         const bool live = i < nb;
-        // ---- ids: pairs, shared negatives (O8 with the batch counter, tag BNEG),
-        // fetched during the previous batch's write-back (fetch_ids below)
-        if (!hi) {
-            if (live) {
-                s_src[i] = nx_pr.x;
-                s_dst[i] = nx_pr.y;
-            }
-            if (i < (uint32_t)KP) s_neg[i] = (uint32_t)(p.c_begin + (nx_coin < nx_ta.x ? nx_col : nx_ta.y));
-        }
-        __syncthreads();
-        // ---- gather V and N rows (cp.async, 16 B per lane; a warp covers 8 rows
-        // x 4 chunks so each quarter-warp writes 128 contiguous bytes)
-        for (uint32_t f = tid; f < kBatch * KC; f += NT) {
-            const uint32_t q = f >> 5, l = f & 31u;
-            const uint32_t row = (q / (KC / 4)) * 8 + (l & 7u), chunk = (q % (KC / 4)) * 4 + (l >> 3);
-            const uint32_t off = tile_off(row, chunk, D, kLboPad);
-            if (row < nb) cp_async16(sV + off, p.V + (uint64_t)(s_src[row] - p.v_begin) * D + chunk * 4);
-            else *reinterpret_cast<float4*>(sV + off) = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (row < (uint32_t)KP) cp_async16(sN + off, p.C + (uint64_t)(s_neg[row] - p.c_begin) * D + chunk * 4);
-        }
+        const uint32_t* s_src = s_ids + buf * kIds;
+        const uint32_t* s_dst = s_src + kBatch;
+        const uint32_t* s_neg = s_src + 2 * kBatch;
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
+        // positive context rows c+_r (chunk `lane`), issued before the
+        // transposes so their latency overlaps them; warp w takes rows 8w + u
+        // and 64 + 8w + u, and keeps them for the vertex write-back, which
+        // visits the same rows with the same warp (no C row is written before)
+        static_assert(KC == 32, "one float4 of a row per lane");
+        static_assert(NW * 8 * 2 == kBatch, "two groups of 8 rows per warp cover the batch");
+        float4 cpos[2][8];
+#pragma unroll
+        for (uint32_t g = 0; g < 2; ++g)
+#pragma unroll
+            for (uint32_t u = 0; u < 8; ++u) {
+                const uint32_t r = 64 * g + warp * 8 + u;
+                cpos[g][u] = r < nb ? __ldcg(reinterpret_cast<const float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D) +
+                                             lane)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         transpose_tile<kBatch, D, NT>(sV, sVt, tid);
         transpose_tile<KP, D, NT>(sN, sNt, tid);
         fence_async_smem();
@@ -323,29 +372,20 @@ __global__ void __launch_bounds__(kBatchThreads, 1) sgns_batch_kernel(SgnsParams
             mma_commit(&bar[0]);
         }
         // ---- positive terms (CUDA cores, overlapping MMA1): x_r = v_r . c+_r,
-        // warp per row, the context row read coalesced from global memory (no
-        // shared copy; no C row is written before every read of it, below)
-        // (rows in groups of 8 per warp: 8 independent row loads in flight per lane)
-        static_assert(KC == 32, "one float4 of a row per lane");
-        for (uint32_t r0 = warp * 8; r0 < nb; r0 += NW * 8) {
-            float4 cc[8];
+        // warp per row
+#pragma unroll
+        for (uint32_t g = 0; g < 2; ++g)
 #pragma unroll
             for (uint32_t u = 0; u < 8; ++u) {
-                const uint32_t r = r0 + u;
-                cc[u] = r < nb ? __ldcg(reinterpret_cast<const float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D) +
-                                        lane)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (uint32_t u = 0; u < 8; ++u) {
-                const uint32_t r = r0 + u;
+                const uint32_t r = 64 * g + warp * 8 + u;
+                if (r >= nb) break;  // warp-uniform
                 const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, lane, D, kLboPad));
-                float x = fmaf(v.x, cc[u].x, fmaf(v.y, cc[u].y, fmaf(v.z, cc[u].z, v.w * cc[u].w)));
+                const float4 c = cpos[g][u];
+                float x = fmaf(v.x, c.x, fmaf(v.y, c.y, fmaf(v.z, c.z, v.w * c.w)));
 #pragma unroll
                 for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
-                if (lane == 0 && r < nb) s_gpos[r] = x;
+                if (lane == 0) s_gpos[r] = x;
             }
-        }
         __syncthreads();
         float gpos = 0.f;  // lr (sigma(x_i) - 1) of this thread's row
         if (live) {
@@ -396,16 +436,30 @@ __global__ void __launch_bounds__(kBatchThreads, 1) sgns_batch_kernel(SgnsParams
         fence_after();
         __syncthreads();
         if (!hi) s_gpos[i] = gpos;
-        fetch_ids(b + gridDim.x);  // the next batch's ids load while this one is written back
+        __syncthreads();
         // ---- write-back from the batch-start snapshot; every row update is a
-        // coalesced red.global.add of the delta by a warp.  (1) vertex rows,
-        // -(dV + gpos c+), two halves of 64 rows staged through the G / G^T
-        // tiles (consumed by the products); c+ is read again from global memory
-        // (no C row has been written yet).  tcgen05.ld is warp-collective: the
+        // coalesced red.global.add of the delta by a warp.  (3) first: positive
+        // context rows, -gpos v (every c+ read happened in the positive terms);
+        // after it V and N are free for the next batch's gather.
+        for (uint32_t r = warp; r < nb; r += NW) {
+            const float g = s_gpos[r];
+            float4* cw = reinterpret_cast<float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D);
+            for (uint32_t c = lane; c < KC; c += 32) {
+                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, c, D, kLboPad));
+                atomicAdd(cw + c, make_float4(-g * v.x, -g * v.y, -g * v.z, -g * v.w));
+            }
+        }
+        const uint64_t bn = b + gridDim.x;
+        const bool ahead = !p.deterministic && bn < nbatch;
+        __syncthreads();
+        if (ahead) prepare(buf ^ 1u, bn);
+        // (1) vertex rows, -(dV + gpos c+), two halves of 64 rows staged through the G / G^T
+        // tiles (consumed by the products); c+ comes from the registers the
+        // positive terms loaded it into.  tcgen05.ld is warp-collective: the
         // two warps of a lane quarter load 64 columns each of their 32 rows.
         float* stage = reinterpret_cast<float*>(sG);  // 64 x D floats (G and G^T are adjacent)
-#pragma unroll 1
-        for (uint32_t half = 0; half < 2; ++half) {
+#pragma unroll
+        for (uint32_t half = 0; half < 2; ++half) {  // unrolled: cpos[half] stays in registers
             if (((warp & 3u) >> 1) == half) {
 #pragma unroll 1
                 for (uint32_t d0 = hi * (D / 2); d0 < (hi + 1) * (D / 2); d0 += 32) {
@@ -424,23 +478,15 @@ __global__ void __launch_bounds__(kBatchThreads, 1) sgns_batch_kernel(SgnsParams
             __syncthreads();
             {
                 const uint32_t r0 = 64 * half + warp * 8;  // 8 warps x 8 rows = the half
-                float4 cc[8];
-#pragma unroll
-                for (uint32_t u = 0; u < 8; ++u) {
-                    const uint32_t r = r0 + u;
-                    cc[u] = r < nb ? __ldcg(reinterpret_cast<const float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D) +
-                                            lane)
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
 #pragma unroll
                 for (uint32_t u = 0; u < 8; ++u) {
                     const uint32_t r = r0 + u;
                     if (r >= nb) break;
                     const float g = s_gpos[r];
+                    const float4 c = cpos[half][u];
                     const float4 dv = reinterpret_cast<const float4*>(stage + (r - 64 * half) * D)[lane ^ (r & 7u)];
                     atomicAdd(reinterpret_cast<float4*>(p.V + (uint64_t)(s_src[r] - p.v_begin) * D) + lane,
-                              make_float4(-(dv.x + g * cc[u].x), -(dv.y + g * cc[u].y), -(dv.z + g * cc[u].z),
-                                          -(dv.w + g * cc[u].w)));
+                              make_float4(-(dv.x + g * c.x), -(dv.y + g * c.y), -(dv.z + g * c.z), -(dv.w + g * c.w)));
                 }
             }
             __syncthreads();
@@ -453,16 +499,7 @@ __global__ void __launch_bounds__(kBatchThreads, 1) sgns_batch_kernel(SgnsParams
             for (uint32_t e = 0; e < (uint32_t)KP / 2; ++e) stage[(hi * (KP / 2) + e) * D + i] = dn[e];
         }
         fence_before();
-        __syncthreads();  // every c+ read (1) is done before any C row is written
-        // (3) positive context rows: -gpos v
-        for (uint32_t r = warp; r < nb; r += NW) {
-            const float g = s_gpos[r];
-            float4* cw = reinterpret_cast<float4*>(p.C + (uint64_t)(s_dst[r] - p.c_begin) * D);
-            for (uint32_t c = lane; c < KC; c += 32) {
-                const float4 v = *reinterpret_cast<const float4*>(sV + tile_off(r, c, D, kLboPad));
-                atomicAdd(cw + c, make_float4(-g * v.x, -g * v.y, -g * v.z, -g * v.w));
-            }
-        }
+        __syncthreads();
         // (4) negative rows: -dN
         for (uint32_t j = warp; j < (uint32_t)KP; j += NW) {
             float4* nrow = reinterpret_cast<float4*>(p.C + (uint64_t)(s_neg[j] - p.c_begin) * D);
@@ -472,6 +509,8 @@ __global__ void __launch_bounds__(kBatchThreads, 1) sgns_batch_kernel(SgnsParams
             }
         }
         __syncthreads();
+        if (!ahead && bn < nbatch) prepare(buf ^ 1u, bn);
+        buf ^= 1u;
         phase ^= 1u;
     }
     if (loss != 0.0) atomicAdd(p.loss, loss);

@@ -490,6 +490,39 @@ ne::PoolParams pool_params(const ne_ctx* c, uint32_t epoch, uint32_t episode, ui
 // position -- the same pool as the unsharded construction, O(N/P) per rank.
 // A layout-only rank (no NCCL) runs the same kernels for every shard and copies
 // its part's segment in place of the receive.
+// Developer knob NE_BUILD_TIMING=1: per-stage times of every pool build on
+// stderr (events on the build's stream; read after finish_pool's sync).
+struct BuildTimer {
+    ne_ctx* c;
+    bool on;
+    std::vector<std::pair<const char*, cudaEvent_t>> marks;
+    explicit BuildTimer(ne_ctx* cc) : c(cc) {
+        static const bool timing = [] { const char* e = std::getenv("NE_BUILD_TIMING"); return e && std::atoi(e); }();
+        on = timing;
+        mark("start");
+    }
+    void mark(const char* name) {
+        if (!on) return;
+        cudaEvent_t e = next_event(c);
+        cudaEventRecord(e, c->ws);
+        marks.push_back({name, e});
+    }
+    void report(uint32_t episode, uint64_t N) {
+        if (!on || marks.size() < 2) return;
+        cudaEventSynchronize(marks.back().second);
+        std::string line;
+        for (size_t m = 1; m < marks.size(); ++m) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[m - 1].second, marks[m].second);
+            char buf[96];
+            std::snprintf(buf, sizeof buf, " %s=%.2f", marks[m].first, ms);
+            line += buf;
+        }
+        std::fprintf(stderr, "[ne build rank %d ep %u N=%llu]%s\n", c->rank, episode, (unsigned long long)N,
+                     line.c_str());
+    }
+};
+
 int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     const uint32_t P = (uint32_t)c->world, me = (uint32_t)c->rank;
     uint64_t u0, units;
@@ -497,16 +530,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     const uint64_t row = c->cfg.walk_len + 1;
     const bool real = c->comm != nullptr;
     c->tmat.assign((size_t)P * P, 0);
-    // developer knob NE_BUILD_TIMING=1: per-stage times of this build on stderr
-    static const bool timing = [] { const char* e = std::getenv("NE_BUILD_TIMING"); return e && std::atoi(e); }();
-    std::vector<std::pair<const char*, cudaEvent_t>> marks;
-    auto mark = [&](const char* name) {
-        if (!timing) return;
-        cudaEvent_t e = next_event(c);
-        cudaEventRecord(e, c->ws);
-        marks.push_back({name, e});
-    };
-    mark("start");
+    BuildTimer bt(c);
     // this rank's shard (real) or shard s (emulation): counts -> scan -> part totals
     auto count_shard = [&](uint32_t s, const uint32_t* walks, uint64_t su, uint64_t* tot_dev) -> int {
         ne::PoolParams pp = pool_params(c, epoch, episode, u0, su);
@@ -538,7 +562,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
             NE_TRY(count_shard(s, w, su, c->d_tmat + (uint64_t)s * P));
         }
     }
-    mark("count+scan+allgather");
+    bt.mark("count+scan+allgather");
     NE_CUDA(c, cudaMemcpyAsync(c->tmat.data(), c->d_tmat, c->tmat.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                c->ws));
     NE_TRY(wait_stream(c, c->ws));
@@ -573,10 +597,10 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         (void)s;
         return NE_OK;
     };
-    mark("host");
+    bt.mark("host");
     if (real) {
         NE_TRY(gen_shard(me, c->d_walks, c->shard_units));
-        mark("pairs_parts");
+        bt.mark("pairs_parts");
         NE_NCCL(c, ncclGroupStart());
         for (uint32_t q = 0; q < P; ++q) {
             if (M(me, q)) NE_NCCL(c, ncclSend(c->d_pool + send_off(me, q), M(me, q), ncclUint64, (int)q, c->comm_walk,
@@ -596,7 +620,7 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
                                        cudaMemcpyDeviceToDevice, c->ws));
         }
     }
-    mark("exchange");
+    bt.mark("exchange");
     // O6: pi over the gathered pool, then order + bucketing
     ne::PoolParams pp = pool_params(c, epoch, episode, u0, units);
     pp.N = N;
@@ -610,21 +634,10 @@ int do_build_sharded(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         }
         c->launches += 1;
     }
-    mark("feistel_keys");
+    bt.mark("feistel_keys");
     NE_TRY(finish_pool(c, N, keyed));
-    mark("order+bucket");
-    if (timing && !marks.empty()) {
-        cudaEventSynchronize(marks.back().second);
-        std::string line;
-        for (size_t m = 1; m < marks.size(); ++m) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, marks[m - 1].second, marks[m].second);
-            char buf[96];
-            std::snprintf(buf, sizeof buf, " %s=%.2f", marks[m].first, ms);
-            line += buf;
-        }
-        std::fprintf(stderr, "[ne build rank %u ep %u N=%llu]%s\n", me, episode, (unsigned long long)N, line.c_str());
-    }
+    bt.mark("order+bucket");
+    bt.report(episode, N);
     c->built_epoch = epoch;
     c->built_episode = episode;
     return NE_OK;
@@ -635,6 +648,7 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
     if (c->world > 1 && c->cfg.walk_len > 0) return do_build_sharded(c, epoch, episode);
     uint64_t u0, units;
     episode_range(c, episode, &u0, &units);
+    BuildTimer bt(c);
     ne::PoolParams p = pool_params(c, epoch, episode, u0, units);
     // O5: kept pairs per unit, exclusive scan -> part-local index bases, N_g
     uint64_t N = 0;
@@ -651,6 +665,7 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
         NE_CUDA(c, cudaMemcpyAsync(&N, c->d_total, sizeof N, cudaMemcpyDeviceToHost, c->ws));
         NE_CUDA(c, cudaStreamSynchronize(c->ws));
     }
+    bt.mark("count+scan");
     if (N > c->N_max) return ne_fail(c, NE_ERANGE, "episode pool %llu > bound %llu (internal)", (unsigned long long)N,
                                   (unsigned long long)c->N_max);
     NE_TRY(ensure_pool(c, N));
@@ -666,7 +681,10 @@ int do_build(ne_ctx* c, uint32_t epoch, uint32_t episode) {
             NE_CUDA(c, ne::launch_pairs_line(c->d_off, c->d_tgt, c->n, p, c->d_base, sink, c->dev, c->ws));
         c->launches += 1;
     }
+    bt.mark("pairs+keys");
     NE_TRY(finish_pool(c, N, keyed));
+    bt.mark("order+bucket");
+    bt.report(episode, N);
     c->built_epoch = epoch;
     c->built_episode = episode;
     return NE_OK;

@@ -403,7 +403,8 @@ cudaError_t launch_sgns_rows(const SgnsParams& p, const Device& dev, cudaStream_
     const uint32_t q = p.d / 4;
     // 64 < d <= 96 at K = 5: 8-lane groups x 3 float4, four samples per warp, so
     // a 384-byte row uses every lane (16-lane groups leave a quarter idle)
-    if (q > 16 && q <= 24 && p.K == 5) return launch_sgns_k<8, 3, 5, BF>(p, dev, s);
+    // (developer knob NE_SGNS_D96=16: the 16-lane kernel instead, read per launch)
+    if (q > 16 && q <= 24 && p.K == 5 && env_int("NE_SGNS_D96", 8) != 16) return launch_sgns_k<8, 3, 5, BF>(p, dev, s);
     if constexpr (!BF) {  // developer knob: the shared-memory-staged kernel (d <= 128, K = 5, Hogwild)
         const int staged = env_int("NE_SGNS_STAGED", 0);  // read per launch: tests toggle it
         if (staged && q > 16 && q <= 32 && !p.deterministic && p.atomic_writeback && !p.accumulate &&
