@@ -370,11 +370,19 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_samples = 0
     e0.record(stream)
+    e_ph = {"load": 0.0, "train": 0.0, "get": 0.0}  # host-side split (each call returns synchronised)
     for s in range(args.e2e_steps):
+        t0 = time.perf_counter()
         ne.ne_load_graph(eng.ctx, off_h, tgt_h)
+        t1 = time.perf_counter()
         st = eng.train_epoch(s, 0.025)  # loss_sum / samples read back (D2H) by the call
+        t2 = time.perf_counter()
         for which in (ne.NE_VERTEX, ne.NE_CONTEXT):
             ne.ne_get_embeddings(eng.ctx, which, a, b, emb_h[which])
+        t3 = time.perf_counter()
+        e_ph["load"] += (t1 - t0) * 1e3
+        e_ph["train"] += (t2 - t1) * 1e3
+        e_ph["get"] += (t3 - t2) * 1e3
         e_samples += st["samples"]
     e1.record(stream)
     barrier()
@@ -435,7 +443,8 @@ def main():
                     # block offsets, pool size and loss per episode
                     "d2h_bytes_per_step": d2h + 32 + episodes * (8 * (args.subparts * world + 1) + 16),
                     "step": "ne_load_graph (pinned host CSR) + ne_train_epoch + ne_get_embeddings of both "
-                            "matrices (this rank's rows, to pinned host memory)"},
+                            "matrices (this rank's rows, to pinned host memory)",
+                    "phases_ms_per_step": {k: v / max(1, args.e2e_steps) for k, v in e_ph.items()}},
             "clocks": clk.summary(),
             "gpu_launches": int(tsum[3]),
         }
