@@ -48,7 +48,8 @@ struct ne_ctx {
     std::vector<float*> vslot;  // ring: 2k buffers (ping-pong); one GPU: k; host staging: 3
     float* h_V = nullptr;       // host staging: this rank's vertex rows, pinned
     size_t h_V_bytes = 0;
-    cudaStream_t copy_stream = nullptr;  // host staging H2D (D2H uses comm_stream)
+    cudaStream_t copy_stream = nullptr;  // host staging H2D (one GPU: D2H uses comm_stream)
+    cudaStream_t d2h_stream = nullptr;   // host staging with the ring: D2H, off the ring's comm stream
     cudaEvent_t stage_done = nullptr;    // last D2H of a call (deferred like ring_done)
     bool stage_pending = false;
     cudaEvent_t stage_pre_ev = nullptr;  // one GPU: the next episode's sub-part 0, prefetched into slot 0

@@ -161,6 +161,7 @@ void free_all(ne_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
     if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+    if (c->d2h_stream) cudaStreamSynchronize(c->d2h_stream);
     if (c->build_stream) cudaStreamSynchronize(c->build_stream);
     c->stage_pending = c->stage_pre = false;
     for (auto& a : c->allocs) {
@@ -875,14 +876,15 @@ int launch_train_staged_ring(ne_ctx* c, uint32_t epoch, uint32_t episode, float 
             }
             std::swap(cur, nxt);
         }
-        // home again (set cur): stage 2, D2H on the comm stream after the last receive
+        // home again (set cur): stage 2, D2H after the last receive, on its own
+        // stream so the next window's ring transfers do not queue behind it
         for (uint32_t t = 0; t < wn; ++t) {
             const uint64_t vs = (uint64_t)g * k + t0 + t, sb = c->sub_bounds[vs];
-            NE_CUDA(c, cudaStreamWaitEvent(c->comm_stream, recv[t], 0));
+            NE_CUDA(c, cudaStreamWaitEvent(c->d2h_stream, recv[t], 0));
             NE_CUDA(c, cudaMemcpyAsync(host_row(c, sb), slot(cur, t), (c->sub_bounds[vs + 1] - sb) * d * esz,
-                                       cudaMemcpyDeviceToHost, c->comm_stream));
+                                       cudaMemcpyDeviceToHost, c->d2h_stream));
             drained[t] = next_event(c);
-            NE_CUDA(c, cudaEventRecord(drained[t], c->comm_stream));
+            NE_CUDA(c, cudaEventRecord(drained[t], c->d2h_stream));
         }
         // next window trains the prefetched set; this window's home set drains
         // and then takes the prefetch of the window after
@@ -891,7 +893,7 @@ int launch_train_staged_ring(ne_ctx* c, uint32_t epoch, uint32_t episode, float 
         pre = home;
     }
     if (!c->stage_done) NE_CUDA(c, cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
-    NE_CUDA(c, cudaEventRecord(c->stage_done, c->comm_stream));
+    NE_CUDA(c, cudaEventRecord(c->stage_done, c->d2h_stream));  // after every receive it waited for
     c->stage_pending = true;
     return NE_OK;
 }
@@ -1174,6 +1176,7 @@ int ne_create(ne_ctx** out, const ne_config* cfg, int device, ne_alloc_fn alloc,
         cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->build_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&c->d_loss, sizeof(double)) != cudaSuccess ||
         cudaMalloc(&c->d_bad, 3 * sizeof(unsigned long long)) != cudaSuccess)
@@ -1240,6 +1243,7 @@ int ne_load_graph(ne_ctx* c, uint32_t n, uint64_t nnz, const uint64_t* offsets,
     NE_TRY(ipc_drain(c, true));                          // IPC ring: pushes into / out of the slots
     NE_CUDA(c, cudaStreamSynchronize(c->comm_stream));  // ring transfers into the vertex slots
     NE_CUDA(c, cudaStreamSynchronize(c->copy_stream));
+    NE_CUDA(c, cudaStreamSynchronize(c->d2h_stream));
     c->ring_pending = false;
     c->stage_pending = c->stage_pre = false;
     if (c->alias_thread.joinable()) c->alias_thread.join();
@@ -1603,6 +1607,7 @@ static int rows_op(ne_ctx* c, int which, uint32_t row_begin, uint32_t row_end, f
     if (which == NE_CONTEXT) return copy(c->d_C, c->c_begin, row_begin, row_end);
     if (c->cfg.staging == NE_STAGE_HOST) {
         NE_CUDA(c, cudaStreamSynchronize(c->copy_stream));
+        NE_CUDA(c, cudaStreamSynchronize(c->d2h_stream));
         c->stage_pending = c->stage_pre = false;
         // pinned host rows (device-accessible under UVA: the bf16 conversion kernel reads them in place)
         return copy(static_cast<float*>(host_row(c, row_begin)), row_begin, row_begin, row_end);
@@ -1861,6 +1866,7 @@ void ne_destroy(ne_ctx* c) {
     if (c->stage_pre_ev) cudaEventDestroy(c->stage_pre_ev);
     if (c->h_V) cudaFreeHost(c->h_V);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     if (c->build_stream) cudaStreamDestroy(c->build_stream);
     if (c->comm_walk) ncclCommDestroy(c->comm_walk);
     if (c->comm) ncclCommDestroy(c->comm);
