@@ -142,6 +142,7 @@ struct SgnsParams {
     int bf16;                   // rows stored as bfloat16 (NEXT-4, reading D16); V, C point at them
     int accumulate;             // update rule: 0 sequential, 1 accumulated (word2vec), 2 shared-negative batch
     uint32_t* capture;          // test hook: (src, dst, negs) per position, [count][2+K] (nullptr: off)
+    uint32_t l2hint;            // developer knob (fp32 rows): L2 policy of vertex (bits 0-1) / context (2-3) rows
 };
 cudaError_t launch_sgns(const SgnsParams& p, const Device& dev, cudaStream_t s);
 // bf16-row instantiations (kernels_sgns_bf16.cu); launch_sgns dispatches on p.bf16.

@@ -734,6 +734,11 @@ ne::SgnsParams sgns_params(const ne_ctx* c, uint32_t vsub, float* V, uint32_t ep
         return e ? std::atoi(e) : 0;
     }();
     p.reserve_sms = std::max((c->world > 1 && c->comm) ? reserve : 0, c->sgns_reserve);
+    static const uint32_t l2hint = [] {  // developer knob NE_SGNS_L2HINT (V policy | C policy << 2; 1 first, 2 last)
+        const char* e = std::getenv("NE_SGNS_L2HINT");
+        return e ? (uint32_t)std::atoi(e) : 0u;
+    }();
+    p.l2hint = l2hint;
     return p;
 }
 

@@ -129,7 +129,28 @@ struct RowIO<false> {
     static __device__ __forceinline__ void add(float* m, uint64_t row, uint32_t d, uint32_t e, float4 dv) {
         atomicAdd(reinterpret_cast<float4*>(m + row * d) + e, dv);
     }
+    // the same with an L2 eviction-priority policy (createpolicy; developer knob NE_SGNS_L2HINT)
+    static __device__ __forceinline__ float4 load(const float* m, uint64_t row, uint32_t d, uint32_t e, uint64_t pol) {
+        float4 v;
+        asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                     : "l"(reinterpret_cast<const float4*>(m + row * d) + e), "l"(pol));
+        return v;
+    }
+    static __device__ __forceinline__ void add(float* m, uint64_t row, uint32_t d, uint32_t e, float4 dv, uint64_t pol) {
+        asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                     ::"l"(reinterpret_cast<float4*>(m + row * d) + e), "f"(dv.x), "f"(dv.y), "f"(dv.z), "f"(dv.w),
+                     "l"(pol) : "memory");
+    }
 };
+
+__device__ __forceinline__ uint64_t l2_policy(uint32_t kind) {  // 0 normal, 1 evict_first, 2 evict_last
+    uint64_t pol;
+    if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 
 template <>
 struct RowIO<true> {

@@ -43,6 +43,25 @@ __global__ void __launch_bounds__(T, MINB) sgns_kernel(SgnsParams p) {
     const uint2 key = key_of(p.seed);
     const uint32_t tagw = tag_word(kTagNeg, p.epoch);
     double loss = 0.0;  // lane sub == 0 of each group
+    // developer knob p.l2hint (fp32 rows): L2 eviction priorities for vertex / context rows
+    const bool hint = !BF && p.l2hint != 0;
+    uint64_t pol_v = 0, pol_c = 0;
+    if (hint) {
+        pol_v = l2_policy(p.l2hint & 3u);         // bits 0-1: vertex rows (1 evict_first, 2 evict_last)
+        pol_c = l2_policy((p.l2hint >> 2) & 3u);  // bits 2-3: context rows
+    }
+    auto row_load = [&](const float* m, uint64_t row, uint32_t e, uint64_t pol) -> float4 {
+        if constexpr (!BF) {
+            if (hint) return IO::load(m, row, p.d, e, pol);
+        }
+        return IO::load(m, row, p.d, e);
+    };
+    auto row_add = [&](float* m, uint64_t row, uint32_t e, float4 dv, uint64_t pol) {
+        if constexpr (!BF) {
+            if (hint) return IO::add(m, row, p.d, e, dv, pol);
+        }
+        IO::add(m, row, p.d, e, dv);
+    };
 
     // pair + negatives of the iteration starting at sample b (lane L < spw*K
     // draws negative L % K of sample b + L / K); the alias entry is loaded here
@@ -85,7 +104,7 @@ __global__ void __launch_bounds__(T, MINB) sgns_kernel(SgnsParams p) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t e = sub + G * r;
-            v[r] = (act && e < q) ? IO::load(p.V, vr, p.d, e) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[r] = (act && e < q) ? row_load(p.V, vr, e, pol_v) : make_float4(0.f, 0.f, 0.f, 0.f);
             if constexpr (ADD || ACC) v0[r] = v[r];
             if constexpr (ACC) eacc[r] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -96,7 +115,7 @@ __global__ void __launch_bounds__(T, MINB) sgns_kernel(SgnsParams p) {
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const uint32_t e = sub + G * r;
-                    c[j][r] = (act && e < q) ? IO::load(p.C, cr, p.d, e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    c[j][r] = (act && e < q) ? row_load(p.C, cr, e, pol_c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
         }
@@ -135,7 +154,7 @@ __global__ void __launch_bounds__(T, MINB) sgns_kernel(SgnsParams p) {
                     const uint32_t e = sub + G * r;
                     if (act && e < q) {
                         if constexpr (ADD)  // this update's delta, at every occurrence
-                            IO::add(p.C, cr, p.d, e, scaled(-a, vo[r]));
+                            row_add(p.C, cr, e, scaled(-a, vo[r]), pol_c);
                         else if (last)      // the row's final value, once
                             IO::store(p.C, cr, p.d, e, c[j][r]);
                     }
@@ -149,8 +168,8 @@ __global__ void __launch_bounds__(T, MINB) sgns_kernel(SgnsParams p) {
                 v[r] = make_float4(v0[r].x - eacc[r].x, v0[r].y - eacc[r].y, v0[r].z - eacc[r].z, v0[r].w - eacc[r].w);
             if (act && e < q) {
                 if constexpr (ADD)
-                    IO::add(p.V, vr, p.d, e, make_float4(v[r].x - v0[r].x, v[r].y - v0[r].y,
-                                                         v[r].z - v0[r].z, v[r].w - v0[r].w));
+                    row_add(p.V, vr, e, make_float4(v[r].x - v0[r].x, v[r].y - v0[r].y,
+                                                    v[r].z - v0[r].z, v[r].w - v0[r].w), pol_v);
                 else
                     IO::store(p.V, vr, p.d, e, v[r]);
             }
