@@ -366,6 +366,11 @@ def main():
     h2d = off_h.numel() * 8 + tgt_h.numel() * 4
     a, b = eng.part
     emb_h = [torch.empty((b - a, w.dim), dtype=torch.float32).pin_memory() for _ in range(2)]
+    # one GPU, fp32 rows in HBM: the vertex rows stream out during the epoch's last
+    # episode (ne_export_vertex_on_train); otherwise they are read after it
+    export_v = world == 1 and esz == 4 and args.staging == "device"
+    if export_v:
+        ne.ne_export_vertex_on_train(eng.ctx, emb_h[0])
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_samples = 0
@@ -377,7 +382,7 @@ def main():
         t1 = time.perf_counter()
         st = eng.train_epoch(s, 0.025)  # loss_sum / samples read back (D2H) by the call
         t2 = time.perf_counter()
-        for which in (ne.NE_VERTEX, ne.NE_CONTEXT):
+        for which in ((ne.NE_CONTEXT,) if export_v else (ne.NE_VERTEX, ne.NE_CONTEXT)):
             ne.ne_get_embeddings(eng.ctx, which, a, b, emb_h[which])
         t3 = time.perf_counter()
         e_ph["load"] += (t1 - t0) * 1e3
@@ -443,7 +448,9 @@ def main():
                     # block offsets, pool size and loss per episode
                     "d2h_bytes_per_step": d2h + 32 + episodes * (8 * (args.subparts * world + 1) + 16),
                     "step": "ne_load_graph (pinned host CSR) + ne_train_epoch + ne_get_embeddings of both "
-                            "matrices (this rank's rows, to pinned host memory)",
+                            "matrices (this rank's rows, to pinned host memory)"
+                            + ("; the vertex rows stream out during the epoch's last episode "
+                               "(ne_export_vertex_on_train)" if export_v else ""),
                     "phases_ms_per_step": {k: v / max(1, args.e2e_steps) for k, v in e_ph.items()}},
             "clocks": clk.summary(),
             "gpu_launches": int(tsum[3]),

@@ -50,6 +50,9 @@ struct ne_ctx {
     size_t h_V_bytes = 0;
     cudaStream_t copy_stream = nullptr;  // host staging H2D (one GPU: D2H uses comm_stream)
     cudaStream_t d2h_stream = nullptr;   // host staging with the ring: D2H, off the ring's comm stream
+    float* export_V = nullptr;           // ne_export_vertex_on_train: host rows of this rank's part
+    size_t export_cap = 0;
+    bool export_now = false;             // this episode is the call's last: copy sub-parts out
     cudaEvent_t stage_done = nullptr;    // last D2H of a call (deferred like ring_done)
     bool stage_pending = false;
     cudaEvent_t stage_pre_ev = nullptr;  // one GPU: the next episode's sub-part 0, prefetched into slot 0

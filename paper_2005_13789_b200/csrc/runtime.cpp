@@ -947,6 +947,12 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
             if (sp.count) { c->launches += 1; tp.launches += 1; }
             tp.timed.push_back({e0, e1});
             tp.samples += sp.count;
+            if (P == 1 && c->export_now) {  // sub-part t is final for this call: copy it out now
+                const uint64_t rb = c->sub_bounds[vs], rows = c->sub_bounds[vs + 1] - rb;
+                NE_CUDA(c, cudaStreamWaitEvent(c->d2h_stream, e1, 0));
+                NE_CUDA(c, cudaMemcpyAsync(c->export_V + (rb - c->part_bounds[c->rank]) * d, V, rows * d * sizeof(float),
+                                           cudaMemcpyDeviceToHost, c->d2h_stream));
+            }
             if (P > 1 && ipc) {  // copy-engine push into rank + 1 (ring_ipc.cpp)
                 const uint64_t send_rows = c->sub_bounds[vs + 1] - c->sub_bounds[vs];
                 NE_TRY(ipc_push(c, t, V, send_rows * d * elem_bytes(c), e1, ring_kind(P, G, r), ring_dest(P, G, r, g),
@@ -1505,10 +1511,22 @@ int ne_train_epoch(ne_ctx* c, uint32_t epoch, float lr, uint32_t flags, ne_stats
     ne_stats acc;
     std::memset(&acc, 0, sizeof acc);
     const uint32_t l0 = c->launches;
+    if (c->export_V) {
+        const uint64_t need = (c->part_bounds[c->rank + 1] - c->part_bounds[c->rank]) * c->cfg.dim;
+        if (c->export_cap < need)
+            return ne_fail(c, NE_ERANGE, "export buffer %zu floats < %llu (part rows x d)", c->export_cap,
+                           (unsigned long long)need);
+    }
+    // the vertex export (ne_export_vertex_on_train) rides on the call's last episode
+    struct ExportGuard {
+        ne_ctx* c;
+        ~ExportGuard() { c->export_now = false; }
+    } export_guard{c};
     if (flags & NE_REUSE_SAMPLES) {
         if (c->cfg.episodes != 1 || c->built_episode != 0)
             return ne_fail(c, NE_ESTATE, "NE_REUSE_SAMPLES needs episodes == 1 and a built pool");
         c->next.valid = false;
+        c->export_now = c->export_V != nullptr;
         NE_TRY(do_train(c, epoch, 0, lr, &acc));
     } else {
         // Walk engine decoupled from training ("we run our walk engine for
@@ -1543,6 +1561,7 @@ int ne_train_epoch(ne_ctx* c, uint32_t epoch, float lr, uint32_t flags, ne_stats
             const bool pre = more && pipelined(c);
             TrainPending tp;
             c->sgns_reserve = pre ? build_reserve : 0;
+            c->export_now = c->export_V != nullptr && e + 1 == E;
             int rc = launch_train(c, epoch, e, lr, tp);
             c->sgns_reserve = 0;
             if (rc == NE_OK && pre) rc = prebuild_next(c, e + 1 < E ? epoch : epoch + 1, e + 1 < E ? e + 1 : 0);
@@ -1555,8 +1574,30 @@ int ne_train_epoch(ne_ctx* c, uint32_t epoch, float lr, uint32_t flags, ne_stats
             c->ev_used = 0;
         }
     }
+    if (c->export_V) NE_CUDA(c, cudaStreamSynchronize(c->d2h_stream));  // host rows complete on return
     acc.kernel_launches = c->launches - l0;
     if (stats) *stats = acc;
+    return NE_OK;
+}
+
+int ne_export_vertex_on_train(ne_ctx* c, float* host_rows, size_t cap_floats) {
+    NE_TRY(enter(c));
+    if (!host_rows) {
+        c->export_V = nullptr;
+        c->export_cap = 0;
+        return NE_OK;
+    }
+    if (c->world != 1) return ne_fail(c, NE_EINVAL, "vertex export during training needs world == 1 (world=%d)", c->world);
+    if (c->cfg.storage != NE_STORE_F32) return ne_fail(c, NE_EINVAL, "vertex export during training needs fp32 rows");
+    if (c->cfg.staging != NE_STAGE_DEVICE) return ne_fail(c, NE_EINVAL, "vertex export during training needs device staging");
+    if (c->loaded) {
+        const uint64_t need = (c->part_bounds[c->rank + 1] - c->part_bounds[c->rank]) * c->cfg.dim;
+        if (cap_floats < need)
+            return ne_fail(c, NE_ERANGE, "export buffer %zu floats < %llu (part rows x d)", cap_floats,
+                           (unsigned long long)need);
+    }
+    c->export_V = host_rows;
+    c->export_cap = cap_floats;
     return NE_OK;
 }
 

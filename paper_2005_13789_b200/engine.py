@@ -92,6 +92,13 @@ class Engine:
             ne.ne_get_embeddings(self.ctx, which, a, b, out)
         return out
 
+    def export_vertex_on_train(self, out) -> None:
+        """Every later train_epoch streams this rank's vertex rows into `out`
+        (float32 [part rows][d], pinned for the overlap) while it trains; None
+        turns it off.  The engine keeps a reference to `out`."""
+        ne.ne_export_vertex_on_train(self.ctx, out)
+        self._export = out
+
     def set_embeddings(self, which: int, row_begin: int, data: np.ndarray) -> None:
         data = np.ascontiguousarray(data, np.float32)
         ne.ne_set_embeddings(self.ctx, which, row_begin, row_begin + data.shape[0], data)

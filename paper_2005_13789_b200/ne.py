@@ -69,6 +69,7 @@ _sig = {
     "ne_train_samples": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_float, C.POINTER(ne_stats)]),
     "ne_train_epoch": (C.c_int, [_P, C.c_uint32, C.c_float, C.c_uint32, C.POINTER(ne_stats)]),
     "ne_get_embeddings": (C.c_int, [_P, C.c_int, C.c_uint32, C.c_uint32, _P, C.c_size_t]),
+    "ne_export_vertex_on_train": (C.c_int, [_P, _P, C.c_size_t]),
     "ne_set_embeddings": (C.c_int, [_P, C.c_int, C.c_uint32, C.c_uint32, _P]),
     "ne_last_error": (C.c_char_p, [_P]),
     "ne_destroy": (None, [_P]),
@@ -199,6 +200,15 @@ def ne_train_epoch(ctx, epoch: int, lr: float, flags: int = 0) -> ne_stats:
 def ne_get_embeddings(ctx, which: int, row_begin: int, row_end: int, out) -> None:
     cap = out.numel() if hasattr(out, "numel") else out.size
     _check(ctx, _lib.ne_get_embeddings(ctx, which, row_begin, row_end, _ptr(out, 4, "out (f32)"), cap))
+
+
+def ne_export_vertex_on_train(ctx, out) -> None:
+    """out: this rank's vertex rows (float32, part rows x d, pinned for the overlap), or None."""
+    if out is None:
+        _check(ctx, _lib.ne_export_vertex_on_train(ctx, None, 0))
+        return
+    cap = out.numel() if hasattr(out, "numel") else out.size
+    _check(ctx, _lib.ne_export_vertex_on_train(ctx, _ptr(out, 4, "out (f32)"), cap))
 
 
 def ne_set_embeddings(ctx, which: int, row_begin: int, row_end: int, data) -> None:

@@ -590,6 +590,46 @@ def test_host_staged_vertex_matrix_matches_oracle(subparts):
     assert dv <= TOL and dc <= TOL, (dv, dc)
 
 
+@pytest.mark.parametrize("subparts,episodes", [(1, 1), (4, 2), (7, 3)])
+def test_export_vertex_on_train(subparts, episodes):
+    """ne_export_vertex_on_train: every train_epoch copies each vertex sub-part
+    out as soon as its block of the last episode has trained; on return the
+    host rows equal ne_get_embeddings(NE_VERTEX), across reloads; None stops it."""
+    import torch
+    off, tgt = synth.rmat_graph(3000, 20000, 44)
+    eng = engine(dim=64, walk_len=10, window=3, subparts=subparts, episodes=episodes, deterministic=False)
+    eng.load_graph(off, tgt)
+    out = torch.full((3000, 64), float("nan"), dtype=torch.float32).pin_memory()
+    eng.export_vertex_on_train(out)
+    for ep in range(2):
+        eng.train_epoch(ep, 0.025)
+        assert np.array_equal(out.numpy(), eng.embeddings(0))
+    eng.load_graph(off, tgt)  # the registration survives a reload
+    eng.train_epoch(0, 0.025)
+    assert np.array_equal(out.numpy(), eng.embeddings(0))
+    eng.export_vertex_on_train(None)
+    before = out.numpy().copy()
+    eng.train_epoch(1, 0.025)
+    assert np.array_equal(out.numpy(), before)
+    eng.close()
+
+
+def test_export_vertex_on_train_rejects():
+    from paper_2005_13789_b200 import ne
+    off, tgt = synth.rmat_graph(3000, 20000, 44)
+    eng = engine(dim=64, walk_len=10, window=3)
+    eng.load_graph(off, tgt)
+    with pytest.raises(ne.NEError, match="NE_ERANGE"):
+        eng.export_vertex_on_train(np.zeros((2999, 64), np.float32))
+    eng.close()
+    for kw, msg in ((dict(storage=ne.NE_STORE_BF16), "fp32 rows"), (dict(staging=ne.NE_STAGE_HOST), "device staging"),
+                    (dict(rank=1, world=2), "world == 1")):
+        eng = engine(dim=64, walk_len=10, window=3, **kw)
+        with pytest.raises(ne.NEError, match=msg):
+            eng.export_vertex_on_train(np.zeros((3000, 64), np.float32))
+        eng.close()
+
+
 def test_host_staged_write_drops_prefetch():
     """A host write between epochs lands after the next episode's sub-part 0
     was prefetched: the write must win (the prefetch is dropped), so the run
