@@ -1518,9 +1518,12 @@ int ne_train_epoch(ne_ctx* c, uint32_t epoch, float lr, uint32_t flags, ne_stats
                            (unsigned long long)need);
     }
     // the vertex export (ne_export_vertex_on_train) rides on the call's last episode
-    struct ExportGuard {
+    struct ExportGuard {  // also on an error return: no copy into the caller's rows left in flight
         ne_ctx* c;
-        ~ExportGuard() { c->export_now = false; }
+        ~ExportGuard() {
+            if (c->export_now) cudaStreamSynchronize(c->d2h_stream);
+            c->export_now = false;
+        }
     } export_guard{c};
     if (flags & NE_REUSE_SAMPLES) {
         if (c->cfg.episodes != 1 || c->built_episode != 0)
