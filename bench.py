@@ -366,9 +366,9 @@ def main():
     h2d = off_h.numel() * 8 + tgt_h.numel() * 4
     a, b = eng.part
     emb_h = [torch.empty((b - a, w.dim), dtype=torch.float32).pin_memory() for _ in range(2)]
-    # one GPU, fp32 rows in HBM: the vertex rows stream out during the epoch's last
-    # episode (ne_export_vertex_on_train); otherwise they are read after it
-    export_v = world == 1 and esz == 4 and args.staging == "device"
+    # fp32 rows in HBM: the vertex rows stream out during the epoch (ne_export_vertex_on_train:
+    # one GPU, after the last episode's block; ring, on arrival home); otherwise read after it
+    export_v = esz == 4 and args.staging == "device"
     if export_v:
         ne.ne_export_vertex_on_train(eng.ctx, emb_h[0])
     barrier()
@@ -449,8 +449,8 @@ def main():
                     "d2h_bytes_per_step": d2h + 32 + episodes * (8 * (args.subparts * world + 1) + 16),
                     "step": "ne_load_graph (pinned host CSR) + ne_train_epoch + ne_get_embeddings of both "
                             "matrices (this rank's rows, to pinned host memory)"
-                            + ("; the vertex rows stream out during the epoch's last episode "
-                               "(ne_export_vertex_on_train)" if export_v else ""),
+                            + ("; the vertex rows stream out during the epoch as their sub-parts become "
+                               "final (ne_export_vertex_on_train)" if export_v else ""),
                     "phases_ms_per_step": {k: v / max(1, args.e2e_steps) for k, v in e_ph.items()}},
             "clocks": clk.summary(),
             "gpu_launches": int(tsum[3]),

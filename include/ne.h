@@ -289,16 +289,16 @@ int ne_get_embeddings(ne_ctx *ctx, int which, uint32_t row_begin, uint32_t row_e
 /* Stream this rank's trained vertex rows to host memory during training
  * (e2e; the paper's stage 2 "send vertex embeddings back"): from the
  * next ne_train_epoch on, every call copies vertex sub-part t to
- * host_rows[(row - part begin) * d ...] on a copy engine as soon as its block
- * of the call's last episode has trained -- overlapping the remaining
- * sub-parts' training -- and returns with the copies complete, host_rows
- * then equal to ne_get_embeddings(NE_VERTEX) of the whole part.  host_rows
- * should be pinned (page-locked) for the overlap; it stays registered across
- * ne_load_graph until replaced or turned off with NULL.
- * One GPU (world == 1; with the ring the sub-parts come home only at the
- * end), fp32 rows, device staging.  Errors: NE_EINVAL (world > 1, bf16
- * storage, host staging), NE_ERANGE (cap_floats < part rows x d, checked
- * here and at every ne_train_epoch). */
+ * host_rows[(row - part begin) * d ...] on a copy engine as soon as it is
+ * final -- one GPU: after its block of the call's last episode; with the ring:
+ * when it arrives home after the last round -- overlapping the remaining
+ * training, and returns with the copies complete, host_rows then equal to
+ * ne_get_embeddings(NE_VERTEX) of the whole part.  host_rows should be pinned
+ * (page-locked) for the overlap; it stays registered across ne_load_graph
+ * until replaced or turned off with NULL.  fp32 rows, device staging.
+ * Errors: NE_EINVAL (bf16 storage, host staging, a layout-only world > 1
+ * context), NE_ERANGE (cap_floats < part rows x d, checked here and at every
+ * ne_train_epoch). */
 int ne_export_vertex_on_train(ne_ctx *ctx, float *host_rows, size_t cap_floats);
 
 /* Overwrite rows [row_begin, row_end) of this rank's part (checkpoint resume,

@@ -166,6 +166,7 @@ int ipc_wait_arrival(ne_ctx* c, uint32_t t, uint32_t kind);  // compute stream w
 int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t after, uint32_t kind, uint32_t dest,
              uint32_t credit_to, uint32_t next_kind);
 int ipc_drain(ne_ctx* c, bool host_sync);            // every push into / out of this rank has landed
+int ipc_wait_home(ne_ctx* c, cudaStream_t s, uint32_t t, uint32_t kind);  // s waits for the last round's push into t
 void ipc_release(ne_ctx* c);
 
 // NVTX range for profilers (nsys / ncu --nvtx): walk, build, train, ring phases.

@@ -170,6 +170,11 @@ int ipc_push(ne_ctx* c, uint32_t t, const void* src, size_t bytes, cudaEvent_t a
     return NE_OK;
 }
 
+int ipc_wait_home(ne_ctx* c, cudaStream_t s, uint32_t t, uint32_t kind) {
+    // the push of this call's last round into slot t has landed (no arrival consumed)
+    return wait_ge(c, s, c->ipc.flags + arrived_idx(c, kind, t), c->ipc.pushed[kind][t]);
+}
+
 int ipc_drain(ne_ctx* c, bool host_sync) {
     if (!c->ipc.region || !c->ipc.connected) return NE_OK;
     const uint32_t k = c->cfg.subparts;

@@ -972,6 +972,15 @@ int launch_train(ne_ctx* c, uint32_t epoch, uint32_t episode, float lr, TrainPen
                 NE_CUDA(c, cudaEventRecord(rv, c->comm_stream));
                 recv[t] = rv;
             }
+            if (P > 1 && c->export_now && r + 1 == P) {  // sub-part t comes home final: copy it out on arrival
+                const uint32_t vs_home = (uint32_t)plan_vsub(P, G, k, P, t, g);
+                const uint64_t rb = c->sub_bounds[vs_home], rows = c->sub_bounds[vs_home + 1] - rb;
+                if (ipc) NE_TRY(ipc_wait_home(c, c->d2h_stream, t, ring_kind(P, G, r)));
+                else NE_CUDA(c, cudaStreamWaitEvent(c->d2h_stream, recv[t], 0));
+                NE_CUDA(c, cudaMemcpyAsync(c->export_V + (rb - c->part_bounds[c->rank]) * d,
+                                           c->vslot[(1 - c->cur) * k + t], rows * d * sizeof(float),
+                                           cudaMemcpyDeviceToHost, c->d2h_stream));
+            }
         }
         if (P > 1) c->cur = 1 - c->cur;
     }
@@ -1590,7 +1599,8 @@ int ne_export_vertex_on_train(ne_ctx* c, float* host_rows, size_t cap_floats) {
         c->export_cap = 0;
         return NE_OK;
     }
-    if (c->world != 1) return ne_fail(c, NE_EINVAL, "vertex export during training needs world == 1 (world=%d)", c->world);
+    if (c->world > 1 && !c->comm && !ipc_ring(c))
+        return ne_fail(c, NE_EINVAL, "vertex export during training needs a ring (NCCL or IPC; layout-only context)");
     if (c->cfg.storage != NE_STORE_F32) return ne_fail(c, NE_EINVAL, "vertex export during training needs fp32 rows");
     if (c->cfg.staging != NE_STAGE_DEVICE) return ne_fail(c, NE_EINVAL, "vertex export during training needs device staging");
     if (c->loaded) {

@@ -623,7 +623,7 @@ def test_export_vertex_on_train_rejects():
         eng.export_vertex_on_train(np.zeros((2999, 64), np.float32))
     eng.close()
     for kw, msg in ((dict(storage=ne.NE_STORE_BF16), "fp32 rows"), (dict(staging=ne.NE_STAGE_HOST), "device staging"),
-                    (dict(rank=1, world=2), "world == 1")):
+                    (dict(rank=1, world=2), "layout-only")):
         eng = engine(dim=64, walk_len=10, window=3, **kw)
         with pytest.raises(ne.NEError, match=msg):
             eng.export_vertex_on_train(np.zeros((3000, 64), np.float32))

@@ -47,12 +47,16 @@ def main():
     eng = Engine(deterministic=(mode == "det"), device=dev, rank=rank, world=world, nccl_id=None,
                  transport=ne.NE_TRANSPORT_IPC, **kw)
     eng.load_graph(off, tgt, all_gather=all_gather)
+    a, b = eng.part
+    exp = torch.full((b - a, kw["dim"]), float("nan")).pin_memory()  # rows streamed out on arrival home
+    eng.export_vertex_on_train(exp)
     stats = [eng.train_epoch(ep, 0.025) for ep in range(epochs)]
+    assert np.array_equal(exp.numpy(), eng.embeddings(0)), "exported vertex rows differ from ne_get_embeddings"
     if mode == "det":  # a reload of the same graph keeps the ring connected and restarts it
         eng.load_graph(off, tgt, all_gather=all_gather)
         stats = [eng.train_epoch(ep, 0.025) for ep in range(epochs)]
-    a, b = eng.part
     V, Cm = eng.embeddings(0), eng.embeddings(1)
+    assert np.array_equal(exp.numpy(), V), "exported vertex rows differ from ne_get_embeddings"
     parts = [None] * world
     dist.all_gather_object(parts, (a, b, V, Cm, stats))
     if rank == 0:

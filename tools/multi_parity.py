@@ -53,9 +53,15 @@ def main():
         return out
 
     eng.load_graph(off, tgt, all_gather=all_gather)
-    stats = [eng.train_epoch(ep, 0.025) for ep in range(epochs)]
     a, b = eng.part
+    # the vertex rows stream out as their sub-parts come home (fp32 rows in HBM)
+    exp = torch.full((b - a, 128), float("nan")).pin_memory() if kind not in ("staged", "bf16") else None
+    if exp is not None:
+        eng.export_vertex_on_train(exp)
+    stats = [eng.train_epoch(ep, 0.025) for ep in range(epochs)]
     V, Cm = eng.embeddings(0), eng.embeddings(1)
+    if exp is not None:
+        assert np.array_equal(exp.numpy(), V), "exported vertex rows differ from ne_get_embeddings"
     parts = [None] * world
     dist.all_gather_object(parts, (a, b, V, Cm, stats))
     if rank == 0:
