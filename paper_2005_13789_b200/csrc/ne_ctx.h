@@ -58,6 +58,8 @@ struct ne_ctx {
     cudaEvent_t stage_pre_ev = nullptr;  // one GPU: the next episode's sub-part 0, prefetched into slot 0
     bool stage_pre = false;
     uint32_t stage_base = 0;             // one GPU: sub-part t of this episode uses slot (t + base) % 3
+    uint32_t stage_pre_set = 0;          // with the ring: the slot set holding the prefetched window 0
+    uint32_t stage_drain_set = 1;        // (stage_pre), and the set the last window's rows drain from
     int cur = 0;                // half [cur*k, cur*k+k) holds the current sub-parts
     uint64_t max_sub_rows = 0;
 

@@ -833,6 +833,15 @@ int launch_train_staged_ring(ne_ctx* c, uint32_t epoch, uint32_t episode, float 
     const uint32_t nwin = (k + w - 1) / w;
     uint32_t cur = 0, nxt = 1, pre = 2;
     std::vector<cudaEvent_t> loaded(w, nullptr), drained(w, nullptr);
+    // window 0 prefetched during the previous episode's last window: it trains
+    // in that set; the previous last window's home set is still draining
+    const bool resumed = c->stage_pre;
+    if (resumed) {
+        cur = c->stage_pre_set;
+        pre = c->stage_drain_set;
+        nxt = 3 - cur - pre;
+    }
+    c->stage_pre = false;
     auto prefetch = [&](uint32_t win, uint32_t set) -> int {  // stage 5: H2D of the window's home sub-parts
         for (uint32_t t = 0; t < w && win * w + t < k; ++t) {
             if (drained[t]) NE_CUDA(c, cudaStreamWaitEvent(c->copy_stream, drained[t], 0));
@@ -845,12 +854,24 @@ int launch_train_staged_ring(ne_ctx* c, uint32_t epoch, uint32_t episode, float 
         }
         return NE_OK;
     };
-    NE_TRY(prefetch(0, cur));
+    if (resumed) std::fill(loaded.begin(), loaded.end(), c->stage_pre_ev);
+    else NE_TRY(prefetch(0, cur));
     std::vector<cudaEvent_t> recv(w, nullptr);
     for (uint32_t win = 0; win < nwin; ++win) {
         const uint32_t t0 = win * w, wn = std::min(w, k - t0);
         for (uint32_t t = 0; t < wn; ++t) recv[t] = loaded[t];
         if (win + 1 < nwin) NE_TRY(prefetch(win + 1, pre));  // overlaps this whole window
+        // the last window also overlaps the next episode's window 0: its rows
+        // came home and were copied back at the end of window 0 (ordered before
+        // the drain this prefetch waits for), so the next episode does not
+        // start behind a window's H2D.  Host writers (rows_op, load_graph)
+        // drop it.  One window per episode: no free set yet, no prefetch.
+        const bool ahead = win + 1 == nwin && nwin > 1;
+        if (ahead) {
+            NE_TRY(prefetch(0, pre));
+            if (!c->stage_pre_ev) NE_CUDA(c, cudaEventCreateWithFlags(&c->stage_pre_ev, cudaEventDisableTiming));
+            NE_CUDA(c, cudaEventRecord(c->stage_pre_ev, c->copy_stream));
+        }
         for (uint32_t r = 0; r < P; ++r) {
             for (uint32_t t = 0; t < wn; ++t) {
                 const uint32_t vs = (uint32_t)plan_vsub(P, G, k, r, t0 + t, g);
@@ -896,6 +917,11 @@ int launch_train_staged_ring(ne_ctx* c, uint32_t epoch, uint32_t episode, float 
         const uint32_t home = cur;
         cur = pre;
         pre = home;
+        if (ahead) {  // cur now holds the next episode's window 0, pre drains
+            c->stage_pre = true;
+            c->stage_pre_set = cur;
+            c->stage_drain_set = pre;
+        }
     }
     if (!c->stage_done) NE_CUDA(c, cudaEventCreateWithFlags(&c->stage_done, cudaEventDisableTiming));
     NE_CUDA(c, cudaEventRecord(c->stage_done, c->d2h_stream));  // after every receive it waited for
